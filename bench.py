@@ -1,0 +1,359 @@
+"""Benchmark of the DESSERT scoring hot path on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], "cfg1"): N = 100,000 sets, m_i =
+clip(round(N(70, 20)), 8, 180) (~7.0 M vectors), d = 128 fp16 unit vectors
+from a 4,096-centroid Gaussian mixture, L = 64 tables x C = 7 bits; 1,000
+query sets of m_q = 32; exhaustive scoring of every set; top-100.
+A step = hash the 32,000 query vectors (K1) + score every (query set, set)
+pair (K3) + top-100 per query set (K4), inputs resident in HBM.
+The index (7.0 M x 64 B plane records = 448 MB) exceeds the 126 MB L2, so no
+L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 1|3|4]
+
+Multi-GPU (torchrun): weak scaling -- every rank holds its own 100k-set shard
+(seeded per rank), all ranks score the same query sets, local top-k are
+all-gathered over NCCL and merged with the same (score desc, doc id asc) key.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "set-pair scores/sec (cfg1: 100k sets x 1000 query sets, L=64 C=7, exhaustive, top-100)"
+UNIT = "set-pairs/s"
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.gpu = gpu_index
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def _port_worker(args):
+    codes, off, qcodes, lut, sets = args
+    from oracle import dessert_oracle as O
+
+    r = 1 << 7 if codes.max() < 128 else 1 << 8
+    L = codes.shape[1]
+    tables = [O.build_tiny_table(codes[off[i]:off[i + 1]], L, r) for i in sets]
+    t0 = time.perf_counter()
+    out = []
+    for qc in qcodes:
+        out.append([O.score_port(t, qc, lut) for t in tables])
+    return time.perf_counter() - t0, len(qcodes) * len(sets)
+
+
+def cpu_port_rate(codes, off, qcodes, lut, n_sets_sample, threads):
+    """Reference algorithm (TinyTable collision keys + numpy mean, index.py:183-216)
+    on a fork pool of `threads` processes, each scoring a contiguous shard."""
+    import multiprocessing as mp
+
+    sets = np.arange(n_sets_sample)
+    shards = np.array_split(sets, threads)
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(threads) as pool:
+        res = pool.map(_port_worker, [(codes, off, qcodes, lut, s) for s in shards])
+    wall = time.perf_counter() - t0
+    pairs = sum(r[1] for r in res)
+    slowest = max(r[0] for r in res)
+    return pairs / slowest, pairs, slowest, wall
+
+
+def host_sample_codes(n_sets, L, C, seed, m_q=32, n_q=2):
+    """cfg1-shaped codes for a bounded sample, generated and hashed on the host
+    (numpy + oracle hash) so the reference arm touches no GPU code."""
+    from oracle import dessert_oracle as O
+    from paper_2210_15748_b200 import workloads
+
+    rng = np.random.default_rng(seed)
+    sizes = workloads.set_sizes(n_sets, 70, 20, seed)
+    off = workloads.offsets(sizes)
+    cents = rng.standard_normal((4096, 128))
+    cents /= np.linalg.norm(cents, axis=1, keepdims=True)
+    X = cents[rng.integers(0, 4096, size=int(off[-1]))] + 0.05 * rng.standard_normal((int(off[-1]), 128))
+    X = (X / np.linalg.norm(X, axis=1, keepdims=True)).astype(np.float16)
+    P = O.sample_planes(128, C, L, 0)
+    codes = O.hash_matrix(P, L, C, X.astype(np.float64))
+    qs = []
+    for _ in range(n_q):
+        s = int(rng.integers(0, n_sets))
+        rows = off[s] + rng.integers(0, sizes[s], size=m_q)
+        q = X[rows].astype(np.float64) + 0.1 * rng.standard_normal((m_q, 128))
+        qs.append(O.hash_matrix(P, L, C, q / np.linalg.norm(q, axis=1, keepdims=True)))
+    return codes, off, np.stack(qs), O.sim_lut(C, L)
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    n_sample = min(100_000, 250 * threads)
+    codes, off, qcodes, lut = host_sample_codes(n_sample, 64, 7, seed=1, n_q=8)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_port_rate(codes, off, qcodes[:1], lut, min(200, n_sample), threads)
+    for _ in range(args.steps):
+        rate, pairs, slowest, wall = cpu_port_rate(codes, off, qcodes, lut, n_sample, threads)
+        vals.append(rate)
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * 1e8 / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (cfg1-shaped sample, host-generated)",
+        "config": {"workload": "cfg1", "n_sets": 100_000, "n_qsets": 1000, "m_q": 32, "L": 64,
+                   "C": 7, "top_k": 100, "sample": f"{qcodes.shape[0]} query sets x {n_sample} sets"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{qcodes.shape[0]} query sets x {n_sample} sets per step, "
+                                   "fork pool, reference TinyTable algorithm (oracle port)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2210_15748_b200 as d
+    from paper_2210_15748_b200 import engine, workloads
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_sets, n_q, m_q, L, C, top_k = 100_000, 1000, 32, 64, 7, 100
+
+    # ---- setup (untimed): synthetic cfg1 shard, index build on the GPU
+    sizes = workloads.set_sizes(n_sets, 70, 20, seed=100 + rank)
+    off = workloads.offsets(sizes)
+    X, _ = workloads.gpu_mixture(int(off[-1]), 4096, 128, 0.05, seed=200 + rank,
+                                 dtype=torch.float16, device=dev)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
+    doc_ids = np.arange(n_sets, dtype=np.int64) + rank * n_sets
+    idx = d.build_from_vectors(X, sizes, doc_ids, cfg, keep_codes=(rank == 0))
+    Qv = workloads.gpu_queries(X, off, n_q, m_q, seed=300)      # same queries on every rank
+    Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
+    del X
+    torch.cuda.synchronize()
+
+    planes = idx.family.device_planes(d.lsh.default_mode(Q2.dtype), dev)
+    mode = d.lsh.default_mode(Q2.dtype)
+    stream = torch.cuda.current_stream()
+    ev = []
+
+    def step(timed_kernel=False):
+        _, qrecs, _ = engine.hash_vectors(Q2, planes, mode, L, C, want_codes=False,
+                                          check_zero=False)
+        if timed_kernel:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        scores, _ = engine.score_all(idx.records, idx.set_off, qrecs, m_q, L, C, idx.lut_dev)
+        if timed_kernel:
+            e1.record(stream)
+            ev.append((e0, e1))
+        out_s, out_i, _ = engine.topk(scores, top_k, ids=idx.doc_ids_dev)
+        if world > 1:
+            gs = [torch.empty_like(out_s) for _ in range(world)]
+            gi = [torch.empty_like(out_i) for _ in range(world)]
+            dist.all_gather(gs, out_s)
+            dist.all_gather(gi, out_i)
+            out_s, out_i, _ = engine.topk(torch.cat(gs, 1).contiguous(), top_k,
+                                          ids=torch.cat(gi, 1).contiguous())
+        return out_s, out_i
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # INT-pipe peak (microbenchmark, measured now on this GPU)
+    mb = engine.microbench_int()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(timed_kernel=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    pairs_per_step = n_q * n_sets * world
+    value = pairs_per_step / (ms * 1e-3)
+
+    # ---- e2e: public API, host (pinned) query vectors in, host results out
+    Qh = Qv.cpu().pin_memory()
+    for _ in range(2):
+        d.query_batch(idx, Qh.to(dev, non_blocking=True), top_k, return_tensors=True)
+    torch.cuda.synchronize()
+    e2e_steps = max(1, min(args.steps, 5))
+    te = time.perf_counter()
+    h2d = d2h = 0
+    for _ in range(e2e_steps):
+        Qd = Qh.to(dev, non_blocking=True)
+        s_, i_ = d.query_batch(idx, Qd, top_k, return_tensors=True)
+        if world > 1:
+            gs = [torch.empty_like(s_) for _ in range(world)]
+            gi = [torch.empty_like(i_) for _ in range(world)]
+            dist.all_gather(gs, s_)
+            dist.all_gather(gi, i_)
+            s_, i_, _ = engine.topk(torch.cat(gs, 1).contiguous(), top_k,
+                                    ids=torch.cat(gi, 1).contiguous())
+        hs, hi = s_.cpu(), i_.cpu()
+        h2d = Qh.numel() * Qh.element_size()
+        d2h = hs.numel() * 8 + hi.numel() * 8
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - te) / e2e_steps
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+
+    # ---- roofline of the dominant kernel (K3 scoring)
+    total_vec = int(off[-1])
+    compares = float(n_q) * m_q * L * total_vec                   # per launch
+    achieved = compares / (kern_ms * 1e-3)
+    p_int = mb["lop3_ops_per_s"] * 4.0                            # 4 byte-compares / lane-op
+    rec_bytes = total_vec * engine.record_words(L, C) * 4
+    roofline = {
+        "bound": "int", "unit": "Gcompare/s", "achieved": achieved / 1e9, "peak": p_int / 1e9,
+        "frac": achieved / p_int, "traffic": None,
+        "kernel": "score_all_kernel<7,2,1,8>", "kernel_ms": kern_ms,
+        "per_launch": {"compares": compares, "code_bytes": rec_bytes,
+                       "hbm_floor_ms": rec_bytes / 6456.2e9 * 1e3},
+        "peak_source": "measured on this GPU in-run: LOP3 lane-ops/s x 4 (dsrt_microbench_int)",
+        "int_microbench": mb,
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (cfg1-shaped, generated on GPU)",
+        "config": {"workload": "cfg1", "n_sets_per_gpu": n_sets, "n_qsets": n_q, "m_q": m_q,
+                   "L": L, "C": C, "top_k": top_k, "vectors_per_gpu": total_vec,
+                   "l2": "inputs larger than L2 (448 MB plane records), no flush",
+                   "parallelism": f"shard{world}" if world > 1 else "single"},
+        "query_sets_per_sec": n_q / (ms * 1e-3),
+        "e2e": {"value": pairs_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": 3 * args.steps + (1 if world > 1 else 0) * args.steps,
+        "roofline": roofline,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # bounded sample (~1.5 s per core): 8 query sets x 1000 sets per process
+        threads = len(os.sched_getaffinity(0))
+        n_sample = min(n_sets, 1000 * threads)
+        codes = idx.codes[: int(off[n_sample])].cpu().numpy().astype(np.int64)
+        qcd, _ = d.lsh.hash_device(idx.family, Q2[: 8 * m_q], want_records=False)
+        qc = qcd.cpu().numpy().astype(np.int64).reshape(8, m_q, L)
+        rate, pairs, slowest, wall = cpu_port_rate(codes, off[: n_sample + 1], qc,
+                                                   idx.lookup.table, n_sample, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"8 query sets x {n_sample} sets ({pairs} set-pairs, "
+                                          f"{slowest:.1f} s), reference TinyTable algorithm "
+                                          "(oracle port), fork pool"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

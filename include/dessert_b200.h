@@ -1,0 +1,157 @@
+/*
+ * dessert_b200 -- C ABI of the B200-native DESSERT vector-set search hot path.
+ *
+ * Every entry point takes plain device pointers (caller-owned, e.g. torch
+ * tensors' data_ptr()), sizes, and a cudaStream_t passed as void*.  Calls are
+ * asynchronous on that stream unless stated otherwise.  Return value: 0 on
+ * success, a DSRT_E* status otherwise; dsrt_last_error() returns a
+ * thread-local message whose prefix matches the reference's ValueError text
+ * ("invalid parameter", "dimension mismatch", ...), so a host shim can re-raise
+ * the reference's exception types unchanged.  No C++ exception crosses the ABI.
+ *
+ * The reference (/root/reference/pkg/src/dessert) is pure Python/numpy and has
+ * no FFI; each entry point below names the Python function it replaces.  The
+ * ctypes binding a maintainer would add to the reference is in INTEGRATION.md.
+ *
+ * Device data layout ("plane records"): a vector's L codes of C
+ * bits are stored bit-sliced -- W = ceil(L/32) words per bit plane, plane b of
+ * word w holds bit b of codes 32w..32w+31 -- in a record of
+ * R = dsrt_record_words(L, C) uint32 words (C*W rounded up to a multiple of 4,
+ * i.e. 16-byte aligned records).  A set is a contiguous run of records;
+ * set_off[N+1] (int64) gives the CSR boundaries.
+ */
+#ifndef DESSERT_B200_H
+#define DESSERT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum dsrt_status {
+    DSRT_OK = 0,
+    DSRT_EINVAL = 1,       /* bad argument -> ValueError                */
+    DSRT_ECUDA = 2,        /* CUDA runtime / launch error -> RuntimeError */
+    DSRT_EUNSUPPORTED = 3, /* shape outside what the kernels implement   */
+    DSRT_ERANGE = 4        /* index out of range -> IndexError           */
+};
+
+/* element types of vector inputs */
+enum dsrt_dtype { DSRT_F32 = 0, DSRT_F64 = 1, DSRT_F16 = 2, DSRT_BF16 = 3 };
+
+/* hashing arithmetic (K1) */
+enum dsrt_hash_mode {
+    DSRT_HASH_F64 = 0,      /* planes float64 (L*C, d); DFMA accumulation         */
+    DSRT_HASH_F32 = 1,      /* planes float32 (L*C, d); FFMA accumulation         */
+    DSRT_HASH_TC_F16 = 2,   /* tcgen05 kind::f16; planes fp16 (L*C, d), X fp16      */
+    DSRT_HASH_TC_BF16X2 = 3 /* tcgen05 kind::f16; planes bf16 hi/lo (2, L*C, d), X bf16 */
+};
+
+const char *dsrt_last_error(void);
+int dsrt_version(void);
+/* uint32 words per plane record for (L, C); 0 if out of range. */
+int dsrt_record_words(int L, int C);
+/* SM count etc. of the current device (host call, synchronous). */
+int dsrt_device_info(int *sm_count, int *cc_major, int *cc_minor, size_t *free_bytes);
+
+/*
+ * K1 -- replaces lsh.hash_matrix (lsh.py:90-106) and hash_vector (lsh.py:80-87).
+ * X: (n, d) row-major of x_dtype.  planes: per mode above.  Outputs (either may
+ * be NULL): codes (n, L) of width 1/2/4 bytes for C<=8/<=16/<=24, and plane
+ * records (n, R).  zero_rows (may be NULL): device uint32 counter incremented
+ * per all-zero row (the reference raises "zero vector").
+ */
+int dsrt_hash(const void *X, int x_dtype, int64_t n, int d, const void *planes, int mode, int L,
+              int C, void *codes_out, uint32_t *records_out, uint32_t *zero_rows, void *stream);
+
+/*
+ * K2 -- replaces the per-set build_tiny_table loop (index.py:142-145,
+ * sketch.py:51-80) by the device layout.
+ *   dsrt_codes_to_records: (n, L) codes of width code_bytes -> plane records;
+ *     bad_codes (may be NULL) counts codes >= 2^C ("code out of range").
+ *   dsrt_sizes_to_offsets: exclusive scan of set sizes -> set_off (N+1);
+ *     bad (may be NULL) counts sizes < 1 ("empty set") or > 65535 ("set too large").
+ *   dsrt_counting_sort: vectors tagged with set ids (any order) -> set_off (N+1)
+ *     and a stable permutation perm (n) grouping vectors by set (counting sort:
+ *     histogram, scan, scatter, per-set stabilisation).  workspace from
+ *     dsrt_counting_sort_workspace.
+ *   dsrt_gather_rows: dst[i] = src[perm[i]] for rows of row_bytes (multiple of 4).
+ */
+int dsrt_codes_to_records(const void *codes, int code_bytes, int64_t n, int L, int C,
+                          uint32_t *records_out, uint32_t *bad_codes, void *stream);
+int dsrt_sizes_to_offsets(const int64_t *sizes, int64_t n_sets, int64_t *set_off_out,
+                          uint32_t *bad, void *workspace, size_t workspace_bytes, void *stream);
+size_t dsrt_scan_workspace(int64_t n_sets);
+int dsrt_counting_sort(const int64_t *set_of_vec, int64_t n, int64_t n_sets, int64_t *set_off_out,
+                       int64_t *perm_out, void *workspace, size_t workspace_bytes, void *stream);
+size_t dsrt_counting_sort_workspace(int64_t n, int64_t n_sets);
+int dsrt_gather_rows(const void *src, int64_t row_bytes, const int64_t *perm, int64_t n, void *dst,
+                     void *stream);
+/*
+ * TinyTable export (replaces build_tiny_table, sketch.py:51-80, for one set of
+ * the device layout): offsets (L, 2^C + 1) and ids (L, m) as int32, with
+ * bucket (t, h) = ids[t, offsets[t,h]:offsets[t,h+1]] in ascending vector id
+ * (the reference's stable counting sort).  codes: (n_vec, L) of code_bytes.
+ */
+int dsrt_tinytable(const void *codes, int code_bytes, const int64_t *set_off, int64_t set, int L,
+                   int C, int32_t *offsets_out, int32_t *ids_out, void *stream);
+
+/*
+ * K3 -- replaces _score_one/_score_chunk/score_candidate (index.py:183-261) for
+ * sigma = max with default weights:
+ *   score = pairwise_sum_f64(lut[c_q], q < m_q) / m_q,
+ *   c_q   = max_j sum_t [code_q[t] == code_j[t]].
+ * lut: (L+1) float64 from build_sim_lookup (host-computed bytes).
+ *
+ * dsrt_score_all: every query set against sets [set_begin, set_end):
+ *   scores[q * ld + (s - set_begin)].
+ * dsrt_score_candidates: query set q against cand[q * cand_ld + e] for
+ *   e < n_cand[q] (n_cand may be NULL: all cand_ld; cand may be NULL: identity);
+ *   scores[q * cand_ld + e].
+ * maxcounts (may be NULL): uint16 c_q at [(q * ld_or_cand_ld + e) * m_q + qi].
+ * qrecords: (n_qsets, m_q, R) plane records of the query codes.
+ */
+int dsrt_score_all(const uint32_t *records, const int64_t *set_off, int64_t set_begin,
+                   int64_t set_end, const uint32_t *qrecords, int64_t n_qsets, int m_q, int L,
+                   int C, const double *lut, double *scores, int64_t ld, uint16_t *maxcounts,
+                   void *stream);
+int dsrt_score_candidates(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                          const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                          const uint32_t *qrecords, int64_t n_qsets, int m_q, int L, int C,
+                          const double *lut, double *scores, uint16_t *maxcounts, void *stream);
+
+/*
+ * K4 -- replaces heapq.nsmallest(top_k, ..., key=(-score, doc_id)) (index.py:314-319).
+ * Row r: scores[r * ld + i], i < n (n_valid[r] if given).  ids: doc id of
+ * element i -- shared (ids[i]) if ids_ld == 0, else ids[r * ids_ld + i]; NULL
+ * means id = i.  Outputs (k per row, padded with score -1 / id UINT64_MAX /
+ * pos -1 when fewer are valid): out_scores, out_ids, out_pos (element index).
+ */
+int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, int64_t ids_ld,
+              const int32_t *n_valid, int64_t n, int64_t n_rows, int k, double *out_scores,
+              uint64_t *out_ids, int64_t *out_pos, void *stream);
+int dsrt_topk_max_k(void);
+
+/*
+ * K5 -- replaces prefilter.filter_candidates (prefilter.py:111-144).
+ * Q: (n_qsets * m_q, d) float64 query vectors; centroids (k_c, d) float64.
+ * postings CSR: post_off (k_c + 1), post_docs (ascending doc indices).
+ * Output per query set: cand[q * k_filter + e] (count desc, index asc) and
+ * n_cand[q].  workspace from dsrt_prefilter_workspace.
+ */
+int dsrt_prefilter(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
+                   int64_t k_c, const int64_t *post_off, const int64_t *post_docs, int64_t n_docs,
+                   int probe, int k_filter, int64_t *cand, int32_t *n_cand, void *workspace,
+                   size_t workspace_bytes, void *stream);
+size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
+
+/* Microbenchmark of the INT pipe (LOP3 / POPC / IMNMX lane-ops per second);
+ * host call, synchronous.  Writes ops/s for {lop3, popc, imnmx, mixed}. */
+int dsrt_microbench_int(double *ops_per_s_out4, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DESSERT_B200_H */

@@ -1,0 +1,169 @@
+// K3 dispatch + C ABI (kernels in score_kernels.cuh, instantiated in score_inst_*.cu).
+#include "score_kernels.cuh"
+
+namespace dsrt {
+
+// ----------------------------------------------- m_q > 128: finalize pass
+__device__ double pw_rec(const double *a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pw_rec(a, n2), pw_rec(a + n2, n - n2));
+}
+
+// One thread per (row): LUT[maxcounts] -> numpy pairwise mean; a = per-thread
+// scratch in global memory (rows * m_q doubles).
+__global__ void finalize_kernel(const uint16_t *__restrict__ mc, int64_t rows, int m_q,
+                                const double *__restrict__ lut, double *__restrict__ scratch,
+                                double *__restrict__ scores, int64_t row_len, int64_t ld) {
+    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (r >= rows) return;
+    double *a = scratch + r * m_q;
+    for (int i = 0; i < m_q; ++i) a[i] = __ldg(lut + mc[r * m_q + i]);
+    const double sum = __dadd_rn(0.0, pw_rec(a, m_q));
+    scores[(r / row_len) * ld + (r % row_len)] = __ddiv_rn(sum, static_cast<double>(m_q));
+}
+
+
+extern template int run_w<1>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<2>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<3>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<4>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<5>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<6>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<7>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<8>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<9>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<10>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<11>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<12>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<13>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<14>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<15>(const ScoreArgs &, int, int, cudaStream_t);
+extern template int run_w<16>(const ScoreArgs &, int, int, cudaStream_t);
+
+static int run_k(const ScoreArgs &a, int C, int qpl, cudaStream_t st) {
+    const int W = plane_words(a.L);
+    if (C * W > 32) {  // keep query planes within a register budget
+        set_error("invalid parameter: C*ceil(L/32)=%d exceeds the kernel register budget (32)", C * W);
+        return DSRT_EUNSUPPORTED;
+    }
+    switch (C) {
+#define DSRT_CASE(k) \
+    case k: return run_w<k>(a, W, qpl, st);
+        DSRT_CASE(1) DSRT_CASE(2) DSRT_CASE(3) DSRT_CASE(4) DSRT_CASE(5) DSRT_CASE(6)
+        DSRT_CASE(7) DSRT_CASE(8) DSRT_CASE(9) DSRT_CASE(10) DSRT_CASE(11) DSRT_CASE(12)
+        DSRT_CASE(13) DSRT_CASE(14) DSRT_CASE(15) DSRT_CASE(16)
+#undef DSRT_CASE
+        default: break;
+    }
+    set_error("invalid parameter: C=%d unsupported by the scoring kernel (C <= 16)", C);
+    return DSRT_EUNSUPPORTED;
+}
+
+// m_q <= 128 runs in one pass; larger m_q runs 128-query slices writing
+// maxcounts, then finalize_kernel applies numpy's recursive pairwise sum.
+static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
+    DSRT_REQUIRE(a.m_q >= 1, DSRT_EINVAL, "empty query: need at least one query vector");
+    DSRT_REQUIRE(a.L >= 1 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", a.L, C);
+    if (a.n_qsets == 0) return DSRT_OK;
+    const int R = record_words(a.L, C);
+    if (a.m_q <= 128) {
+        const int qpl = (a.m_q + 31) / 32;
+        a.mc_stride = a.m_q;
+        a.mc_q0 = 0;
+        return run_k(a, C, qpl == 3 ? 4 : qpl, st);
+    }
+    const int64_t row_len = a.cand_mode ? a.cand_ld : (a.se - a.sb);
+    const int64_t rows = a.n_qsets * row_len;
+    if (rows == 0) return DSRT_OK;
+    // Each 128-query slice is a pseudo query set: query slice r of set q has
+    // records at qrecs + (q*m_q + 128*r)*R, which the kernel addresses as
+    // (qset*m_q_slice + qi)*R only when m_q_slice == m_q.  Run slices per query
+    // set with n_qsets = 1 to keep the addressing simple.
+    uint16_t *mc = a.mc;
+    uint16_t *own = nullptr;
+    if (mc == nullptr) {
+        DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&own), rows * a.m_q * sizeof(uint16_t), st));
+        mc = own;
+    }
+    double *scratch = nullptr;
+    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch), rows * a.m_q * sizeof(double), st));
+    int rc = DSRT_OK;
+    for (int64_t qs = 0; qs < a.n_qsets && rc == DSRT_OK; ++qs) {
+        for (int q0 = 0; q0 < a.m_q && rc == DSRT_OK; q0 += 128) {
+            ScoreArgs b = a;
+            b.n_qsets = 1;
+            b.m_q = min(128, a.m_q - q0);
+            b.qrecs = a.qrecs + (qs * a.m_q + q0) * static_cast<int64_t>(R);
+            b.scores = nullptr;
+            b.mc = mc + qs * row_len * a.m_q;
+            b.mc_stride = a.m_q;
+            b.mc_q0 = q0;
+            if (b.cand_mode && b.cand) b.cand = a.cand + qs * a.cand_ld;
+            if (b.cand_mode && b.n_cand) b.n_cand = a.n_cand + qs;
+            const int qpl = (b.m_q + 31) / 32;
+            rc = run_k(b, C, qpl == 3 ? 4 : qpl, st);
+        }
+    }
+    if (rc == DSRT_OK && a.scores != nullptr) {
+        const int64_t blocks = (rows + 127) / 128;
+        finalize_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(
+            mc, rows, a.m_q, a.lut, scratch, a.scores, row_len, a.cand_mode ? a.cand_ld : a.ld);
+        if (cudaGetLastError() != cudaSuccess) rc = DSRT_ECUDA;
+    }
+    cudaFreeAsync(scratch, st);
+    if (own) cudaFreeAsync(own, st);
+    return rc;
+}
+
+}  // namespace dsrt
+
+using namespace dsrt;
+
+extern "C" int dsrt_score_all(const uint32_t *records, const int64_t *set_off, int64_t set_begin,
+                              int64_t set_end, const uint32_t *qrecords, int64_t n_qsets, int m_q,
+                              int L, int C, const double *lut, double *scores, int64_t ld,
+                              uint16_t *maxcounts, void *stream) {
+    DSRT_REQUIRE(set_begin >= 0 && set_end >= set_begin, DSRT_EINVAL,
+                 "invalid parameter: set range [%lld, %lld)", (long long)set_begin,
+                 (long long)set_end);
+    DSRT_REQUIRE(ld >= set_end - set_begin, DSRT_EINVAL, "invalid parameter: ld < set count");
+    if (set_end == set_begin) return DSRT_OK;
+    ScoreArgs a{};
+    a.cand_mode = false;
+    a.recs = records; a.set_off = set_off; a.sb = set_begin; a.se = set_end;
+    a.n_sets = set_end; a.qrecs = qrecords; a.n_qsets = n_qsets; a.m_q = m_q; a.L = L;
+    a.lut = lut; a.scores = scores; a.ld = ld; a.mc = maxcounts;
+    return score_dispatch(a, C, as_stream(stream));
+}
+
+extern "C" int dsrt_score_candidates(const uint32_t *records, const int64_t *set_off,
+                                     int64_t n_sets, const int64_t *cand, const int32_t *n_cand,
+                                     int64_t cand_ld, const uint32_t *qrecords, int64_t n_qsets,
+                                     int m_q, int L, int C, const double *lut, double *scores,
+                                     uint16_t *maxcounts, void *stream) {
+    DSRT_REQUIRE(cand_ld >= 0, DSRT_EINVAL, "invalid parameter: cand_ld < 0");
+    if (cand_ld == 0) return DSRT_OK;
+    ScoreArgs a{};
+    a.cand_mode = true;
+    a.recs = records; a.set_off = set_off; a.n_sets = n_sets; a.cand = cand; a.n_cand = n_cand;
+    a.cand_ld = cand_ld; a.qrecs = qrecords; a.n_qsets = n_qsets; a.m_q = m_q; a.L = L;
+    a.lut = lut; a.scores = scores; a.ld = cand_ld; a.mc = maxcounts;
+    return score_dispatch(a, C, as_stream(stream));
+}

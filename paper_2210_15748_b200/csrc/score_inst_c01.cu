@@ -1,0 +1,6 @@
+// Explicit instantiation of the scoring kernels for C = 1.
+#include "score_kernels.cuh"
+
+namespace dsrt {
+template int run_w<1>(const ScoreArgs &, int, int, cudaStream_t);
+}  // namespace dsrt

@@ -1,0 +1,6 @@
+// Explicit instantiation of the scoring kernels for C = 12.
+#include "score_kernels.cuh"
+
+namespace dsrt {
+template int run_w<12>(const ScoreArgs &, int, int, cudaStream_t);
+}  // namespace dsrt

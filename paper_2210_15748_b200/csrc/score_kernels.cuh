@@ -1,0 +1,473 @@
+// K3 -- DESSERT set scoring (sigma = max, A = mean with default weights).
+//
+// Replaces the reference's per-candidate Python loop
+//   _score_chunk / _score_one / score_candidate   (index.py:183-261)
+// which sorts collision keys gathered from TinyTables (sketch.py:156-178).
+// The dense form computed here is the same integer count
+//   c_q = max_j sum_t [code_q[t] == code_j[t]]
+// (pinned by the reference's own tests: sketch.py oracle equivalence,
+// test_index.py:130-144), followed by the float64 LUT and numpy's pairwise
+// mean (index.py:216), reproduced bit-for-bit in warp_score() below.
+//
+// Compare arithmetic is bit-sliced: per 32 tables and C code bits, the
+// mismatch mask is OR_b (q_b XOR x_b) -- C LOP3 + 1 POPC per 32 table
+// compares -- and the running max of matches is a running min of mismatches.
+// Mapping: one warp = one query set, lane = query vector (so max_j needs no
+// cross-lane reduction); set vectors are read from shared memory with
+// broadcast LDS.128.
+#pragma once
+#include "common.cuh"
+
+namespace dsrt {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------ finalize
+// Per-lane running minima of mismatches -> set score (identical in all lanes).
+// Implements numpy pairwise_sum_DOUBLE for n <= 128 (one leaf: 8 strided
+// accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential remainder),
+// preceded by the reduction identity 0.0 and followed by / m_q (np.mean).
+template <int QPL>
+__device__ __forceinline__ double warp_score(const int (&rmin)[QPL], int L, int m_q,
+                                             const double *__restrict__ lut_s,
+                                             uint16_t *__restrict__ mc_row, int mc_q0) {
+    const int lane = threadIdx.x & 31;
+    double a[QPL];
+#pragma unroll
+    for (int s = 0; s < QPL; ++s) {
+        const int qi = lane + 32 * s;
+        const int c = L - rmin[s];
+        a[s] = (qi < m_q) ? lut_s[c] : 0.0;
+        if (mc_row != nullptr && qi < m_q) mc_row[mc_q0 + qi] = static_cast<uint16_t>(c);
+    }
+    double res;
+    if (m_q < 8) {
+        res = 0.0;
+        for (int i = 0; i < m_q; ++i) res = __dadd_rn(res, __shfl_sync(kFull, a[0], i));
+    } else {
+        const int n8 = m_q - (m_q & 7);
+        const int j = lane & 7;
+        double r = __shfl_sync(kFull, a[0], j);
+#pragma unroll
+        for (int ib = 1; ib < 4 * QPL; ++ib) {
+            const double v = __shfl_sync(kFull, a[ib >> 2], ((ib & 3) << 3) + j);
+            if (ib * 8 < n8) r = __dadd_rn(r, v);
+        }
+        r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 1));
+        r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 2));
+        r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 4));
+        res = r;
+        const int rem = m_q & 7;
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            const int i = n8 + t;  // < 32*QPL when t < rem
+            double v = 0.0;
+#pragma unroll
+            for (int s = 0; s < QPL; ++s) {
+                const double w = __shfl_sync(kFull, a[s], i & 31);
+                if ((i >> 5) == s) v = w;
+            }
+            if (t < rem) res = __dadd_rn(res, v);
+        }
+    }
+    res = __dadd_rn(0.0, res);
+    return __ddiv_rn(res, static_cast<double>(m_q));
+}
+
+// Mismatch count of one query (registers) vs one record (uint32 words).
+template <int K, int W>
+__device__ __forceinline__ int mismatches(const uint32_t (&q)[K * W], const uint32_t *x) {
+    int mm = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint32_t acc = q[w] ^ x[w];
+#pragma unroll
+        for (int b = 1; b < K; ++b) acc |= q[b * W + w] ^ x[b * W + w];
+        mm += __popc(acc);
+    }
+    return mm;
+}
+
+template <int K, int W, int QPL>
+__device__ __forceinline__ void load_queries(uint32_t (&q)[QPL][K * W],
+                                             const uint32_t *__restrict__ qrecs, int64_t qset,
+                                             int m_q, bool active) {
+    constexpr int R = ((K * W) + 3) & ~3;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 0; s < QPL; ++s) {
+        const int qi = lane + 32 * s;
+        const bool ok = active && qi < m_q;
+        const uint32_t *src = qrecs + (qset * m_q + (ok ? qi : 0)) * R;
+#pragma unroll
+        for (int i = 0; i < K * W; ++i) q[s][i] = ok ? __ldg(src + i) : 0u;
+    }
+}
+
+// Process vectors [0, nv) of a shared-memory record array.
+template <int K, int W, int QPL>
+__device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], int (&rmin)[QPL],
+                                             const uint32_t *xs, int nv) {
+    constexpr int R = ((K * W) + 3) & ~3;
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(xs);
+#pragma unroll 2
+    for (int i = 0; i < nv; ++i) {
+        uint4 xv[R / 4];
+#pragma unroll
+        for (int u = 0; u < R / 4; ++u) xv[u] = x4[i * (R / 4) + u];
+        const uint32_t *x = reinterpret_cast<const uint32_t *>(xv);
+#pragma unroll
+        for (int s = 0; s < QPL; ++s) rmin[s] = min(rmin[s], mismatches<K, W>(q[s], x));
+    }
+}
+
+// ------------------------------------------------------- exhaustive (shared)
+constexpr int kTileVec = 128;  // vectors per TMA bulk tile
+constexpr int kStages = 4;     // smem ring depth
+
+template <int K, int W>
+constexpr int tile_bytes() {
+    return kTileVec * (((K * W) + 3) & ~3) * 4;
+}
+
+// grid: (query-set groups of NW, set chunks).  One producer warp streams the
+// chunk's plane records through a kStages ring with cp.async.bulk (TMA);
+// NW consumer warps (one query set each) share every tile.
+template <int K, int W, int QPL, int NW>
+__global__ void __launch_bounds__((NW + 1) * 32)
+    score_all_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
+                     int64_t set_begin, int64_t set_end, const uint32_t *__restrict__ qrecs,
+                     int64_t n_qsets, int m_q, int L, const double *__restrict__ lut,
+                     double *__restrict__ scores, int64_t ld, uint16_t *__restrict__ maxcounts,
+                     int mc_stride, int mc_q0, int n_chunks) {
+    constexpr int R = ((K * W) + 3) & ~3;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t *tiles = reinterpret_cast<uint32_t *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * tile_bytes<K, W>());
+    uint64_t *empty = full + kStages;
+    double *lut_s = reinterpret_cast<double *>(empty + kStages);
+    __shared__ int64_t bounds[2];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int chunk = blockIdx.y;
+    if (threadIdx.x == 0) {
+        const int64_t nset = set_end - set_begin;
+        const int64_t v0 = __ldg(set_off + set_begin), v1 = __ldg(set_off + set_end);
+        const int64_t tv = v1 - v0;
+        const int64_t t_lo = v0 + (tv * chunk) / n_chunks;
+        const int64_t t_hi = v0 + (tv * (chunk + 1)) / n_chunks;
+        bounds[0] = chunk == 0 ? set_begin : set_begin + lower_bound_i64(set_off + set_begin, nset, t_lo);
+        bounds[1] = chunk == n_chunks - 1 ? set_end
+                                          : set_begin + lower_bound_i64(set_off + set_begin, nset, t_hi);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
+    __syncthreads();
+    const int64_t s_lo = bounds[0], s_hi = bounds[1];
+    if (s_lo >= s_hi) return;
+    const int64_t vbeg = __ldg(set_off + s_lo), vend = __ldg(set_off + s_hi);
+    const int64_t n_tiles = (vend - vbeg + kTileVec - 1) / kTileVec;
+
+    if (warp == NW) {  // ---------------- producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            for (int64_t t = 0; t < n_tiles; ++t) {
+                const int st = static_cast<int>(t % kStages);
+                const uint32_t n = static_cast<uint32_t>(t / kStages);
+                if (t >= kStages) mbar_wait(&empty[st], (n - 1) & 1);
+                const int64_t tv0 = vbeg + t * kTileVec;
+                const int64_t nvec = tmin<int64_t>(kTileVec, vend - tv0);
+                const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);
+                mbar_arrive_expect_tx(&full[st], bytes);
+                bulk_g2s_keep(tiles + st * (kTileVec * R), recs + tv0 * R, bytes, &full[st], pol);
+            }
+        }
+        return;
+    }
+
+    // -------------------------------------- consumers: one query set per warp
+    const int64_t qset = static_cast<int64_t>(blockIdx.x) * NW + warp;
+    const bool active = qset < n_qsets;
+    uint32_t q[QPL][K * W];
+    load_queries<K, W, QPL>(q, qrecs, active ? qset : 0, m_q, active);
+    int rmin[QPL];
+#pragma unroll
+    for (int s = 0; s < QPL; ++s) rmin[s] = L;
+
+    int64_t s = s_lo;
+    int64_t s_end_v = __ldg(set_off + s + 1);
+    int64_t v = vbeg;
+    auto finalize = [&]() {
+        if (active) {
+            uint16_t *mc_row =
+                maxcounts ? maxcounts + (qset * ld + (s - set_begin)) * mc_stride : nullptr;
+            const double sc = warp_score<QPL>(rmin, L, m_q, lut_s, mc_row, mc_q0);
+            if (scores != nullptr && lane == 0) scores[qset * ld + (s - set_begin)] = sc;
+        }
+#pragma unroll
+        for (int i = 0; i < QPL; ++i) rmin[i] = L;
+        ++s;
+        if (s < s_hi) s_end_v = __ldg(set_off + s + 1);
+    };
+
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        const int st = static_cast<int>(t % kStages);
+        mbar_wait(&full[st], static_cast<uint32_t>(t / kStages) & 1);
+        const uint32_t *tile = tiles + st * (kTileVec * R);
+        const int64_t tv0 = vbeg + t * kTileVec;
+        const int64_t tv1 = tmin<int64_t>(tv0 + kTileVec, vend);
+        while (v < tv1) {
+            const int64_t stop = min(s_end_v, tv1);
+            if (active && stop > v)
+                scan_vectors<K, W, QPL>(q, rmin, tile + (v - tv0) * R, static_cast<int>(stop - v));
+            v = stop;
+            while (s < s_hi && v == s_end_v) finalize();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    while (s < s_hi) finalize();  // trailing empty sets (validated away upstream)
+}
+
+// --------------------------------------------------------- candidate lists
+constexpr int kPieceBytes = 3072;  // per-warp staging piece
+constexpr int kBufs = 3;           // per-warp ring depth
+constexpr int kCandWarps = 8;
+
+template <int K, int W>
+constexpr int piece_vec() {
+    return kPieceBytes / ((((K * W) + 3) & ~3) * 4);
+}
+
+// One warp = (query set, run of candidate slots).  Each warp streams its
+// candidates' records through a private kBufs-deep ring filled by
+// cp.async.bulk issued from lane 0.
+template <int K, int W, int QPL>
+__global__ void __launch_bounds__(kCandWarps * 32)
+    score_cand_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
+                      int64_t n_sets, const int64_t *__restrict__ cand,
+                      const int32_t *__restrict__ n_cand, int64_t cand_ld,
+                      const uint32_t *__restrict__ qrecs, int64_t n_qsets, int m_q, int L,
+                      const double *__restrict__ lut, double *__restrict__ scores,
+                      uint16_t *__restrict__ maxcounts, int mc_stride, int mc_q0, int64_t run_len,
+                      int64_t runs_per_q) {
+    constexpr int R = ((K * W) + 3) & ~3;
+    constexpr int PV = piece_vec<K, W>();
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *bufs = reinterpret_cast<uint32_t *>(smem) + warp * (kBufs * PV * R);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kCandWarps * kBufs * kPieceBytes) + warp * kBufs;
+    double *lut_s = reinterpret_cast<double *>(
+        smem + kCandWarps * kBufs * kPieceBytes + kCandWarps * kBufs * sizeof(uint64_t));
+
+    if (lane == 0) {
+        for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
+    __syncthreads();
+
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kCandWarps + warp;
+    const int64_t qset = gw / runs_per_q;
+    if (qset >= n_qsets) return;
+    const int64_t nc = n_cand ? tmin<int64_t>(__ldg(n_cand + qset), cand_ld) : cand_ld;
+    const int64_t e_lo = (gw % runs_per_q) * run_len;
+    const int64_t e_hi = min(e_lo + run_len, nc);
+    if (e_lo >= e_hi) return;
+
+    uint32_t q[QPL][K * W];
+    load_queries<K, W, QPL>(q, qrecs, qset, m_q, true);
+    int rmin[QPL];
+#pragma unroll
+    for (int s = 0; s < QPL; ++s) rmin[s] = L;
+
+    auto set_of = [&](int64_t e) -> int64_t {
+        return cand ? __ldg(cand + qset * cand_ld + e) : e;
+    };
+    // producer iterator (lane-uniform state; lane 0 issues the copies)
+    int64_t pe = e_lo, ps = set_of(pe);
+    bool pvalid = ps >= 0 && ps < n_sets;
+    int64_t pv = pvalid ? __ldg(set_off + ps) : 0, pvend = pvalid ? __ldg(set_off + ps + 1) : 0;
+    int64_t issued = 0;
+    auto issue = [&]() {  // issue the next piece (pe, [pv, ..)) into buffer issued % kBufs
+        // skip finished / invalid candidates: they need no data but still a piece slot
+        const int b = static_cast<int>(issued % kBufs);
+        const int64_t nvec = pe < e_hi ? tmin<int64_t>(PV, pvend - pv) : 0;
+        if (lane == 0) {
+            const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);
+            fence_proxy_async_smem();
+            if (bytes > 0) {
+                mbar_arrive_expect_tx(&bars[b], bytes);
+                bulk_g2s(bufs + b * (PV * R), recs + pv * R, bytes, &bars[b]);
+            } else {
+                mbar_arrive(&bars[b]);
+            }
+        }
+        ++issued;
+        pv += nvec;
+        if (pe < e_hi && pv >= pvend) {  // advance to the next candidate
+            ++pe;
+            if (pe < e_hi) {
+                ps = set_of(pe);
+                pvalid = ps >= 0 && ps < n_sets;
+                pv = pvalid ? __ldg(set_off + ps) : 0;
+                pvend = pvalid ? __ldg(set_off + ps + 1) : 0;
+            }
+        }
+    };
+    // consumer iterator
+    int64_t ce = e_lo, cs = set_of(ce);
+    bool cvalid = cs >= 0 && cs < n_sets;
+    int64_t cv = cvalid ? __ldg(set_off + cs) : 0, cvend = cvalid ? __ldg(set_off + cs + 1) : 0;
+    int64_t consumed = 0;
+    for (int i = 0; i < kBufs; ++i) issue();
+    while (ce < e_hi) {
+        const int b = static_cast<int>(consumed % kBufs);
+        mbar_wait(&bars[b], static_cast<uint32_t>(consumed / kBufs) & 1);
+        const int64_t nvec = tmin<int64_t>(PV, cvend - cv);
+        if (nvec > 0) scan_vectors<K, W, QPL>(q, rmin, bufs + b * (PV * R), static_cast<int>(nvec));
+        ++consumed;
+        cv += nvec;
+        if (cv >= cvend) {  // candidate complete
+            const double sc = warp_score<QPL>(
+                rmin, L, m_q, lut_s,
+                maxcounts ? maxcounts + (qset * cand_ld + ce) * mc_stride : nullptr, mc_q0);
+            if (scores != nullptr && lane == 0)
+                scores[qset * cand_ld + ce] = cvalid ? sc : __longlong_as_double(0x7ff8000000000000ll);
+#pragma unroll
+            for (int i = 0; i < QPL; ++i) rmin[i] = L;
+            ++ce;
+            if (ce < e_hi) {
+                cs = set_of(ce);
+                cvalid = cs >= 0 && cs < n_sets;
+                cv = cvalid ? __ldg(set_off + cs) : 0;
+                cvend = cvalid ? __ldg(set_off + cs + 1) : 0;
+            }
+        }
+        __syncwarp();
+        issue();  // refill the buffer just consumed
+    }
+    // drain: wait for outstanding pieces so no bulk copy outlives the CTA
+    while (consumed < issued) {
+        const int b = static_cast<int>(consumed % kBufs);
+        mbar_wait(&bars[b], static_cast<uint32_t>(consumed / kBufs) & 1);
+        ++consumed;
+    }
+}
+
+// ------------------------------------------------------------- dispatch
+template <int K, int W, int QPL>
+static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, int64_t se,
+                      const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
+                      double *scores, int64_t ld, uint16_t *mc, int mc_stride, int mc_q0,
+                      cudaStream_t st) {
+    constexpr int NW = 8;
+    const size_t smem = kStages * tile_bytes<K, W>() + 2 * kStages * sizeof(uint64_t) +
+                        (L + 1) * sizeof(double);
+    auto kern = score_all_kernel<K, W, QPL, NW>;
+    DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t groups = (n_qsets + NW - 1) / NW;
+    int occ = 0;
+    DSRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NW + 1) * 32, smem));
+    occ = occ < 1 ? 1 : occ;
+    const int64_t nset = se - sb;
+    // ~8 waves of CTAs; each chunk keeps >= 64 sets so tile pipelines stay full
+    int64_t chunks = (8LL * sm_count() * occ + groups - 1) / groups;
+    chunks = tmax<int64_t>(1, tmin<int64_t>(chunks, (nset + 63) / 64));
+    chunks = tmin<int64_t>(chunks, 65535);
+    dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(chunks));
+    DSRT_REQUIRE(groups < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many query sets");
+    kern<<<grid, (NW + 1) * 32, smem, st>>>(recs, set_off, sb, se, qrecs, n_qsets, m_q, L, lut,
+                                           scores, ld, mc, mc_stride, mc_q0,
+                                           static_cast<int>(chunks));
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
+template <int K, int W, int QPL>
+static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_sets,
+                       const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                       const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
+                       double *scores, uint16_t *mc, int mc_stride, int mc_q0, cudaStream_t st) {
+    const size_t smem = kCandWarps * kBufs * kPieceBytes + kCandWarps * kBufs * sizeof(uint64_t) +
+                        (L + 1) * sizeof(double);
+    auto kern = score_cand_kernel<K, W, QPL>;
+    DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    DSRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCandWarps * 32, smem));
+    occ = occ < 1 ? 1 : occ;
+    // enough warps for ~4 waves, but runs of >= 4 candidates
+    const int64_t want_warps = 4LL * sm_count() * occ * kCandWarps;
+    int64_t runs = (want_warps + n_qsets - 1) / n_qsets;
+    runs = tmax<int64_t>(1, tmin<int64_t>(runs, (cand_ld + 3) / 4));
+    const int64_t run_len = (cand_ld + runs - 1) / runs;
+    runs = (cand_ld + run_len - 1) / run_len;
+    const int64_t warps = n_qsets * runs;
+    const int64_t blocks = (warps + kCandWarps - 1) / kCandWarps;
+    DSRT_REQUIRE(blocks < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: grid too large");
+    kern<<<static_cast<unsigned>(blocks), kCandWarps * 32, smem, st>>>(
+        recs, set_off, n_sets, cand, n_cand, cand_ld, qrecs, n_qsets, m_q, L, lut, scores, mc,
+        mc_stride, mc_q0, run_len, runs);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
+// Dispatch on (C, W, QPL) template instances.
+struct ScoreArgs {
+    bool cand_mode;
+    const uint32_t *recs;
+    const int64_t *set_off;
+    int64_t sb, se, n_sets;
+    const int64_t *cand;
+    const int32_t *n_cand;
+    int64_t cand_ld;
+    const uint32_t *qrecs;
+    int64_t n_qsets;
+    int m_q, L;
+    const double *lut;
+    double *scores;
+    int64_t ld;
+    uint16_t *mc;
+    int mc_stride, mc_q0;
+};
+
+template <int K, int W, int QPL>
+static int run_one(const ScoreArgs &a, cudaStream_t st) {
+    if (a.cand_mode)
+        return launch_cand<K, W, QPL>(a.recs, a.set_off, a.n_sets, a.cand, a.n_cand, a.cand_ld,
+                                      a.qrecs, a.n_qsets, a.m_q, a.L, a.lut, a.scores, a.mc,
+                                      a.mc_stride, a.mc_q0, st);
+    return launch_all<K, W, QPL>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q, a.L,
+                                 a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+}
+
+template <int K, int W>
+static int run_qpl(const ScoreArgs &a, int qpl, cudaStream_t st) {
+    switch (qpl) {
+        case 1: return run_one<K, W, 1>(a, st);
+        case 2: return run_one<K, W, 2>(a, st);
+        default: return run_one<K, W, 4>(a, st);
+    }
+}
+
+template <int K>
+int run_w(const ScoreArgs &a, int W, int qpl, cudaStream_t st) {
+    switch (W) {
+        case 1: return run_qpl<K, 1>(a, qpl, st);
+        case 2: return run_qpl<K, 2>(a, qpl, st);
+        case 3: return run_qpl<K, 3>(a, qpl, st);
+        case 4: return run_qpl<K, 4>(a, qpl, st);
+        default: break;
+    }
+    set_error("invalid parameter: L=%d unsupported by the scoring kernel (L <= 128)", a.L);
+    return DSRT_EUNSUPPORTED;
+}
+
+
+template <int K>
+int run_w(const ScoreArgs &a, int W, int qpl, cudaStream_t st);
+}  // namespace dsrt

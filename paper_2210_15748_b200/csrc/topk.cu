@@ -1,0 +1,235 @@
+// K4 -- batched top-k by (score desc, doc_id asc).
+//
+// Replaces heapq.nsmallest(top_k, ((score, doc_id) ...), key=lambda e:
+// (-e[0], e[1])) in query() (index.py:314-319).  One CTA per row (query set):
+//  1. MSB radix select (8-bit digits) on the float64 bit pattern (scores are
+//     >= 0, so the IEEE pattern is monotone) -> threshold prefix T and the
+//     number of T-ties still needed;
+//  2. if more ties than needed: radix select on doc_id (ascending) among the
+//     ties (reference tie-break: lower doc id first);
+//  3. compact the k winners into shared memory and bitonic-sort them by
+//     (score desc, doc_id asc).
+#include "common.cuh"
+
+namespace dsrt {
+
+constexpr int kTopkThreads = 1024;
+constexpr int kTopkMax = 4096;
+
+struct RowView {
+    const double *s;
+    const uint64_t *ids;
+    int64_t row, ids_ld;
+    __device__ __forceinline__ uint64_t key(int64_t i) const {
+        return static_cast<uint64_t>(__double_as_longlong(__ldg(s + i)));
+    }
+    __device__ __forceinline__ uint64_t id(int64_t i) const {
+        if (ids == nullptr) return static_cast<uint64_t>(i);
+        return ids_ld ? __ldg(ids + row * ids_ld + i) : __ldg(ids + i);
+    }
+};
+
+// Block-wide MSB radix select.  Among elements with pred(i), find the value
+// prefix such that exactly `need` elements are >= (descending) or <=
+// (ascending) it, counting ties into the last bin.  Returns (prefix, mask,
+// remaining) through shared memory.
+template <bool DESC, typename KeyF, typename PredF>
+__device__ void radix_select(int64_t n, int64_t need, KeyF keyf, PredF pred, uint32_t *hist,
+                             uint64_t *out_prefix, uint64_t *out_mask, int64_t *out_rem) {
+    __shared__ uint64_t s_prefix, s_mask;
+    __shared__ int64_t s_rem;
+    __shared__ int s_done;
+    if (threadIdx.x == 0) {
+        s_prefix = 0;
+        s_mask = 0;
+        s_rem = need;
+        s_done = 0;
+    }
+    __syncthreads();
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix, mask = s_mask;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            if (!pred(i)) continue;
+            const uint64_t k = keyf(i);
+            if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t rem = s_rem, cum = 0;
+            int sel = DESC ? 0 : 255;
+            for (int t = 0; t < 256; ++t) {
+                const int dgt = DESC ? 255 - t : t;
+                const int64_t h = hist[dgt];
+                if (cum + h >= rem) {
+                    sel = dgt;
+                    break;
+                }
+                cum += h;
+            }
+            s_rem = rem - cum;
+            s_prefix = prefix | (static_cast<uint64_t>(sel) << shift);
+            s_mask = mask | (255ull << shift);
+            if (static_cast<int64_t>(hist[sel]) == s_rem) s_done = 1;  // take the whole bin
+        }
+        __syncthreads();
+        if (s_done) break;
+    }
+    if (threadIdx.x == 0) {
+        *out_prefix = s_prefix;
+        *out_mask = s_mask;
+        *out_rem = s_rem;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ bool before(uint64_t ka, uint64_t ia, uint64_t kb, uint64_t ib) {
+    // (score desc, id asc)
+    return ka > kb || (ka == kb && ia < ib);
+}
+
+__global__ void __launch_bounds__(kTopkThreads)
+    topk_kernel(const double *__restrict__ scores, int64_t ld, const uint64_t *__restrict__ ids,
+                int64_t ids_ld, const int32_t *__restrict__ n_valid, int64_t n, int k,
+                double *__restrict__ out_s, uint64_t *__restrict__ out_id,
+                int64_t *__restrict__ out_pos) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t *bkey = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *bid = bkey + kTopkMax;
+    int64_t *bpos = reinterpret_cast<int64_t *>(bid + kTopkMax);
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t t_prefix, t_mask, i_prefix, i_mask;
+    __shared__ int64_t t_rem, i_rem;
+    __shared__ int cnt;
+
+    const int64_t row = blockIdx.x;
+    RowView rv{scores + row * ld, ids, row, ids_ld};
+    int64_t nr = n;
+    if (n_valid) nr = tmin<int64_t>(n, tmax<int64_t>(0, __ldg(n_valid + row)));
+    const int64_t kk = tmin<int64_t>(k, nr);
+
+    bool use_id_filter = false;
+    if (kk > 0 && kk < nr) {
+        radix_select<true>(
+            nr, kk, [&](int64_t i) { return rv.key(i); }, [](int64_t) { return true; }, hist,
+            &t_prefix, &t_mask, &t_rem);
+        // how many elements tie with the threshold bin?
+        if (threadIdx.x == 0) cnt = 0;
+        __syncthreads();
+        const uint64_t tp = t_prefix, tm = t_mask;
+        int local = 0;
+        for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) local += ((rv.key(i) & tm) == tp);
+        atomicAdd(&cnt, local);
+        __syncthreads();
+        if (cnt > t_rem) {
+            use_id_filter = true;
+            radix_select<false>(
+                nr, t_rem, [&](int64_t i) { return rv.id(i); },
+                [&](int64_t i) { return (rv.key(i) & tm) == tp; }, hist, &i_prefix, &i_mask,
+                &i_rem);
+        }
+    } else if (threadIdx.x == 0) {
+        t_prefix = 0;
+        t_mask = 0;  // everything matches (key & 0) == 0 -> take all
+        t_rem = nr;
+    }
+    __syncthreads();
+    // collect winners
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const uint64_t tp = t_prefix, tm = t_mask, ip = i_prefix, im = i_mask;
+    if (kk > 0) {
+        for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) {
+            const uint64_t key = rv.key(i);
+            const uint64_t km = key & tm;
+            bool take = km > tp;
+            if (km == tp) {
+                if (!use_id_filter) {
+                    take = true;
+                } else {
+                    const uint64_t idm = rv.id(i) & im;
+                    take = idm <= ip;
+                }
+            }
+            if (take) {
+                const int slot = atomicAdd(&cnt, 1);
+                if (slot < kTopkMax) {
+                    bkey[slot] = key;
+                    bid[slot] = rv.id(i);
+                    bpos[slot] = i;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int m = tmin<int64_t>(cnt, kTopkMax);
+    int p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    for (int i = m + threadIdx.x; i < p2; i += blockDim.x) {  // sentinels sort last
+        bkey[i] = 0;
+        bid[i] = ~0ull;
+        bpos[i] = -1;
+    }
+    __syncthreads();
+    // bitonic sort, "before" order; sentinel pos -1 forced last
+    for (int size = 2; size <= p2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const bool vi = bpos[i] >= 0, vj = bpos[j] >= 0;
+                    bool i_first;
+                    if (vi != vj)
+                        i_first = vi;
+                    else
+                        i_first = before(bkey[i], bid[i], bkey[j], bid[j]);
+                    if (i_first != up) {
+                        const uint64_t tk = bkey[i], ti = bid[i];
+                        const int64_t tpz = bpos[i];
+                        bkey[i] = bkey[j]; bid[i] = bid[j]; bpos[i] = bpos[j];
+                        bkey[j] = tk; bid[j] = ti; bpos[j] = tpz;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const int64_t o = row * static_cast<int64_t>(k) + i;
+        if (i < m) {
+            if (out_s) out_s[o] = __longlong_as_double(static_cast<long long>(bkey[i]));
+            if (out_id) out_id[o] = bid[i];
+            if (out_pos) out_pos[o] = bpos[i];
+        } else {
+            if (out_s) out_s[o] = -1.0;
+            if (out_id) out_id[o] = ~0ull;
+            if (out_pos) out_pos[o] = -1;
+        }
+    }
+}
+
+}  // namespace dsrt
+
+using namespace dsrt;
+
+extern "C" int dsrt_topk_max_k(void) { return kTopkMax; }
+
+extern "C" int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, int64_t ids_ld,
+                         const int32_t *n_valid, int64_t n, int64_t n_rows, int k,
+                         double *out_scores, uint64_t *out_ids, int64_t *out_pos, void *stream) {
+    DSRT_REQUIRE(k >= 1, DSRT_EINVAL, "invalid parameter: top_k must be >= 1, got %d", k);
+    DSRT_REQUIRE(k <= kTopkMax, DSRT_EUNSUPPORTED,
+                 "invalid parameter: top_k=%d exceeds the device top-k limit %d", k, kTopkMax);
+    DSRT_REQUIRE(n >= 0 && ld >= n, DSRT_EINVAL, "invalid parameter: n=%lld ld=%lld",
+                 (long long)n, (long long)ld);
+    if (n_rows == 0) return DSRT_OK;
+    DSRT_REQUIRE(n_rows < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many rows");
+    const size_t smem = kTopkMax * (2 * sizeof(uint64_t) + sizeof(int64_t));
+    DSRT_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    topk_kernel<<<static_cast<unsigned>(n_rows), kTopkThreads, smem, as_stream(stream)>>>(
+        scores, ld, ids, ids_ld, n_valid, n, k, out_scores, out_ids, out_pos);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}

@@ -1,0 +1,227 @@
+"""Thin typed wrappers over the C ABI, taking torch CUDA tensors as buffers.
+
+Each function checks shapes/dtypes/devices, passes ``data_ptr()`` and the
+current CUDA stream to the library, and returns freshly allocated output
+tensors.  torch is used only for device memory and streams; every
+computation happens in the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_DT = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.float16: _lib.F16,
+       torch.bfloat16: _lib.BF16}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _need(t, dtype, name):
+    if not t.is_cuda:
+        raise ValueError(f"invalid parameter: {name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"invalid parameter: {name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"invalid parameter: {name} must be contiguous")
+
+
+def code_dtype(C: int):
+    return torch.uint8 if C <= 8 else (torch.int16 if C <= 16 else torch.int32)
+
+
+def code_bytes(C: int) -> int:
+    return 1 if C <= 8 else (2 if C <= 16 else 4)
+
+
+def record_words(L: int, C: int) -> int:
+    r = _lib.lib().dsrt_record_words(L, C)
+    if r <= 0:
+        raise ValueError(f"invalid parameter: L={L} C={C}")
+    return r
+
+
+def device_info():
+    sms, ma, mi, fr = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+    _lib.call("dsrt_device_info", ctypes.byref(sms), ctypes.byref(ma), ctypes.byref(mi),
+              ctypes.byref(fr))
+    return {"sm_count": sms.value, "cc": (ma.value, mi.value), "free_bytes": fr.value}
+
+
+# ------------------------------------------------------------------- K1
+def hash_vectors(X: torch.Tensor, planes: torch.Tensor, mode: int, L: int, C: int,
+                 want_codes: bool = True, want_records: bool = True, check_zero: bool = True):
+    """X (n, d) CUDA tensor -> (codes (n, L) or None, records (n, R) or None, n_zero_rows)."""
+    if X.dim() != 2:
+        raise ValueError(f"dimension mismatch: expected (n, d) matrix, got shape {tuple(X.shape)}")
+    if X.dtype not in _DT:
+        raise ValueError(f"invalid parameter: unsupported vector dtype {X.dtype}")
+    X = X.contiguous()
+    n, d = X.shape
+    codes = torch.empty((n, L), dtype=code_dtype(C), device=X.device) if want_codes else None
+    recs = (torch.empty((n, record_words(L, C)), dtype=torch.int32, device=X.device)
+            if want_records else None)
+    zero = torch.zeros(1, dtype=torch.int32, device=X.device) if check_zero else None
+    _lib.call("dsrt_hash", _ptr(X), _DT[X.dtype], n, d, _ptr(planes), mode, L, C, _ptr(codes),
+              _ptr(recs), _ptr(zero), _stream())
+    return codes, recs, zero
+
+
+# ------------------------------------------------------------------- K2
+def codes_to_records(codes: torch.Tensor, L: int, C: int, check: bool = True):
+    if codes.dim() != 2 or codes.shape[1] != L:
+        raise ValueError(f"expected (m, {L}) code matrix, got shape {tuple(codes.shape)}")
+    codes = codes.contiguous()
+    cb = codes.element_size()
+    n = codes.shape[0]
+    recs = torch.empty((n, record_words(L, C)), dtype=torch.int32, device=codes.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=codes.device) if check else None
+    _lib.call("dsrt_codes_to_records", _ptr(codes), cb, n, L, C, _ptr(recs), _ptr(bad), _stream())
+    return recs, bad
+
+
+def sizes_to_offsets(sizes: torch.Tensor):
+    _need(sizes, torch.int64, "sizes")
+    n = sizes.shape[0]
+    out = torch.empty(n + 1, dtype=torch.int64, device=sizes.device)
+    ws_bytes = _lib.lib().dsrt_scan_workspace(n)
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=sizes.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=sizes.device)
+    _lib.call("dsrt_sizes_to_offsets", _ptr(sizes), n, _ptr(out), _ptr(bad), _ptr(ws), ws_bytes,
+              _stream())
+    return out, bad
+
+
+def counting_sort(set_of_vec: torch.Tensor, n_sets: int):
+    """Vectors tagged by set id -> (set_off (N+1), stable perm (n))."""
+    _need(set_of_vec, torch.int64, "set_of_vec")
+    n = set_of_vec.shape[0]
+    set_off = torch.empty(n_sets + 1, dtype=torch.int64, device=set_of_vec.device)
+    perm = torch.empty(n, dtype=torch.int64, device=set_of_vec.device)
+    ws_bytes = _lib.lib().dsrt_counting_sort_workspace(n, n_sets)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=set_of_vec.device)
+    _lib.call("dsrt_counting_sort", _ptr(set_of_vec), n, n_sets, _ptr(set_off), _ptr(perm),
+              _ptr(ws), ws_bytes, _stream())
+    return set_off, perm
+
+
+def gather_rows(src: torch.Tensor, perm: torch.Tensor):
+    _need(perm, torch.int64, "perm")
+    src = src.contiguous()
+    row_bytes = src[0].numel() * src.element_size() if src.shape[0] else 4
+    dst = torch.empty((perm.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    _lib.call("dsrt_gather_rows", _ptr(src), row_bytes, _ptr(perm), perm.shape[0], _ptr(dst),
+              _stream())
+    return dst
+
+
+def tinytable(codes: torch.Tensor, set_off: torch.Tensor, s: int, m: int, L: int, C: int):
+    r = 1 << C
+    offsets = torch.empty((L, r + 1), dtype=torch.int32, device=codes.device)
+    ids = torch.empty((L, m), dtype=torch.int32, device=codes.device)
+    _lib.call("dsrt_tinytable", _ptr(codes), codes.element_size(), _ptr(set_off), s, L, C,
+              _ptr(offsets), _ptr(ids), _stream())
+    return offsets, ids
+
+
+# ------------------------------------------------------------------- K3
+def score_all(records, set_off, qrecords, m_q: int, L: int, C: int, lut, set_begin=0,
+              set_end=None, scores=None, ld=None, want_counts=False):
+    n_sets = set_off.shape[0] - 1
+    set_end = n_sets if set_end is None else set_end
+    n_q = qrecords.shape[0] // m_q if qrecords.dim() == 2 else qrecords.shape[0]
+    width = set_end - set_begin
+    if scores is None:
+        ld = width if ld is None else ld
+        scores = torch.empty((n_q, ld), dtype=torch.float64, device=records.device)
+    ld = scores.shape[1] if ld is None else ld
+    mc = (torch.empty((n_q, ld, m_q), dtype=torch.int16, device=records.device)
+          if want_counts else None)
+    _lib.call("dsrt_score_all", _ptr(records), _ptr(set_off), set_begin, set_end, _ptr(qrecords),
+              n_q, m_q, L, C, _ptr(lut), _ptr(scores), ld, _ptr(mc), _stream())
+    return scores, mc
+
+
+def score_candidates(records, set_off, qrecords, m_q: int, L: int, C: int, lut, cand=None,
+                     n_cand=None, cand_ld=None, n_qsets=None, want_counts=False):
+    n_sets = set_off.shape[0] - 1
+    n_q = n_qsets if n_qsets is not None else (qrecords.shape[0] // m_q)
+    if cand is not None:
+        _need(cand, torch.int64, "cand")
+        cand_ld = cand.shape[-1]
+    elif cand_ld is None:
+        cand_ld = n_sets
+    if n_cand is not None:
+        _need(n_cand, torch.int32, "n_cand")
+    scores = torch.empty((n_q, cand_ld), dtype=torch.float64, device=records.device)
+    mc = (torch.empty((n_q, cand_ld, m_q), dtype=torch.int16, device=records.device)
+          if want_counts else None)
+    _lib.call("dsrt_score_candidates", _ptr(records), _ptr(set_off), n_sets, _ptr(cand),
+              _ptr(n_cand), cand_ld, _ptr(qrecords), n_q, m_q, L, C, _ptr(lut), _ptr(scores),
+              _ptr(mc), _stream())
+    return scores, mc
+
+
+# ------------------------------------------------------------------- K4
+def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None):
+    """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D)."""
+    _need(scores, torch.float64, "scores")
+    rows, ld = scores.shape
+    n = ld if n is None else n
+    ids_ld = 0
+    if ids is not None:
+        if ids.dtype not in (torch.int64, torch.uint64):
+            raise ValueError("invalid parameter: ids must be 64-bit")
+        ids = ids.contiguous()
+        ids_ld = ids.shape[1] if ids.dim() == 2 else 0
+    if n_valid is not None:
+        _need(n_valid, torch.int32, "n_valid")
+    out_s = torch.empty((rows, k), dtype=torch.float64, device=scores.device)
+    out_i = torch.empty((rows, k), dtype=torch.int64, device=scores.device)
+    out_p = torch.empty((rows, k), dtype=torch.int64, device=scores.device)
+    _lib.call("dsrt_topk", _ptr(scores), ld, _ptr(ids), ids_ld, _ptr(n_valid), n, rows, k,
+              _ptr(out_s), _ptr(out_i), _ptr(out_p), _stream())
+    return out_s, out_i, out_p
+
+
+def topk_max_k() -> int:
+    return _lib.lib().dsrt_topk_max_k()
+
+
+# ------------------------------------------------------------------- K5
+def prefilter(Q, m_q: int, centroids, post_off, post_docs, n_docs: int, probe: int,
+              k_filter: int):
+    """Q (n_qsets*m_q, d) float64 -> (cand (n_qsets, k_filter) int64, n_cand (n_qsets) int32)."""
+    _need(Q, torch.float64, "Q")
+    _need(centroids, torch.float64, "centroids")
+    n_q = Q.shape[0] // m_q
+    k_c, d = centroids.shape
+    cand = torch.empty((n_q, k_filter), dtype=torch.int64, device=Q.device)
+    n_cand = torch.empty(n_q, dtype=torch.int32, device=Q.device)
+    ws_bytes = _lib.lib().dsrt_prefilter_workspace(n_q, m_q, k_c, n_docs, probe)
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=Q.device)
+    _lib.call("dsrt_prefilter", _ptr(Q), n_q, m_q, d, _ptr(centroids), k_c, _ptr(post_off),
+              _ptr(post_docs), n_docs, probe, k_filter, _ptr(cand), _ptr(n_cand), _ptr(ws),
+              ws_bytes, _stream())
+    return cand, n_cand
+
+
+def microbench_int() -> dict:
+    out = (ctypes.c_double * 4)()
+    _lib.call("dsrt_microbench_int", out, _stream())
+    return {"lop3_ops_per_s": out[0], "popc_ops_per_s": out[1], "imnmx_ops_per_s": out[2],
+            "mix_compares_per_s": out[3]}
+
+
+def as_numpy(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()

@@ -1,0 +1,484 @@
+"""Index build and query -- drop-in for dessert.index (reference: pkg/src/dessert/index.py).
+
+Same names, arguments, defaults, results and error messages as the
+reference, executed by the sm_100a kernels in ``csrc/``:
+
+* ``build_index``  (index.py:131-167): hash every vector on the GPU (K1),
+  lay the codes out per set (K2: size scan -> CSR of bit-sliced records),
+  optional centroid prefilter.
+* ``query``        (index.py:264-319): hash Q (K1), prefilter (K5) or all
+  sets, score (K3), top-k by (score desc, doc_id asc) (K4).
+* ``query_batch``  (new, batched form of ``query`` for many query sets).
+* ``score_candidate`` (index.py:230-247).
+* ``add_sets``     (new: append sets to a built index; equals building over
+  the concatenated docs when the prefilter is off).
+
+The index is immutable during queries (queries never write to it), so
+concurrent queries on different streams are safe.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import engine
+from .lsh import (SimLookup, SrpFamily, build_sim_lookup, hash_device, sample_srp_family,
+                  to_device_matrix)
+from .scoring import Scorer, default_scorer, max_aggregation, require_device_scorer
+from .sketch import SketchView
+
+RankedResults = list[tuple[int, float]]
+
+MAX_TRAIN_SAMPLES = 1 << 20
+# Scores materialised per exhaustive pass before a top-k merge (bytes).
+SCORE_BUFFER_BYTES = 4 << 30
+
+
+@dataclass(frozen=True)
+class FilterConfig:
+    """Centroid prefilter settings; centroids=0 means ceil(sqrt(total vectors)) (index.py:35-44)."""
+
+    enabled: bool = True
+    centroids: int = 0
+    iters: int = 10
+    probe: int = 1
+    k_filter: int = 4096
+
+
+@dataclass(frozen=True)
+class IndexConfig:
+    """index.py:46-62."""
+
+    d: int
+    C: int = 7
+    L: int = 32
+    seed: int = 0
+    inner_kind: str = "max"
+    phi: str | None = None
+    filter: FilterConfig = field(default_factory=FilterConfig)
+
+    @property
+    def code_range(self) -> int:
+        return 1 << self.C
+
+    def scorer(self) -> Scorer:
+        if self.inner_kind == "max":
+            return Scorer(inner=max_aggregation(), weights=None)
+        from .scoring import InnerAggregation
+
+        return Scorer(inner=InnerAggregation(kind="avg", alpha=1.0, beta=1.0, phi=self.phi))
+
+
+PROFILES: dict[str, dict] = {  # index.py:66-71 (paper App. B)
+    "msmarco-k10-fast": {"C": 7, "L": 32, "k_filter": 4096, "probe": 1},
+    "msmarco-k10-slow": {"C": 7, "L": 64, "k_filter": 4096, "probe": 2},
+    "msmarco-k1000-fast": {"C": 6, "L": 32, "k_filter": 8192, "probe": 4},
+    "msmarco-k1000-slow": {"C": 7, "L": 32, "k_filter": 16384, "probe": 4},
+}
+
+
+def apply_profile(config: IndexConfig, name: str) -> IndexConfig:
+    """index.py:74-84."""
+    if name not in PROFILES:
+        raise ValueError(f"unknown profile: {name!r} (choose from {sorted(PROFILES)})")
+    p = PROFILES[name]
+    return replace(config, C=p["C"], L=p["L"],
+                   filter=replace(config.filter, probe=p["probe"], k_filter=p["k_filter"]))
+
+
+@dataclass
+class DessertIndex:
+    """N sets in the device layout plus the shared hash family, LUT and prefilter.
+
+    Device state: ``records`` (sum m_i, R) int32 bit-sliced codes,
+    ``set_off`` (N+1) int64, ``codes`` (sum m_i, L) raw codes (optional),
+    ``lut_dev`` (L+1) float64, ``doc_ids_dev`` (N) int64.
+    """
+
+    config: IndexConfig
+    family: SrpFamily
+    lookup: SimLookup
+    doc_ids: np.ndarray
+    sizes: np.ndarray
+    filter: tuple | None
+    records: torch.Tensor
+    set_off: torch.Tensor
+    codes: torch.Tensor | None
+    lut_dev: torch.Tensor
+    doc_ids_dev: torch.Tensor
+
+    @property
+    def n_docs(self) -> int:
+        return int(self.sizes.shape[0])
+
+    @property
+    def m_max(self) -> int:
+        return int(self.sizes.max())
+
+    @property
+    def sketches(self) -> SketchView:
+        return SketchView(self)
+
+    @property
+    def device(self):
+        return self.records.device
+
+
+# --------------------------------------------------------------------- build
+def _validated_docs(docs, d: int):
+    """index.py:108-128 (shape checks on the host; zero rows are found by K1)."""
+    out, seen = [], set()
+    for doc_id, S in docs:
+        doc_id = int(doc_id)
+        if doc_id in seen:
+            raise ValueError(f"duplicate doc id: {doc_id}")
+        seen.add(doc_id)
+        X = S if isinstance(S, torch.Tensor) else np.asarray(S)
+        if X.ndim != 2 or X.shape[0] == 0:
+            raise ValueError(f"empty set: document {doc_id} has no vectors")
+        if X.shape[1] != d:
+            raise ValueError(
+                f"dimension mismatch: document {doc_id} has d={X.shape[1]}, expected {d}")
+        out.append((doc_id, X))
+    if not out:
+        raise ValueError("empty collection: nothing to index")
+    return out
+
+
+def _stack(items, device):
+    mats = [X for _, X in items]
+    if all(isinstance(X, torch.Tensor) for X in mats):
+        dt = mats[0].dtype
+        if any(X.dtype != dt for X in mats):
+            mats = [X.to(torch.float64) for X in mats]
+        return torch.cat([X.to(device) for X in mats], dim=0).contiguous()
+    arrs = [X.cpu().numpy() if isinstance(X, torch.Tensor) else np.asarray(X) for X in mats]
+    dt = arrs[0].dtype
+    if dt not in (np.float32, np.float64, np.float16) or any(a.dtype != dt for a in arrs):
+        arrs = [a.astype(np.float64) for a in arrs]
+    return torch.from_numpy(np.ascontiguousarray(np.concatenate(arrs, axis=0))).to(device)
+
+
+def _zero_row_doc(items) -> int:
+    for doc_id, X in items:
+        a = X.float().cpu().numpy() if isinstance(X, torch.Tensor) else np.asarray(X, np.float64)
+        if np.any(np.linalg.norm(a, axis=1) == 0.0):
+            return doc_id
+    return -1
+
+
+def _layout(sizes: np.ndarray, device):
+    sizes_dev = torch.from_numpy(np.ascontiguousarray(sizes, dtype=np.int64)).to(device)
+    set_off, bad = engine.sizes_to_offsets(sizes_dev)
+    if int(bad.item()) != 0:
+        raise ValueError("set too large: m must be <= 65535")
+    return set_off
+
+
+def build_from_vectors(X: torch.Tensor, sizes: np.ndarray, doc_ids, config: IndexConfig,
+                       keep_codes: bool = True, hash_mode: int | None = None,
+                       filt=None) -> DessertIndex:
+    """Build from one device matrix of all vectors grouped by set (fast path)."""
+    family = sample_srp_family(config.d, config.C, config.L, config.seed)
+    lookup = build_sim_lookup(config.C, config.L)
+    codes, recs = hash_device(family, X, mode=hash_mode, want_codes=keep_codes)
+    set_off = _layout(sizes, X.device)
+    ids = np.asarray(doc_ids, dtype=np.uint64)
+    return DessertIndex(
+        config=config, family=family, lookup=lookup, doc_ids=ids,
+        sizes=np.asarray(sizes, dtype=np.int64), filter=filt, records=recs, set_off=set_off,
+        codes=codes, lut_dev=torch.from_numpy(lookup.table).to(X.device),
+        doc_ids_dev=torch.from_numpy(ids.view(np.int64)).to(X.device))
+
+
+def build_from_codes(codes: torch.Tensor, sizes: np.ndarray, doc_ids, config: IndexConfig,
+                     keep_codes: bool = True, filt=None) -> DessertIndex:
+    """Build from precomputed (sum m_i, L) codes on the device (codes-only configs)."""
+    family = sample_srp_family(config.d, config.C, config.L, config.seed)
+    lookup = build_sim_lookup(config.C, config.L)
+    recs, bad = engine.codes_to_records(codes, config.L, config.C)
+    if int(bad.item()) != 0:
+        raise ValueError(f"code out of range: codes must lie in [0, {config.code_range})")
+    set_off = _layout(sizes, codes.device)
+    ids = np.asarray(doc_ids, dtype=np.uint64)
+    return DessertIndex(
+        config=config, family=family, lookup=lookup, doc_ids=ids,
+        sizes=np.asarray(sizes, dtype=np.int64), filter=filt, records=recs, set_off=set_off,
+        codes=codes if keep_codes else None,
+        lut_dev=torch.from_numpy(lookup.table).to(codes.device),
+        doc_ids_dev=torch.from_numpy(ids.view(np.int64)).to(codes.device))
+
+
+def build_index(docs, config: IndexConfig, device="cuda", keep_codes: bool = True,
+                hash_mode: int | None = None) -> DessertIndex:
+    """Sketch every (doc_id, vector set) pair on the GPU and build the optional prefilter.
+
+    index.py:131-167.  Deterministic in the inputs and config.seed.
+    """
+    items = _validated_docs(docs, config.d)
+    X = _stack(items, device)
+    sizes = np.array([x.shape[0] for _, x in items], dtype=np.int64)
+    try:
+        index = build_from_vectors(X, sizes, [i for i, _ in items], config, keep_codes, hash_mode)
+    except ValueError as e:
+        if str(e).startswith("zero vector"):
+            raise ValueError(f"zero vector in document {_zero_row_doc(items)}") from None
+        raise
+    if config.filter.enabled:
+        from .prefilter import build_centroid_index, train_centroids
+
+        n = X.shape[0]
+        pool_idx = None
+        if n > MAX_TRAIN_SAMPLES:
+            rng = np.random.default_rng([config.seed, 0xF117E2])
+            pool_idx = rng.choice(n, size=MAX_TRAIN_SAMPLES, replace=False)
+        n_pool = n if pool_idx is None else MAX_TRAIN_SAMPLES
+        k = config.filter.centroids or math.isqrt(n_pool - 1) + 1
+        k = min(k, n_pool)
+        pool = X if pool_idx is None else X[torch.from_numpy(pool_idx).to(X.device)]
+        centroids = train_centroids(pool, k, config.filter.iters, config.seed)
+        cindex = build_centroid_index(X, centroids, set_off=index.set_off, n_docs=index.n_docs)
+        index.filter = (centroids, cindex)
+    return index
+
+
+def add_sets(index: DessertIndex, docs) -> DessertIndex:
+    """Append sets (new API).  Same result as building over the concatenated docs
+    when the prefilter is off; with a prefilter the new sets are assigned to the
+    existing centroids (no retraining)."""
+    items = _validated_docs(docs, index.config.d)
+    existing = set(int(i) for i in index.doc_ids)
+    for doc_id, _ in items:
+        if doc_id in existing:
+            raise ValueError(f"duplicate doc id: {doc_id}")
+    X = _stack(items, index.device)
+    sizes = np.array([x.shape[0] for _, x in items], dtype=np.int64)
+    try:
+        codes, recs = hash_device(index.family, X, want_codes=index.codes is not None)
+    except ValueError as e:
+        if str(e).startswith("zero vector"):
+            raise ValueError(f"zero vector in document {_zero_row_doc(items)}") from None
+        raise
+    all_sizes = np.concatenate([index.sizes, sizes])
+    index.records = torch.cat([index.records, recs])
+    if index.codes is not None:
+        index.codes = torch.cat([index.codes, codes])
+    index.set_off = _layout(all_sizes, index.device)
+    index.sizes = all_sizes
+    index.doc_ids = np.concatenate([index.doc_ids, np.array([i for i, _ in items], np.uint64)])
+    index.doc_ids_dev = torch.from_numpy(index.doc_ids.view(np.int64)).to(index.device)
+    if index.filter is not None:
+        from .prefilter import extend_centroid_index
+
+        centroids, cindex = index.filter
+        index.filter = (centroids, extend_centroid_index(cindex, X, centroids, sizes))
+    return index
+
+
+# --------------------------------------------------------------------- query
+def _query_records(index: DessertIndex, Q) -> tuple[torch.Tensor, int]:
+    t = to_device_matrix(Q, index.config.d, index.device)
+    _, recs = hash_device(index.family, t, want_codes=False)
+    return recs, t.shape[0]
+
+
+def _rank(scores: torch.Tensor, top_k: int, ids: torch.Tensor, n_valid=None):
+    """Row-wise (score desc, doc_id asc) top-k on the device."""
+    rows, n = scores.shape
+    k = min(top_k, n)
+    if k <= engine.topk_max_k():
+        return engine.topk(scores, k, ids=ids, n_valid=n_valid)
+    # k beyond the single-CTA selector: stable two-key sort on the device
+    ids2 = ids if ids.dim() == 2 else ids.expand(rows, n)
+    valid = torch.ones_like(scores, dtype=torch.bool)
+    if n_valid is not None:
+        valid = torch.arange(n, device=scores.device)[None, :] < n_valid[:, None].long()
+    s = torch.where(valid, scores, torch.full_like(scores, -1.0))
+    o1 = torch.argsort(ids2, dim=1, stable=True)
+    s1 = torch.gather(s, 1, o1)
+    o2 = torch.argsort(-s1, dim=1, stable=True)
+    pos = torch.gather(o1, 1, o2)[:, :k]
+    out_s = torch.gather(s, 1, pos)
+    out_i = torch.gather(ids2, 1, pos)
+    bad = out_s < 0
+    return (out_s.masked_fill(bad, -1.0), out_i.masked_fill(bad, -1), pos.masked_fill(bad, -1))
+
+
+def _results(out_s: torch.Tensor, out_i: torch.Tensor) -> list[RankedResults]:
+    s = out_s.cpu().numpy()
+    ids = out_i.cpu().numpy().view(np.uint64)
+    res = []
+    for r in range(s.shape[0]):
+        valid = s[r] >= 0.0
+        res.append([(int(d), float(v)) for d, v in zip(ids[r][valid], s[r][valid])])
+    return res
+
+
+def _candidates(index: DessertIndex, Qdev: torch.Tensor, m_q: int, probe, k_filter):
+    from .prefilter import filter_candidates_device
+
+    centroids, cindex = index.filter
+    cfg = index.config.filter
+    return filter_candidates_device(cindex, centroids, Qdev, m_q,
+                                    cfg.probe if probe is None else probe,
+                                    cfg.k_filter if k_filter is None else k_filter)
+
+
+def rank_records(index: DessertIndex, qrecs: torch.Tensor, m_q: int, top_k: int,
+                 cand=None, n_cand=None):
+    """Score query-set records (n_qsets*m_q, R) and rank; returns (scores, ids) (n_qsets, k)."""
+    n_q = qrecs.shape[0] // m_q
+    L, C = index.config.L, index.config.C
+    N = index.n_docs
+    if cand is not None:
+        scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, m_q, L, C,
+                                            index.lut_dev, cand=cand, n_cand=n_cand)
+        ids = index.doc_ids_dev[cand.clamp(min=0)]
+        out_s, out_i, _ = _rank(scores, top_k, ids, n_valid=n_cand)
+        return out_s, out_i
+    if n_q < 8:
+        scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, m_q, L, C,
+                                            index.lut_dev, cand_ld=N, n_qsets=n_q)
+        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev)
+        return out_s, out_i
+    # exhaustive batched: chunk the set range so the score buffer stays bounded
+    chunk = max(1, min(N, SCORE_BUFFER_BYTES // (8 * n_q)))
+    if chunk >= N:
+        scores, _ = engine.score_all(index.records, index.set_off, qrecs, m_q, L, C,
+                                     index.lut_dev)
+        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev)
+        return out_s, out_i
+    buf = torch.empty((n_q, chunk), dtype=torch.float64, device=index.device)
+    parts_s, parts_i = [], []
+    for s0 in range(0, N, chunk):
+        s1 = min(N, s0 + chunk)
+        engine.score_all(index.records, index.set_off, qrecs, m_q, L, C, index.lut_dev,
+                         set_begin=s0, set_end=s1, scores=buf, ld=chunk)
+        ps, pi, _ = _rank(buf[:, : s1 - s0] if s1 - s0 < chunk else buf, top_k,
+                          index.doc_ids_dev[s0:s1])
+        parts_s.append(ps)
+        parts_i.append(pi)
+    S = torch.cat(parts_s, dim=1).contiguous()
+    I = torch.cat(parts_i, dim=1).contiguous()
+    valid = (S >= 0).sum(dim=1).to(torch.int32)
+    # padded entries (-1) sort last; n_valid is not needed because -1 < any score
+    out_s, out_i, _ = _rank(S, top_k, I)
+    del valid
+    return out_s, out_i
+
+
+def query(index: DessertIndex, Q, top_k: int, probe: int | None = None,
+          k_filter: int | None = None, scorer: Scorer | None = None,
+          threads: int = 1) -> RankedResults:
+    """Rank the top_k sets for one query vector set (index.py:264-319).
+
+    ``threads`` is accepted for signature compatibility; results never depend
+    on it (the device path is deterministic).
+    """
+    if top_k < 1:
+        raise ValueError(f"invalid parameter: top_k must be >= 1, got {top_k}")
+    Qa = Q if isinstance(Q, torch.Tensor) else np.asarray(Q, dtype=np.float64)
+    if Qa.ndim != 2 or Qa.shape[0] == 0:
+        raise ValueError("empty query: need at least one query vector")
+    require_device_scorer(scorer)
+    Qdev = to_device_matrix(Qa, index.config.d, index.device)
+    _, qrecs = hash_device(index.family, Qdev, want_codes=False)
+    m_q = Qdev.shape[0]
+    cand = n_cand = None
+    if index.filter is not None:
+        cand, n_cand = _candidates(index, Qdev, m_q, probe, k_filter)
+        if int(n_cand[0].item()) == 0:
+            return []
+    out_s, out_i = rank_records(index, qrecs, m_q, top_k, cand, n_cand)
+    return _results(out_s, out_i)[0]
+
+
+def query_batch(index: DessertIndex, Qs, top_k: int, probe: int | None = None,
+                k_filter: int | None = None, scorer: Scorer | None = None,
+                return_tensors: bool = False):
+    """Batched ``query`` over n_qsets query sets of equal size m_q.
+
+    Qs: (n_qsets, m_q, d).  Returns a list of RankedResults, or the device
+    tensors (scores (n_qsets, k), doc ids (n_qsets, k)) with return_tensors.
+    """
+    if top_k < 1:
+        raise ValueError(f"invalid parameter: top_k must be >= 1, got {top_k}")
+    require_device_scorer(scorer)
+    if isinstance(Qs, torch.Tensor):
+        t = Qs
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(Qs)))
+    if t.dim() != 3 or t.shape[1] == 0:
+        raise ValueError("empty query: need at least one query vector")
+    n_q, m_q, d = t.shape
+    Qdev = to_device_matrix(t.reshape(n_q * m_q, d), index.config.d, index.device)
+    _, qrecs = hash_device(index.family, Qdev, want_codes=False)
+    cand = n_cand = None
+    if index.filter is not None:
+        cand, n_cand = _candidates(index, Qdev, m_q, probe, k_filter)
+    out_s, out_i = rank_records(index, qrecs, m_q, top_k, cand, n_cand)
+    if return_tensors:
+        return out_s, out_i
+    return _results(out_s, out_i)
+
+
+def query_codes_batch(index: DessertIndex, qcodes, top_k: int, return_tensors=False):
+    """Rank from precomputed query codes (n_qsets, m_q, L) -- the parity hook
+    ("both sides given the same hash codes")."""
+    t = qcodes if isinstance(qcodes, torch.Tensor) else torch.from_numpy(np.asarray(qcodes))
+    n_q, m_q, L = t.shape
+    if L != index.config.L:
+        raise ValueError(f"expected (m_q, {index.config.L}) code matrix, got shape {tuple(t.shape)}")
+    codes = t.reshape(n_q * m_q, L).to(index.device).to(torch.int32).contiguous()
+    qrecs, bad = engine.codes_to_records(codes, L, index.config.C)
+    out_s, out_i = rank_records(index, qrecs, m_q, top_k)
+    if return_tensors:
+        return out_s, out_i
+    return _results(out_s, out_i)
+
+
+def score_candidate(index: DessertIndex, i: int, query_codes, scorer: Scorer | None = None) -> float:
+    """index.py:230-247: relevance of set i for an (m_q, L) code matrix."""
+    if not 0 <= i < index.n_docs:
+        raise IndexError(f"set index out of range: {i} (N={index.n_docs})")
+    qc = np.asarray(query_codes)
+    if qc.ndim != 2 or qc.shape[1] != index.config.L:
+        raise ValueError(f"expected (m_q, {index.config.L}) code matrix, got shape {qc.shape}")
+    require_device_scorer(scorer)
+    if qc.shape[0] == 0:
+        return float("nan")  # np.mean of an empty array (reference warns and returns nan)
+    codes = torch.from_numpy(qc.astype(np.int32)).to(index.device)
+    qrecs, _ = engine.codes_to_records(codes, index.config.L, index.config.C, check=False)
+    cand = torch.tensor([[i]], dtype=torch.int64, device=index.device)
+    scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, qc.shape[0],
+                                        index.config.L, index.config.C, index.lut_dev, cand=cand)
+    return float(scores[0, 0].item())
+
+
+def score_matrix(index: DessertIndex, qcodes, sets=None, want_counts=False):
+    """Scores (and optional integer max counts c_q) of query code sets vs sets (parity API)."""
+    t = qcodes if isinstance(qcodes, torch.Tensor) else torch.from_numpy(np.asarray(qcodes))
+    n_q, m_q, L = t.shape
+    codes = t.reshape(n_q * m_q, L).to(index.device).to(torch.int32).contiguous()
+    qrecs, _ = engine.codes_to_records(codes, L, index.config.C, check=False)
+    if sets is None:
+        if n_q >= 8:
+            return engine.score_all(index.records, index.set_off, qrecs, m_q, L, index.config.C,
+                                    index.lut_dev, want_counts=want_counts)
+        return engine.score_candidates(index.records, index.set_off, qrecs, m_q, L,
+                                       index.config.C, index.lut_dev, cand_ld=index.n_docs,
+                                       n_qsets=n_q, want_counts=want_counts)
+    cand = sets if isinstance(sets, torch.Tensor) else torch.from_numpy(np.asarray(sets, np.int64))
+    cand = cand.to(index.device).contiguous()
+    return engine.score_candidates(index.records, index.set_off, qrecs, m_q, L, index.config.C,
+                                   index.lut_dev, cand=cand, want_counts=want_counts)
+
+
+__all__ = ["FilterConfig", "IndexConfig", "PROFILES", "apply_profile", "DessertIndex",
+           "RankedResults", "build_index", "build_from_vectors", "build_from_codes", "add_sets",
+           "query", "query_batch", "query_codes_batch", "score_candidate", "score_matrix",
+           "default_scorer"]

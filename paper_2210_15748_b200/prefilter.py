@@ -1,0 +1,212 @@
+"""Centroid prefilter -- drop-in for dessert.prefilter (reference: pkg/src/dessert/prefilter.py).
+
+``filter_candidates`` (prefilter.py:111-144) runs on the GPU (K5,
+csrc/prefilter.cu).  Centroid training (prefilter.py:47-82) and the
+centroid->document postings (prefilter.py:85-108) are index-build setup:
+SURVEY.md marks train_centroids out of scope and the postings build as 8(f)
+row f1.  Both are done on the device here with float64 torch tensor ops
+(argmax/unique/sort plumbing, no CPU work), following the reference's
+algorithm and tie rules step by step.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import engine
+
+MAX_TRAIN_SAMPLES = 1 << 20
+
+
+@dataclass(frozen=True)
+class Centroids:
+    """k unit-norm centroid directions (prefilter.py:20-26)."""
+
+    k: int
+    seed: int
+    vectors: np.ndarray
+    _dev: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def device_vectors(self, device) -> torch.Tensor:
+        key = str(device)
+        t = self._dev.get(key)
+        if t is None:
+            t = torch.from_numpy(np.ascontiguousarray(self.vectors, dtype=np.float64)).to(device)
+            self._dev[key] = t
+        return t
+
+
+@dataclass
+class CentroidIndex:
+    """Per-centroid postings of ascending, deduplicated doc indices (prefilter.py:29-34),
+    held on the device as CSR (post_off (k+1), post_docs)."""
+
+    n_docs: int
+    post_off: torch.Tensor
+    post_docs: torch.Tensor
+
+    @property
+    def postings(self) -> list[np.ndarray]:
+        off = self.post_off.cpu().numpy()
+        docs = self.post_docs.cpu().numpy()
+        return [docs[off[c]:off[c + 1]] for c in range(len(off) - 1)]
+
+
+def _unit_rows_dev(X: torch.Tensor, name: str) -> torch.Tensor:
+    X = X.to(torch.float64)
+    if X.dim() != 2 or X.shape[0] == 0:
+        raise ValueError(f"{name} must be a non-empty (n, d) matrix, got shape {tuple(X.shape)}")
+    norms = torch.linalg.norm(X, dim=1, keepdim=True)
+    if bool((norms == 0).any()):
+        raise ValueError(f"zero vector in {name}: cannot assign to a centroid")
+    return X / norms
+
+
+def _as_dev(X, device="cuda") -> torch.Tensor:
+    if isinstance(X, torch.Tensor):
+        return X.to(device)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(X, dtype=np.float64))).to(device)
+
+
+def train_centroids(samples, k: int, iters: int, seed: int, device="cuda") -> Centroids:
+    """Spherical Lloyd iterations (prefilter.py:47-82) on the device in float64."""
+    X = _unit_rows_dev(_as_dev(samples, device), "samples")
+    n = X.shape[0]
+    if k < 1:
+        raise ValueError(f"invalid parameter: k must be >= 1, got {k}")
+    if n < k:
+        raise ValueError(f"too few samples: need at least k={k}, got {n}")
+    if iters < 1:
+        raise ValueError(f"invalid parameter: iters must be >= 1, got {iters}")
+    rng = np.random.default_rng(seed)
+    init = torch.from_numpy(rng.choice(n, size=k, replace=False)).to(X.device)
+    cents = X[init].clone()
+    for _ in range(iters):
+        assign = torch.empty(n, dtype=torch.int64, device=X.device)
+        best = torch.empty(n, dtype=torch.float64, device=X.device)
+        for lo in range(0, n, 1 << 16):
+            sims = X[lo:lo + (1 << 16)] @ cents.T
+            b, a = sims.max(dim=1)  # first max on ties, like np.argmax
+            assign[lo:lo + (1 << 16)] = a
+            best[lo:lo + (1 << 16)] = b
+        sums = torch.zeros_like(cents).index_add_(0, assign, X)
+        counts = torch.bincount(assign, minlength=k)
+        norms = torch.linalg.norm(sums, dim=1)
+        dead = (counts == 0) | (norms < 1e-12)
+        if bool(dead.any()):
+            order = torch.argsort(best, stable=True)
+            slots = torch.nonzero(dead).flatten()
+            pts = order[: slots.numel()]
+            sums[slots] = X[pts]
+            norms[slots] = 1.0
+        cents = sums / norms[:, None]
+    return Centroids(k=k, seed=seed, vectors=cents.cpu().numpy())
+
+
+def _postings_from_assign(doc_of: torch.Tensor, assign: torch.Tensor, k: int, n_docs: int):
+    key = assign * n_docs + doc_of           # (centroid, doc) pairs, deduplicated
+    key = torch.unique(key)                  # sorted: by centroid, then doc ascending
+    cent = key // n_docs
+    docs = key % n_docs
+    counts = torch.bincount(cent, minlength=k)
+    off = torch.zeros(k + 1, dtype=torch.int64, device=key.device)
+    off[1:] = torch.cumsum(counts, 0)
+    return off, docs.contiguous()
+
+
+def _assign(X: torch.Tensor, cvec: torch.Tensor) -> torch.Tensor:
+    n = X.shape[0]
+    out = torch.empty(n, dtype=torch.int64, device=X.device)
+    step = max(1, (1 << 28) // max(1, cvec.shape[0]))
+    for lo in range(0, n, step):
+        out[lo:lo + step] = torch.argmax(X[lo:lo + step] @ cvec.T, dim=1)
+    return out
+
+
+def build_centroid_index(docs, centroids: Centroids, set_off: torch.Tensor | None = None,
+                         n_docs: int | None = None, device="cuda") -> CentroidIndex:
+    """Invert centroid assignment (prefilter.py:85-108): posting c = docs with a
+    vector whose argmax-dot centroid is c, each doc once, ascending.
+
+    ``docs`` is either a list of (m_i, d) arrays or one device matrix of all
+    vectors grouped by set with ``set_off``.
+    """
+    if isinstance(docs, torch.Tensor) and set_off is not None:
+        X = docs.to(torch.float64)
+        off = set_off
+        N = int(n_docs)
+    else:
+        mats = [np.asarray(S, dtype=np.float64) if not isinstance(S, torch.Tensor) else S
+                for S in docs]
+        if not mats:
+            raise ValueError("empty collection: nothing to index")
+        for i, S in enumerate(mats):
+            if S.ndim != 2 or S.shape[1] != centroids.vectors.shape[1]:
+                raise ValueError(
+                    f"dimension mismatch: document {i} has d={S.shape[1]}, "
+                    f"centroids have d={centroids.vectors.shape[1]}")
+        sizes = np.array([S.shape[0] for S in mats], dtype=np.int64)
+        X = torch.cat([_as_dev(S, device) for S in mats]).to(torch.float64)
+        off = torch.from_numpy(np.concatenate([[0], np.cumsum(sizes)])).to(X.device)
+        N = len(mats)
+    Xu = _unit_rows_dev(X, "documents")
+    cvec = centroids.device_vectors(X.device)
+    assign = _assign(Xu, cvec)
+    sizes_dev = off[1:] - off[:-1]
+    doc_of = torch.repeat_interleave(torch.arange(N, device=X.device), sizes_dev)
+    post_off, post_docs = _postings_from_assign(doc_of, assign, centroids.k, N)
+    return CentroidIndex(n_docs=N, post_off=post_off, post_docs=post_docs)
+
+
+def extend_centroid_index(cindex: CentroidIndex, X: torch.Tensor, centroids: Centroids,
+                          sizes: np.ndarray) -> CentroidIndex:
+    """Add postings for new docs (appended after the existing n_docs)."""
+    Xu = _unit_rows_dev(X, "documents")
+    assign = _assign(Xu, centroids.device_vectors(X.device))
+    sizes_dev = torch.from_numpy(np.asarray(sizes, np.int64)).to(X.device)
+    doc_of = cindex.n_docs + torch.repeat_interleave(
+        torch.arange(len(sizes), device=X.device), sizes_dev)
+    old_off = cindex.post_off
+    old_cent = torch.repeat_interleave(torch.arange(centroids.k, device=X.device),
+                                       old_off[1:] - old_off[:-1])
+    N = cindex.n_docs + len(sizes)
+    key = torch.cat([old_cent * N + cindex.post_docs, assign * N + doc_of])
+    post_off, post_docs = _postings_from_assign(key % N, key // N, centroids.k, N)
+    return CentroidIndex(n_docs=N, post_off=post_off, post_docs=post_docs)
+
+
+def filter_candidates_device(cindex: CentroidIndex, centroids: Centroids, Q: torch.Tensor,
+                             m_q: int, probe: int, k_filter: int):
+    """K5 on the device: Q (n_qsets*m_q, d) -> (cand (n_qsets, k_filter), n_cand)."""
+    if probe < 1:
+        raise ValueError(f"invalid parameter: probe must be >= 1, got {probe}")
+    if k_filter < 1:
+        raise ValueError(f"invalid parameter: k_filter must be >= 1, got {k_filter}")
+    Qd = Q.to(torch.float64).contiguous()
+    if Qd.shape[1] != centroids.vectors.shape[1]:
+        raise ValueError(f"dimension mismatch: Q has d={Qd.shape[1]}, "
+                         f"centroids have d={centroids.vectors.shape[1]}")
+    return engine.prefilter(Qd, m_q, centroids.device_vectors(Qd.device), cindex.post_off,
+                            cindex.post_docs, cindex.n_docs, probe, k_filter)
+
+
+def filter_candidates(index: CentroidIndex, centroids: Centroids, Q, probe: int,
+                      k_filter: int) -> np.ndarray:
+    """Drop-in for prefilter.filter_candidates: ordered doc indices (count desc, index asc)."""
+    if probe < 1:
+        raise ValueError(f"invalid parameter: probe must be >= 1, got {probe}")
+    if k_filter < 1:
+        raise ValueError(f"invalid parameter: k_filter must be >= 1, got {k_filter}")
+    Qa = Q if isinstance(Q, torch.Tensor) else np.asarray(Q, dtype=np.float64)
+    if Qa.ndim != 2 or Qa.shape[0] == 0:
+        raise ValueError(f"Q must be a non-empty (m_q, d) matrix, got shape {tuple(Qa.shape)}")
+    if Qa.shape[1] != centroids.vectors.shape[1]:
+        raise ValueError(f"dimension mismatch: Q has d={Qa.shape[1]}, "
+                         f"centroids have d={centroids.vectors.shape[1]}")
+    Qd = _as_dev(Qa, index.post_off.device)
+    cand, n_cand = filter_candidates_device(index, centroids, Qd, Qd.shape[0], probe, k_filter)
+    n = int(n_cand[0].item())
+    return cand[0, :n].cpu().numpy().astype(np.int64)

@@ -1,0 +1,209 @@
+"""Generate golden vectors by running the REAL reference package.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Outputs small .npz fixtures next to this script.  They pin the oracle
+(oracle/dessert_oracle.py) and the CUDA path; nothing at test time reads
+/root/reference.  Only the public reference API plus its private scoring
+helpers (index.py:_score_chunk, sketch.py:accumulate_collisions_batch) are
+called; no reference source is copied.
+"""
+
+from __future__ import annotations
+
+import importlib.util
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+
+import dessert  # noqa: E402  (the reference, via PYTHONPATH)
+from dessert import index as ref_index  # noqa: E402
+from dessert import prefilter as ref_prefilter  # noqa: E402
+from dessert import sketch as ref_sketch  # noqa: E402
+
+
+def _load_workloads():
+    spec = importlib.util.spec_from_file_location(
+        "workloads", os.path.join(REPO, "paper_2210_15748_b200", "workloads.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["workloads"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def no_filter(**kw):
+    return dessert.IndexConfig(filter=dessert.FilterConfig(enabled=False), **kw)
+
+
+def ref_scores(index, qcodes):
+    """Reference scores of every set for one code matrix (index.py:250-261)."""
+    scorer = index.config.scorer()
+    weights = ref_index._resolve_weights(scorer, qcodes.shape[0])
+    return np.array(ref_index._score_chunk(index, np.arange(index.n_docs), qcodes, scorer,
+                                           weights), dtype=np.float64)
+
+
+def ref_maxcounts(index, qcodes):
+    return np.stack([ref_sketch.accumulate_collisions_batch(t, qcodes).max(axis=1)
+                     for t in index.sketches], axis=0)  # (N, m_q)
+
+
+def make_cfg0():
+    wl = _load_workloads()
+    sizes, X, Q = wl.cfg0_data(0)
+    off = wl.offsets(sizes)
+    docs = [(i, X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+    index = dessert.build_index(docs, no_filter(d=128, C=6, L=32, seed=0))
+    codes = np.concatenate([dessert.hash_matrix(index.family, X[off[i]:off[i + 1]])
+                            for i in range(len(sizes))]).astype(np.uint8)
+    qcodes = np.stack([dessert.hash_matrix(index.family, q) for q in Q]).astype(np.uint8)
+    scores = np.stack([ref_scores(index, qc.astype(np.int64)) for qc in qcodes])
+    maxc = np.stack([ref_maxcounts(index, qc.astype(np.int64)) for qc in qcodes]).astype(np.uint8)
+    top_ids = np.zeros((len(Q), 10), dtype=np.int64)
+    top_sc = np.zeros((len(Q), 10), dtype=np.float64)
+    for i, q in enumerate(Q):
+        res = dessert.query(index, q, top_k=10)
+        top_ids[i] = [d for d, _ in res]
+        top_sc[i] = [s for _, s in res]
+    np.savez_compressed(os.path.join(HERE, "cfg0.npz"), sizes=sizes, codes=codes, qcodes=qcodes,
+                        scores=scores, maxcounts=maxc, top_ids=top_ids, top_scores=top_sc,
+                        lut=index.lookup.table, planes_head=index.family.planes[:8])
+
+
+SMALL_SHAPES = [  # (L, C, m_q, n_sets, m_max)
+    (32, 6, 32, 40, 120), (64, 7, 32, 40, 180), (32, 8, 32, 40, 100), (32, 7, 32, 30, 70),
+    (16, 3, 5, 30, 40), (8, 2, 200, 20, 30), (64, 7, 1, 20, 50), (24, 4, 7, 25, 60),
+    (40, 5, 129, 15, 40), (96, 3, 33, 15, 20), (20, 12, 17, 15, 30), (128, 1, 64, 10, 12),
+    (32, 7, 300, 6, 300), (33, 9, 31, 12, 260),
+]
+
+
+def make_small():
+    rng = np.random.default_rng(1234)
+    out = {}
+    for n, (L, C, m_q, n_sets, m_max) in enumerate(SMALL_SHAPES):
+        r = 1 << C
+        sizes = rng.integers(1, m_max + 1, size=n_sets)
+        # bias codes toward a few values so collisions (and ties) are common
+        hot = rng.integers(0, r, size=(L,))
+        codes = rng.integers(0, r, size=(int(sizes.sum()), L))
+        mask = rng.random(codes.shape) < 0.5
+        codes[mask] = np.broadcast_to(hot, codes.shape)[mask]
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        tables = [dessert.build_tiny_table(codes[off[i]:off[i + 1]], L, r) for i in range(n_sets)]
+        fam = dessert.sample_srp_family(4, C, L, 0)
+        index = ref_index.DessertIndex(config=no_filter(d=4, C=C, L=L), family=fam,
+                                       lookup=dessert.build_sim_lookup(C, L), sketches=tables,
+                                       doc_ids=rng.permutation(10 * n_sets)[:n_sets].astype(np.uint64),
+                                       sizes=sizes.astype(np.int64), filter=None)
+        qcodes = rng.integers(0, r, size=(3, m_q, L))
+        qm = rng.random(qcodes.shape) < 0.5
+        qcodes[qm] = np.broadcast_to(hot, qcodes.shape)[qm]
+        scores = np.stack([ref_scores(index, qc) for qc in qcodes])
+        maxc = np.stack([ref_maxcounts(index, qc) for qc in qcodes])
+        out[f"s{n}_shape"] = np.array([L, C, m_q])
+        out[f"s{n}_sizes"] = sizes
+        out[f"s{n}_codes"] = codes.astype(np.int32)
+        out[f"s{n}_qcodes"] = qcodes.astype(np.int32)
+        out[f"s{n}_doc_ids"] = index.doc_ids
+        out[f"s{n}_scores"] = scores
+        out[f"s{n}_maxcounts"] = maxc.astype(np.int32)
+        out[f"s{n}_lut"] = index.lookup.table
+        # TinyTables of the first 3 sets (for layout export parity)
+        for i in range(3):
+            out[f"s{n}_tt{i}_offsets"] = tables[i].offsets
+            out[f"s{n}_tt{i}_ids"] = tables[i].ids
+    out["n_shapes"] = np.array(len(SMALL_SHAPES))
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
+
+
+def make_end_to_end():
+    """Vectors -> build_index -> query, small enough to store the vectors."""
+    rng = np.random.default_rng(77)
+    out = {}
+    cases = [(16, 3, 16, 5, 40, 8, 10), (32, 6, 32, 6, 60, 32, 10), (64, 7, 128, 7, 30, 32, 5),
+             (8, 2, 8, 4, 25, 3, 25), (48, 5, 24, 9, 35, 40, 7)]
+    for n, (d, C, L, seed, n_sets, m_q, top_k) in enumerate(cases):
+        sizes = rng.integers(1, 24, size=n_sets)
+        X = rng.standard_normal((int(sizes.sum()), d))
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        ids = rng.permutation(1000)[:n_sets]
+        docs = [(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(n_sets)]
+        index = dessert.build_index(docs, no_filter(d=d, C=C, L=L, seed=seed))
+        Q = rng.standard_normal((2, m_q, d))
+        res = [dessert.query(index, q, top_k=top_k) for q in Q]
+        out[f"e{n}_shape"] = np.array([d, C, L, seed, top_k])
+        out[f"e{n}_sizes"] = sizes
+        out[f"e{n}_X"] = X
+        out[f"e{n}_ids"] = ids
+        out[f"e{n}_Q"] = Q
+        out[f"e{n}_codes"] = dessert.hash_matrix(index.family, X)
+        out[f"e{n}_top_ids"] = np.array([[d_ for d_, _ in r] for r in res])
+        out[f"e{n}_top_scores"] = np.array([[s for _, s in r] for r in res])
+    out["n_cases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(HERE, "end_to_end.npz"), **out)
+
+
+def make_lsh():
+    rng = np.random.default_rng(5)
+    fam = dessert.sample_srp_family(128, 6, 32, 0)
+    X = rng.standard_normal((256, 128))
+    X[:4] = 0.0
+    X[0, 0] = 1.0          # axis vectors give exact-zero projections on no plane
+    X[1, :] = 1e-3
+    X[2, 5] = -2.0
+    X[3, 7] = 1e-30        # tiny but non-zero
+    luts = {f"lut_{C}_{L}": dessert.build_sim_lookup(C, L).table
+            for C in (1, 2, 3, 6, 7, 8, 12, 24) for L in (1, 4, 8, 16, 32, 33, 64, 128)}
+    np.savez_compressed(os.path.join(HERE, "lsh.npz"), planes=fam.planes, X=X,
+                        codes=dessert.hash_matrix(fam, X),
+                        fam2_planes=dessert.sample_srp_family(16, 3, 5, 9).planes, **luts)
+
+
+def make_prefilter():
+    rng = np.random.default_rng(31)
+    d, k = 16, 24
+    docs = [rng.standard_normal((int(rng.integers(1, 9)), d)) for _ in range(300)]
+    cents = ref_prefilter.train_centroids(np.concatenate(docs), k=k, iters=5, seed=3)
+    vecs = cents.vectors.copy()
+    vecs[5] = vecs[4]      # duplicate centroid: ties must go to the lower id
+    cents = ref_prefilter.Centroids(k=k, seed=3, vectors=vecs)
+    cindex = ref_prefilter.build_centroid_index(docs, cents)
+    out = {"centroids": vecs, "n_docs": np.array(len(docs)),
+           "doc_sizes": np.array([len(x) for x in docs]), "docs": np.concatenate(docs)}
+    post_off = np.concatenate([[0], np.cumsum([len(p) for p in cindex.postings])])
+    out["post_off"] = post_off
+    out["post_docs"] = np.concatenate(cindex.postings).astype(np.int64)
+    cases = []
+    for t in range(24):
+        m_q = int(rng.integers(1, 40))
+        Q = rng.standard_normal((m_q, d))
+        if t % 5 == 0:
+            Q[0] = vecs[4] * 3.0   # exact tie between centroid 4 and 5
+        probe = int(rng.integers(1, 7))
+        k_filter = int(rng.choice([1, 5, 17, 64, 1000]))
+        got = ref_prefilter.filter_candidates(cindex, cents, Q, probe, k_filter)
+        out[f"q{t}"] = Q
+        out[f"r{t}"] = got
+        cases.append((probe, k_filter))
+    out["cases"] = np.array(cases)
+    np.savez_compressed(os.path.join(HERE, "prefilter.npz"), **out)
+
+
+if __name__ == "__main__":
+    assert "reference" in dessert.__file__, dessert.__file__
+    make_lsh()
+    make_small()
+    make_end_to_end()
+    make_prefilter()
+    make_cfg0()
+    print("golden vectors written to", HERE)
+    for f in sorted(os.listdir(HERE)):
+        print(f, os.path.getsize(os.path.join(HERE, f)))
+    sys.exit(0)

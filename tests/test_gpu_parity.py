@@ -1,0 +1,368 @@
+"""CUDA path vs the oracle / reference golden vectors (bit-exact).  Needs a B200."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2210_15748_b200 as d
+from conftest import small_case
+from oracle import c_oracle
+from oracle import dessert_oracle as O
+from paper_2210_15748_b200 import _lib, engine
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _index_from_codes(codes, sizes, L, C, doc_ids=None):
+    cfg = d.IndexConfig(d=4, C=C, L=L, filter=d.FilterConfig(enabled=False))
+    cd = torch.from_numpy(np.ascontiguousarray(codes).astype(np.int32)).to(DEV)
+    ids = np.arange(len(sizes)) if doc_ids is None else doc_ids
+    return d.build_from_codes(cd, sizes, ids, cfg)
+
+
+# ------------------------------------------------------------------ scoring
+def test_small_shapes_scores_and_counts_bit_exact(golden_small):
+    g = golden_small
+    for n in range(int(g["n_shapes"])):
+        c = small_case(g, n)
+        idx = _index_from_codes(c["codes"], c["sizes"], c["L"], c["C"], c["doc_ids"])
+        # all three scoring entry points: exhaustive (n_q<8 -> candidate kernel), explicit sets
+        s, mc = d.score_matrix(idx, c["qcodes"], want_counts=True)
+        np.testing.assert_array_equal(s.cpu().numpy(), c["scores"], err_msg=f"shape {n}")
+        np.testing.assert_array_equal(mc.cpu().numpy().astype(np.int32), c["maxcounts"])
+        # replicate query sets to >= 8 so the shared-tile exhaustive kernel runs
+        qrep = np.concatenate([c["qcodes"]] * 3)
+        s8, mc8 = d.score_matrix(idx, qrep, want_counts=True)
+        np.testing.assert_array_equal(s8.cpu().numpy(), np.concatenate([c["scores"]] * 3))
+        np.testing.assert_array_equal(mc8.cpu().numpy().astype(np.int32),
+                                      np.concatenate([c["maxcounts"]] * 3))
+        sets = np.stack([np.random.default_rng(n).permutation(len(c["sizes"]))] * 3)
+        sc, _ = d.score_matrix(idx, c["qcodes"], sets=sets)
+        np.testing.assert_array_equal(sc.cpu().numpy(),
+                                      np.take_along_axis(c["scores"], sets, axis=1))
+        for q in range(3):
+            i = int(sets[0, q])
+            assert d.score_candidate(idx, i, c["qcodes"][q]) == c["scores"][q, i]
+
+
+def test_cfg0_scores_counts_topk_bit_exact(golden_cfg0):
+    g = golden_cfg0
+    idx = _index_from_codes(g["codes"], g["sizes"], 32, 6)
+    s, mc = d.score_matrix(idx, g["qcodes"], want_counts=True)
+    np.testing.assert_array_equal(s.cpu().numpy(), g["scores"])
+    np.testing.assert_array_equal(mc.cpu().numpy().astype(np.uint8), g["maxcounts"])
+    res = d.query_codes_batch(idx, g["qcodes"], 10)
+    for q, r in enumerate(res):
+        assert [x for x, _ in r] == list(g["top_ids"][q])
+        assert [v for _, v in r] == list(g["top_scores"][q])
+
+
+def test_cfg0_end_to_end_from_vectors(golden_cfg0):
+    """Full path: vectors -> K1 hash -> K2 layout -> K3 -> K4 vs the reference's query()."""
+    from paper_2210_15748_b200 import workloads
+    g = golden_cfg0
+    sizes, X, Q = workloads.cfg0_data(0)
+    off = workloads.offsets(sizes)
+    cfg = d.IndexConfig(d=128, C=6, L=32, seed=0, filter=d.FilterConfig(enabled=False))
+    idx = d.build_from_vectors(torch.from_numpy(X).to(DEV), sizes, np.arange(len(sizes)), cfg)
+    codes = idx.codes.cpu().numpy()
+    mism = int((codes != g["codes"]).sum())
+    assert mism == 0, f"{mism} hash codes differ from the reference"
+    for q in range(len(Q)):
+        r = d.query(idx, Q[q], top_k=10)
+        assert [x for x, _ in r] == list(g["top_ids"][q])
+        assert [v for _, v in r] == list(g["top_scores"][q])
+    out_s, out_i = d.query_batch(idx, Q, 10, return_tensors=True)
+    np.testing.assert_array_equal(out_i.cpu().numpy(), g["top_ids"])
+    np.testing.assert_array_equal(out_s.cpu().numpy(), g["top_scores"])
+    del off
+
+
+# ------------------------------------------------------------------ hashing
+def test_hash_golden_f64(golden_lsh):
+    g = golden_lsh
+    fam = d.sample_srp_family(128, 6, 32, 0)
+    got = d.hash_matrix(fam, g["X"])
+    np.testing.assert_array_equal(got, g["codes"])
+    with pytest.raises(ValueError, match="zero vector"):
+        d.hash_matrix(fam, np.zeros((2, 128)))
+    with pytest.raises(ValueError, match="dimension"):
+        d.hash_matrix(fam, np.ones((2, 5)))
+
+
+@pytest.mark.parametrize("mode", [_lib.HASH_F64, _lib.HASH_F32])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16, torch.bfloat16, torch.float64])
+def test_hash_modes_flip_only_in_band(mode, dtype):
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((4096, 128))
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    Xt = torch.from_numpy(X).to(dtype)
+    Xexact = Xt.to(torch.float64).numpy()          # the values the device sees
+    fam = d.sample_srp_family(128, 7, 64, 3)
+    codes, recs = d.lsh.hash_device(fam, Xt.to(DEV).contiguous(), mode=mode)
+    want = O.hash_matrix(fam.planes, 64, 7, Xexact)
+    got = codes.cpu().numpy().astype(np.int64)
+    proj = O.projections(fam.planes, Xexact)
+    band = np.abs(proj) < 1e-4 * np.linalg.norm(fam.planes, axis=1)[None, :] * \
+        np.linalg.norm(Xexact, axis=1)[:, None]
+    bits_got = ((got[:, :, None] >> np.arange(7)) & 1).reshape(4096, 448)
+    bits_want = ((want[:, :, None] >> np.arange(7)) & 1).reshape(4096, 448)
+    flips = bits_got != bits_want
+    assert not np.any(flips & ~band), f"{int((flips & ~band).sum())} flips outside the band"
+    if mode == _lib.HASH_F64:
+        assert int(flips.sum()) == 0
+    # records agree with codes
+    recs2, _ = engine.codes_to_records(codes, 64, 7)
+    assert torch.equal(recs, recs2)
+
+
+# ------------------------------------------------------------------- layout
+def test_layout_roundtrip_and_tinytable_export(golden_small):
+    g = golden_small
+    for n in range(int(g["n_shapes"])):
+        c = small_case(g, n)
+        idx = _index_from_codes(c["codes"], c["sizes"], c["L"], c["C"])
+        np.testing.assert_array_equal(idx.set_off.cpu().numpy(), c["off"])
+        for i in range(3):
+            tt = idx.sketches[i]
+            np.testing.assert_array_equal(tt.offsets, g[f"s{n}_tt{i}_offsets"])
+            np.testing.assert_array_equal(tt.ids, g[f"s{n}_tt{i}_ids"])
+            assert tt.offsets.dtype == g[f"s{n}_tt{i}_offsets"].dtype
+        tt = d.build_tiny_table(c["codes"][: c["sizes"][0]], c["L"], 1 << c["C"])
+        np.testing.assert_array_equal(tt.ids, g[f"s{n}_tt0_ids"])
+
+
+def test_tinytable_known_answer():  # pkg/tests/test_sketch.py:37-40
+    t = d.build_tiny_table(np.array([[2], [0], [2]]), L=1, r=4)
+    np.testing.assert_array_equal(t.offsets[0], [0, 1, 1, 3, 3])
+    np.testing.assert_array_equal(t.ids[0], [1, 0, 2])
+    with pytest.raises(ValueError, match="out of range"):
+        d.build_tiny_table(np.array([[4]]), L=1, r=4)
+
+
+def test_counting_sort_stable():
+    rng = np.random.default_rng(3)
+    n_sets, n = 1000, 50000
+    set_of = rng.integers(0, n_sets, size=n)
+    so, perm = engine.counting_sort(torch.from_numpy(set_of).to(DEV), n_sets)
+    want = np.argsort(set_of, kind="stable")
+    np.testing.assert_array_equal(perm.cpu().numpy(), want)
+    np.testing.assert_array_equal(so.cpu().numpy(),
+                                  np.concatenate([[0], np.cumsum(np.bincount(set_of, minlength=n_sets))]))
+    rows = torch.from_numpy(rng.integers(0, 1 << 30, size=(n, 4)).astype(np.int32)).to(DEV)
+    got = engine.gather_rows(rows, perm)
+    np.testing.assert_array_equal(got.cpu().numpy(), rows.cpu().numpy()[want])
+
+
+def test_sizes_to_offsets_large_and_bad():
+    rng = np.random.default_rng(4)
+    sizes = rng.integers(1, 181, size=300_001).astype(np.int64)
+    so, bad = engine.sizes_to_offsets(torch.from_numpy(sizes).to(DEV))
+    np.testing.assert_array_equal(so.cpu().numpy(), np.concatenate([[0], np.cumsum(sizes)]))
+    assert int(bad.item()) == 0
+    sizes[7] = 0
+    sizes[9] = 70000
+    _, bad = engine.sizes_to_offsets(torch.from_numpy(sizes).to(DEV))
+    assert int(bad.item()) == 2
+
+
+# -------------------------------------------------------------------- top-k
+@pytest.mark.parametrize("n,k", [(1, 1), (5, 10), (1000, 10), (100_000, 100), (40_000, 1000),
+                                 (9000, 4096)])
+def test_topk_ties_and_order(n, k):
+    rng = np.random.default_rng(n + k)
+    rows = 6
+    # heavy ties: scores from a small value set, ids a random permutation
+    vals = np.sort(rng.random(17))
+    S = vals[rng.integers(0, 17, size=(rows, n))]
+    S[0] = 0.25  # all equal
+    ids = rng.permutation(10 * n)[:n].astype(np.int64)
+    out_s, out_i, out_p = engine.topk(torch.from_numpy(S).to(DEV), k,
+                                      ids=torch.from_numpy(ids).to(DEV))
+    for r in range(rows):
+        want = O.rank_topk(S[r], ids, k)
+        kk = len(want)
+        assert list(out_i[r, :kk].cpu().numpy()) == [w[0] for w in want]
+        assert list(out_s[r, :kk].cpu().numpy()) == [w[1] for w in want]
+        assert np.all(ids[out_p[r, :kk].cpu().numpy()] == out_i[r, :kk].cpu().numpy())
+
+
+def test_topk_n_valid_and_per_row_ids():
+    rng = np.random.default_rng(9)
+    S = rng.random((4, 300))
+    ids = rng.integers(0, 1 << 40, size=(4, 300)).astype(np.int64)
+    nv = np.array([0, 1, 150, 300], dtype=np.int32)
+    out_s, out_i, _ = engine.topk(torch.from_numpy(S).to(DEV), 20,
+                                  ids=torch.from_numpy(ids).to(DEV),
+                                  n_valid=torch.from_numpy(nv).to(DEV))
+    for r in range(4):
+        want = O.rank_topk(S[r, : nv[r]], ids[r, : nv[r]], 20)
+        kk = len(want)
+        assert list(out_i[r, :kk].cpu().numpy()) == [w[0] for w in want]
+        assert np.all(out_s[r, kk:].cpu().numpy() == -1.0)
+
+
+# ----------------------------------------------------------------- prefilter
+def test_prefilter_golden(golden_prefilter):
+    g = golden_prefilter
+    sizes = g["doc_sizes"]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    docs = [g["docs"][off[i]:off[i + 1]] for i in range(len(sizes))]
+    cents = d.Centroids(k=g["centroids"].shape[0], seed=3, vectors=g["centroids"])
+    cindex = d.build_centroid_index(docs, cents)
+    np.testing.assert_array_equal(cindex.post_off.cpu().numpy(), g["post_off"])
+    np.testing.assert_array_equal(cindex.post_docs.cpu().numpy(), g["post_docs"])
+    for t, (probe, kf) in enumerate(g["cases"]):
+        got = d.filter_candidates(cindex, cents, g[f"q{t}"], int(probe), int(kf))
+        np.testing.assert_array_equal(got, g[f"r{t}"], err_msg=f"case {t}")
+
+
+def test_prefilter_random_vs_oracle():
+    rng = np.random.default_rng(21)
+    d_, k = 16, 300
+    docs = [rng.standard_normal((int(rng.integers(1, 12)), d_)) for _ in range(2000)]
+    C = rng.standard_normal((k, d_))
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    cents = d.Centroids(k=k, seed=0, vectors=C)
+    cindex = d.build_centroid_index(docs, cents)
+    post = O.build_centroid_index(docs, C)
+    for t in range(12):
+        Q = rng.standard_normal((int(rng.integers(1, 40)), d_))
+        probe, kf = int(rng.integers(1, 9)), int(rng.choice([1, 7, 100, 4096]))
+        got = d.filter_candidates(cindex, cents, Q, probe, kf)
+        want = O.filter_candidates(post, len(docs), C, Q, probe, kf)
+        np.testing.assert_array_equal(got, want)
+
+
+# ------------------------------------------------------- reference API tests
+def test_end_to_end_golden_build_and_query(golden_e2e):
+    g = golden_e2e
+    for n in range(int(g["n_cases"])):
+        dd, C, L, seed, top_k = (int(x) for x in g[f"e{n}_shape"])
+        sizes = g[f"e{n}_sizes"]
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        X = g[f"e{n}_X"]
+        ids = g[f"e{n}_ids"]
+        docs = [(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+        idx = d.build_index(docs, d.IndexConfig(d=dd, C=C, L=L, seed=seed,
+                                                filter=d.FilterConfig(enabled=False)))
+        np.testing.assert_array_equal(idx.codes.cpu().numpy().astype(np.int64), g[f"e{n}_codes"])
+        for q in range(2):
+            r = d.query(idx, g[f"e{n}_Q"][q], top_k=top_k)
+            assert [x for x, _ in r] == list(g[f"e{n}_top_ids"][q]), f"case {n} q {q}"
+            assert [v for _, v in r] == list(g[f"e{n}_top_scores"][q])
+
+
+def test_reference_index_semantics():  # pkg/tests/test_index.py restated
+    nf = d.FilterConfig(enabled=False)
+    rng = np.random.default_rng(0)
+    S = rng.standard_normal((5, 8))
+    idx = d.build_index([(0, S)], d.IndexConfig(d=8, C=3, L=16, filter=nf))
+    assert d.score_candidate(idx, 0, d.hash_matrix(idx.family, S)) == pytest.approx(1.0)
+    v = np.random.default_rng(1).standard_normal(8)
+    idx = d.build_index([(0, v[None, :])], d.IndexConfig(d=8, C=1, L=32, filter=nf))
+    assert d.score_candidate(idx, 0, d.hash_matrix(idx.family, -v[None, :])) == 0.0
+    with pytest.raises(IndexError):
+        d.score_candidate(idx, 1, d.hash_matrix(idx.family, v[None, :]))
+    idx = d.build_index([(7, np.ones((1, 4)))], d.IndexConfig(d=4, C=2, L=3, filter=nf))
+    assert idx.n_docs == 1 and idx.sketches[0].m == 1 and list(idx.doc_ids) == [7]
+    with pytest.raises(ValueError, match="empty query"):
+        d.query(idx, np.ones((0, 4)), 1)
+    with pytest.raises(ValueError, match="invalid parameter"):
+        d.query(idx, np.ones((1, 4)), 0)
+    with pytest.raises(ValueError, match="dimension"):
+        d.query(idx, np.ones((1, 5)), 1)
+    with pytest.raises(ValueError, match="zero vector"):
+        d.query(idx, np.zeros((1, 4)), 1)
+    with pytest.raises(ValueError, match="zero vector"):
+        d.build_index([(0, np.array([[1.0, 1.0], [0.0, 0.0]]))], d.IndexConfig(d=2, filter=nf))
+    # permutation invariance + threads invariance
+    S = rng.standard_normal((6, 8))
+    Q = rng.standard_normal((2, 8))
+    a = d.build_index([(0, S)], d.IndexConfig(d=8, C=3, L=16, seed=11, filter=nf))
+    b = d.build_index([(0, S[::-1])], d.IndexConfig(d=8, C=3, L=16, seed=11, filter=nf))
+    assert d.query(a, Q, 1) == d.query(b, Q, 1)
+    docs = [(i, rng.standard_normal((int(rng.integers(1, 6)), 8))) for i in range(30)]
+    idx = d.build_index(docs, d.IndexConfig(d=8, C=2, L=16, seed=24, filter=nf))
+    assert d.query(idx, Q, 10, threads=1) == d.query(idx, Q, 10, threads=4)
+    out = d.query(idx, Q, top_k=30)
+    assert len(out) == 30 and [s for _, s in out] == sorted([s for _, s in out], reverse=True)
+
+
+def test_add_sets_equals_full_build():
+    rng = np.random.default_rng(5)
+    docs = [(i * 3, rng.standard_normal((int(rng.integers(1, 30)), 16))) for i in range(120)]
+    cfg = d.IndexConfig(d=16, C=5, L=32, seed=2, filter=d.FilterConfig(enabled=False))
+    full = d.build_index(docs, cfg)
+    part = d.build_index(docs[:50], cfg)
+    d.add_sets(part, docs[50:])
+    Q = rng.standard_normal((4, 20, 16))
+    assert d.query_batch(full, Q, 15) == d.query_batch(part, Q, 15)
+    with pytest.raises(ValueError, match="duplicate"):
+        d.add_sets(part, docs[:1])
+
+
+def test_filtered_query_matches_reference_pipeline():
+    """build_index with the prefilter on: candidates from K5, then K3/K4 over them,
+    equals the oracle pipeline given the same centroids and postings."""
+    rng = np.random.default_rng(8)
+    docs = [(i, rng.standard_normal((int(rng.integers(2, 10)), 16))) for i in range(400)]
+    cfg = d.IndexConfig(d=16, C=4, L=32, seed=1,
+                        filter=d.FilterConfig(enabled=True, centroids=24, probe=2, k_filter=50))
+    idx = d.build_index(docs, cfg)
+    cents, cindex = idx.filter
+    post = cindex.postings
+    codes = idx.codes.cpu().numpy()
+    off = idx.set_off.cpu().numpy()
+    lut = O.sim_lut(4, 32)
+    for t in range(6):
+        Q = rng.standard_normal((int(rng.integers(1, 20)), 16))
+        got = d.query(idx, Q, top_k=10)
+        cand = O.filter_candidates(post, 400, cents.vectors, Q, 2, 50)
+        qc = O.hash_matrix(idx.family.planes, 32, 4, Q)
+        s = O.score_sets_dense(qc, codes, off, lut, sets=cand)
+        want = O.rank_topk(s, [int(i) for i in idx.doc_ids[cand]], 10)
+        assert got == want
+
+
+# ------------------------------------------------------------ larger shapes
+def test_cfg1_shape_sampled_parity():
+    """cfg1 shapes (L=64, C=7, m_i ~ N(70,20) clipped) at 20k sets: 16 query sets
+    exhaustive vs the C oracle, all bit-exact, plus top-100."""
+    from paper_2210_15748_b200 import workloads
+    sizes = workloads.set_sizes(20_000, 70, 20, seed=1)
+    off = workloads.offsets(sizes)
+    rng = np.random.default_rng(2)
+    hot = rng.integers(0, 128, size=64)
+    codes = rng.integers(0, 128, size=(int(off[-1]), 64))
+    m = rng.random(codes.shape) < 0.6
+    codes[m] = np.broadcast_to(hot, codes.shape)[m]
+    q = rng.integers(0, 128, size=(16, 32, 64))
+    qm = rng.random(q.shape) < 0.6
+    q[qm] = np.broadcast_to(hot, q.shape)[qm]
+    idx = _index_from_codes(codes, sizes, 64, 7)
+    s, _ = d.score_matrix(idx, q)
+    want = c_oracle.score(codes, off, q, O.sim_lut(7, 64))
+    np.testing.assert_array_equal(s.cpu().numpy(), want)
+    res = d.query_codes_batch(idx, q, 100)
+    for r in range(16):
+        assert res[r] == O.rank_topk(want[r], np.arange(20_000), 100)
+
+
+def test_mq_variants_bit_exact():
+    """m_q in {1, 7, 8, 31, 33, 64, 100, 128, 129, 200, 300} (one leaf, multi-slot, recursion)."""
+    rng = np.random.default_rng(12)
+    sizes = rng.integers(1, 90, size=300).astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    codes = rng.integers(0, 8, size=(int(off[-1]), 32))
+    idx = _index_from_codes(codes, sizes, 32, 3)
+    lut = O.sim_lut(3, 32)
+    for m_q in (1, 7, 8, 31, 33, 64, 100, 128, 129, 200, 300):
+        q = rng.integers(0, 8, size=(9, m_q, 32))
+        s, mc = d.score_matrix(idx, q, want_counts=True)
+        want, wmc = c_oracle.score(codes, off, q, lut, want_counts=True)
+        np.testing.assert_array_equal(s.cpu().numpy(), want, err_msg=f"m_q={m_q}")
+        np.testing.assert_array_equal(mc.cpu().numpy().astype(np.uint16), wmc)
+        s2, _ = d.score_matrix(idx, q[:2])
+        np.testing.assert_array_equal(s2.cpu().numpy(), want[:2])
