@@ -7,14 +7,19 @@
 //   c_q = max_j sum_t [code_q[t] == code_j[t]]
 // (pinned by the reference's own tests: sketch.py oracle equivalence,
 // test_index.py:130-144), followed by the float64 LUT and numpy's pairwise
-// mean (index.py:216), reproduced bit-for-bit in warp_score() below.
+// mean (index.py:216), reproduced bit-for-bit in lane_score() below.
 //
 // Compare arithmetic is bit-sliced: per 32 tables and C code bits, the
 // mismatch mask is OR_b (q_b XOR x_b) -- C LOP3 + 1 POPC per 32 table
-// compares -- and the running max of matches is a running min of mismatches.
-// Mapping: one warp = one query set, lane = query vector (so max_j needs no
-// cross-lane reduction); set vectors are read from shared memory with
-// broadcast LDS.128.
+// compares -- and the running max of matches is a running min of mismatches
+// (POPC + add + min fuse into VIADDMNMX for L = 64).
+//
+// Mapping: one warp = one query set, lane = query vector, so max_j needs no
+// cross-lane reduction; set vectors are read from shared memory with
+// broadcast LDS.128.  When a set ends, each lane parks its c_q byte in a
+// per-warp shared "slot" row; after 32 sets every lane turns one slot row
+// into one set score (LUT + numpy pairwise order) -- the float64 epilogue is
+// thus spread over lanes instead of being a warp-wide reduction per set.
 #pragma once
 #include "common.cuh"
 
@@ -22,71 +27,80 @@ namespace dsrt {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// ------------------------------------------------------------------ finalize
-// Per-lane running minima of mismatches -> set score (identical in all lanes).
-// Implements numpy pairwise_sum_DOUBLE for n <= 128 (one leaf: 8 strided
-// accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential remainder),
-// preceded by the reduction identity 0.0 and followed by / m_q (np.mean).
 template <int QPL>
-__device__ __forceinline__ double warp_score(const int (&rmin)[QPL], int L, int m_q,
-                                             const double *__restrict__ lut_s,
-                                             uint16_t *__restrict__ mc_row, int mc_q0) {
-    const int lane = threadIdx.x & 31;
-    double a[QPL];
-#pragma unroll
-    for (int s = 0; s < QPL; ++s) {
-        const int qi = lane + 32 * s;
-        const int c = L - rmin[s];
-        a[s] = (qi < m_q) ? lut_s[c] : 0.0;
-        if (mc_row != nullptr && qi < m_q) mc_row[mc_q0 + qi] = static_cast<uint16_t>(c);
-    }
+struct SlotGeom {
+    static constexpr int kRow = 32 * QPL + 4;  // bytes per slot row (+4: bank skew)
+    static constexpr int kBytes = 32 * kRow;   // 32 slots per warp
+};
+
+// numpy pairwise_sum_DOUBLE for one leaf (n <= 128): 8 strided accumulators,
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential remainder; n < 8 sums
+// sequentially from 0.0.  Then the reduction identity 0.0 and / n (np.mean).
+__device__ __forceinline__ double lane_score(const uint8_t *__restrict__ row, int n,
+                                             const double *__restrict__ lut_s) {
     double res;
-    if (m_q < 8) {
+    if (n < 8) {
         res = 0.0;
-        for (int i = 0; i < m_q; ++i) res = __dadd_rn(res, __shfl_sync(kFull, a[0], i));
+        for (int i = 0; i < n; ++i) res = __dadd_rn(res, lut_s[row[i]]);
     } else {
-        const int n8 = m_q - (m_q & 7);
-        const int j = lane & 7;
-        double r = __shfl_sync(kFull, a[0], j);
+        double r[8];
 #pragma unroll
-        for (int ib = 1; ib < 4 * QPL; ++ib) {
-            const double v = __shfl_sync(kFull, a[ib >> 2], ((ib & 3) << 3) + j);
-            if (ib * 8 < n8) r = __dadd_rn(r, v);
+        for (int j = 0; j < 8; ++j) r[j] = lut_s[row[j]];
+        const int n8 = n - (n & 7);
+        for (int i = 8; i < n8; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], lut_s[row[i + j]]);
         }
-        r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 1));
-        r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 2));
-        r = __dadd_rn(r, __shfl_xor_sync(kFull, r, 4));
-        res = r;
-        const int rem = m_q & 7;
-#pragma unroll
-        for (int t = 0; t < 7; ++t) {
-            const int i = n8 + t;  // < 32*QPL when t < rem
-            double v = 0.0;
-#pragma unroll
-            for (int s = 0; s < QPL; ++s) {
-                const double w = __shfl_sync(kFull, a[s], i & 31);
-                if ((i >> 5) == s) v = w;
-            }
-            if (t < rem) res = __dadd_rn(res, v);
-        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (int i = n8; i < n; ++i) res = __dadd_rn(res, lut_s[row[i]]);
     }
-    res = __dadd_rn(0.0, res);
-    return __ddiv_rn(res, static_cast<double>(m_q));
+    return __ddiv_rn(__dadd_rn(0.0, res), static_cast<double>(n));
 }
 
-// Mismatch count of one query (registers) vs one record (uint32 words).
-template <int K, int W>
-__device__ __forceinline__ int mismatches(const uint32_t (&q)[K * W], const uint32_t *x) {
-    int mm = 0;
+// Per-warp deferred epilogue: 32 slot rows of c_q bytes.
+template <int QPL>
+struct Slots {
+    uint8_t *buf;        // this warp's SlotGeom<QPL>::kBytes
+    int n = 0;           // filled slots (warp-uniform)
+    uint32_t valid = 0;  // bit i: slot i holds a valid set
+
+    // park the finished set's c_q (= L - min mismatches) in slot n
+    __device__ __forceinline__ void push(const int (&rmin)[QPL], int L, int m_q, bool ok) {
+        const int lane = threadIdx.x & 31;
+        uint8_t *row = buf + n * SlotGeom<QPL>::kRow;
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-        uint32_t acc = q[w] ^ x[w];
-#pragma unroll
-        for (int b = 1; b < K; ++b) acc |= q[b * W + w] ^ x[b * W + w];
-        mm += __popc(acc);
+        for (int s = 0; s < QPL; ++s) {
+            const int qi = lane + 32 * s;
+            if (qi < m_q) row[qi] = static_cast<uint8_t>(L - rmin[s]);
+        }
+        valid |= (ok ? 1u : 0u) << n;
+        ++n;
     }
-    return mm;
-}
+
+    // lane i < n scores slot i -> out[col0 + i]; optional uint16 max counts
+    __device__ __forceinline__ void flush(int m_q, const double *__restrict__ lut_s,
+                                          double *__restrict__ out_row, int64_t col0,
+                                          uint16_t *__restrict__ mc, int64_t mc_row0,
+                                          int mc_stride, int mc_q0) {
+        const int lane = threadIdx.x & 31;
+        __syncwarp();
+        if (lane < n) {
+            const uint8_t *row = buf + lane * SlotGeom<QPL>::kRow;
+            const bool ok = (valid >> lane) & 1u;
+            if (out_row != nullptr)
+                out_row[col0 + lane] =
+                    ok ? lane_score(row, m_q, lut_s) : __longlong_as_double(0x7ff8000000000000ll);
+            if (mc != nullptr && ok) {
+                uint16_t *dst = mc + (mc_row0 + col0 + lane) * mc_stride + mc_q0;
+                for (int i = 0; i < m_q; ++i) dst[i] = row[i];
+            }
+        }
+        __syncwarp();
+        n = 0;
+        valid = 0;
+    }
+};
 
 template <int K, int W, int QPL>
 __device__ __forceinline__ void load_queries(uint32_t (&q)[QPL][K * W],
@@ -104,13 +118,27 @@ __device__ __forceinline__ void load_queries(uint32_t (&q)[QPL][K * W],
     }
 }
 
+// Mismatch count of one query (registers) vs one record (uint32 words).
+template <int K, int W>
+__device__ __forceinline__ int mismatches(const uint32_t (&q)[K * W], const uint32_t *x) {
+    int mm = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        uint32_t acc = q[w] ^ x[w];
+#pragma unroll
+        for (int b = 1; b < K; ++b) acc |= q[b * W + w] ^ x[b * W + w];
+        mm += __popc(acc);
+    }
+    return mm;
+}
+
 // Process vectors [0, nv) of a shared-memory record array.
 template <int K, int W, int QPL>
 __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], int (&rmin)[QPL],
                                              const uint32_t *xs, int nv) {
     constexpr int R = ((K * W) + 3) & ~3;
     const uint4 *x4 = reinterpret_cast<const uint4 *>(xs);
-#pragma unroll 2
+#pragma unroll 4
     for (int i = 0; i < nv; ++i) {
         uint4 xv[R / 4];
 #pragma unroll
@@ -121,6 +149,22 @@ __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], in
     }
 }
 
+// Lane-distributed window of set_off: lane l holds set_off[base + l].
+struct OffWindow {
+    const int64_t *off;
+    int64_t base, limit;  // valid indices <= limit
+    int64_t v;
+    __device__ __forceinline__ void load(int64_t b) {
+        base = b;
+        const int64_t i = b + (threadIdx.x & 31);
+        v = i <= limit ? __ldg(off + i) : INT64_MAX;
+    }
+    __device__ __forceinline__ int64_t get(int64_t i) {  // warp-uniform i
+        if (i - base >= 32) load(i);
+        return __shfl_sync(kFull, v, static_cast<int>(i - base));
+    }
+};
+
 // ------------------------------------------------------- exhaustive (shared)
 constexpr int kTileVec = 128;  // vectors per TMA bulk tile
 constexpr int kStages = 4;     // smem ring depth
@@ -129,12 +173,20 @@ template <int K, int W>
 constexpr int tile_bytes() {
     return kTileVec * (((K * W) + 3) & ~3) * 4;
 }
+template <int K, int W, int QPL, int NW>
+constexpr size_t all_smem_static() {
+    return kStages * tile_bytes<K, W>() + 2 * kStages * sizeof(uint64_t) +
+           NW * SlotGeom<QPL>::kBytes;
+}
 
 // grid: (query-set groups of NW, set chunks).  One producer warp streams the
 // chunk's plane records through a kStages ring with cp.async.bulk (TMA);
 // NW consumer warps (one query set each) share every tile.
+#ifndef DSRT_ALL_MINB
+#define DSRT_ALL_MINB 3
+#endif
 template <int K, int W, int QPL, int NW>
-__global__ void __launch_bounds__((NW + 1) * 32)
+__global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     score_all_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
                      int64_t set_begin, int64_t set_end, const uint32_t *__restrict__ qrecs,
                      int64_t n_qsets, int m_q, int L, const double *__restrict__ lut,
@@ -145,7 +197,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     uint32_t *tiles = reinterpret_cast<uint32_t *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * tile_bytes<K, W>());
     uint64_t *empty = full + kStages;
-    double *lut_s = reinterpret_cast<double *>(empty + kStages);
+    uint8_t *slot_mem = reinterpret_cast<uint8_t *>(empty + kStages);
+    double *lut_s = reinterpret_cast<double *>(slot_mem + NW * SlotGeom<QPL>::kBytes);
     __shared__ int64_t bounds[2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -197,21 +250,27 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     int rmin[QPL];
 #pragma unroll
     for (int s = 0; s < QPL; ++s) rmin[s] = L;
+    Slots<QPL> slots{slot_mem + warp * SlotGeom<QPL>::kBytes};
+    double *out_row = (active && scores != nullptr) ? scores + qset * ld : nullptr;
+    uint16_t *mc = active ? maxcounts : nullptr;
+    OffWindow win{set_off, 0, s_hi, 0};
+    win.load(s_lo + 1);
 
-    int64_t s = s_lo;
-    int64_t s_end_v = __ldg(set_off + s + 1);
+    int64_t s = s_lo, slot_col = s_lo - set_begin;
+    int64_t s_end_v = win.get(s + 1);
     int64_t v = vbeg;
-    auto finalize = [&]() {
-        if (active) {
-            uint16_t *mc_row =
-                maxcounts ? maxcounts + (qset * ld + (s - set_begin)) * mc_stride : nullptr;
-            const double sc = warp_score<QPL>(rmin, L, m_q, lut_s, mc_row, mc_q0);
-            if (scores != nullptr && lane == 0) scores[qset * ld + (s - set_begin)] = sc;
-        }
+    auto finish_set = [&]() {
+        if (active) slots.push(rmin, L, m_q, true);
+        else ++slots.n;
 #pragma unroll
         for (int i = 0; i < QPL; ++i) rmin[i] = L;
         ++s;
-        if (s < s_hi) s_end_v = __ldg(set_off + s + 1);
+        if (slots.n == 32) {
+            if (active) slots.flush(m_q, lut_s, out_row, slot_col, mc, qset * ld, mc_stride, mc_q0);
+            slots.n = 0;
+            slot_col += 32;
+        }
+        if (s < s_hi) s_end_v = win.get(s + 1);
     };
 
     for (int64_t t = 0; t < n_tiles; ++t) {
@@ -221,16 +280,18 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         const int64_t tv0 = vbeg + t * kTileVec;
         const int64_t tv1 = tmin<int64_t>(tv0 + kTileVec, vend);
         while (v < tv1) {
-            const int64_t stop = min(s_end_v, tv1);
+            const int64_t stop = tmin(s_end_v, tv1);
             if (active && stop > v)
                 scan_vectors<K, W, QPL>(q, rmin, tile + (v - tv0) * R, static_cast<int>(stop - v));
             v = stop;
-            while (s < s_hi && v == s_end_v) finalize();
+            while (s < s_hi && v == s_end_v) finish_set();
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
     }
-    while (s < s_hi) finalize();  // trailing empty sets (validated away upstream)
+    while (s < s_hi) finish_set();  // trailing empty sets (validated away upstream)
+    if (active && slots.n > 0)
+        slots.flush(m_q, lut_s, out_row, slot_col, mc, qset * ld, mc_stride, mc_q0);
 }
 
 // --------------------------------------------------------- candidate lists
@@ -242,12 +303,19 @@ template <int K, int W>
 constexpr int piece_vec() {
     return kPieceBytes / ((((K * W) + 3) & ~3) * 4);
 }
+template <int QPL>
+constexpr size_t cand_smem_static() {
+    return kCandWarps * (kBufs * kPieceBytes + kBufs * sizeof(uint64_t) + SlotGeom<QPL>::kBytes);
+}
 
 // One warp = (query set, run of candidate slots).  Each warp streams its
 // candidates' records through a private kBufs-deep ring filled by
 // cp.async.bulk issued from lane 0.
+#ifndef DSRT_CAND_MINB
+#define DSRT_CAND_MINB 3
+#endif
 template <int K, int W, int QPL>
-__global__ void __launch_bounds__(kCandWarps * 32)
+__global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     score_cand_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
                       int64_t n_sets, const int64_t *__restrict__ cand,
                       const int32_t *__restrict__ n_cand, int64_t cand_ld,
@@ -260,9 +328,10 @@ __global__ void __launch_bounds__(kCandWarps * 32)
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t *bufs = reinterpret_cast<uint32_t *>(smem) + warp * (kBufs * PV * R);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + kCandWarps * kBufs * kPieceBytes) + warp * kBufs;
-    double *lut_s = reinterpret_cast<double *>(
-        smem + kCandWarps * kBufs * kPieceBytes + kCandWarps * kBufs * sizeof(uint64_t));
+    uint8_t *after_bufs = smem + kCandWarps * kBufs * kPieceBytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(after_bufs) + warp * kBufs;
+    uint8_t *slot_mem = after_bufs + kCandWarps * kBufs * sizeof(uint64_t);
+    double *lut_s = reinterpret_cast<double *>(slot_mem + kCandWarps * SlotGeom<QPL>::kBytes);
 
     if (lane == 0) {
         for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
@@ -276,7 +345,7 @@ __global__ void __launch_bounds__(kCandWarps * 32)
     if (qset >= n_qsets) return;
     const int64_t nc = n_cand ? tmin<int64_t>(__ldg(n_cand + qset), cand_ld) : cand_ld;
     const int64_t e_lo = (gw % runs_per_q) * run_len;
-    const int64_t e_hi = min(e_lo + run_len, nc);
+    const int64_t e_hi = tmin(e_lo + run_len, nc);
     if (e_lo >= e_hi) return;
 
     uint32_t q[QPL][K * W];
@@ -284,6 +353,8 @@ __global__ void __launch_bounds__(kCandWarps * 32)
     int rmin[QPL];
 #pragma unroll
     for (int s = 0; s < QPL; ++s) rmin[s] = L;
+    Slots<QPL> slots{slot_mem + warp * SlotGeom<QPL>::kBytes};
+    double *out_row = scores != nullptr ? scores + qset * cand_ld : nullptr;
 
     auto set_of = [&](int64_t e) -> int64_t {
         return cand ? __ldg(cand + qset * cand_ld + e) : e;
@@ -294,7 +365,6 @@ __global__ void __launch_bounds__(kCandWarps * 32)
     int64_t pv = pvalid ? __ldg(set_off + ps) : 0, pvend = pvalid ? __ldg(set_off + ps + 1) : 0;
     int64_t issued = 0;
     auto issue = [&]() {  // issue the next piece (pe, [pv, ..)) into buffer issued % kBufs
-        // skip finished / invalid candidates: they need no data but still a piece slot
         const int b = static_cast<int>(issued % kBufs);
         const int64_t nvec = pe < e_hi ? tmin<int64_t>(PV, pvend - pv) : 0;
         if (lane == 0) {
@@ -320,7 +390,7 @@ __global__ void __launch_bounds__(kCandWarps * 32)
         }
     };
     // consumer iterator
-    int64_t ce = e_lo, cs = set_of(ce);
+    int64_t ce = e_lo, cs = set_of(ce), slot_col = e_lo;
     bool cvalid = cs >= 0 && cs < n_sets;
     int64_t cv = cvalid ? __ldg(set_off + cs) : 0, cvend = cvalid ? __ldg(set_off + cs + 1) : 0;
     int64_t consumed = 0;
@@ -333,13 +403,13 @@ __global__ void __launch_bounds__(kCandWarps * 32)
         ++consumed;
         cv += nvec;
         if (cv >= cvend) {  // candidate complete
-            const double sc = warp_score<QPL>(
-                rmin, L, m_q, lut_s,
-                maxcounts ? maxcounts + (qset * cand_ld + ce) * mc_stride : nullptr, mc_q0);
-            if (scores != nullptr && lane == 0)
-                scores[qset * cand_ld + ce] = cvalid ? sc : __longlong_as_double(0x7ff8000000000000ll);
+            slots.push(rmin, L, m_q, cvalid);
 #pragma unroll
             for (int i = 0; i < QPL; ++i) rmin[i] = L;
+            if (slots.n == 32) {
+                slots.flush(m_q, lut_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
+                slot_col += 32;
+            }
             ++ce;
             if (ce < e_hi) {
                 cs = set_of(ce);
@@ -351,6 +421,8 @@ __global__ void __launch_bounds__(kCandWarps * 32)
         __syncwarp();
         issue();  // refill the buffer just consumed
     }
+    if (slots.n > 0)
+        slots.flush(m_q, lut_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
     // drain: wait for outstanding pieces so no bulk copy outlives the CTA
     while (consumed < issued) {
         const int b = static_cast<int>(consumed % kBufs);
@@ -366,8 +438,7 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
                       double *scores, int64_t ld, uint16_t *mc, int mc_stride, int mc_q0,
                       cudaStream_t st) {
     constexpr int NW = 8;
-    const size_t smem = kStages * tile_bytes<K, W>() + 2 * kStages * sizeof(uint64_t) +
-                        (L + 1) * sizeof(double);
+    const size_t smem = all_smem_static<K, W, QPL, NW>() + (L + 1) * sizeof(double);
     auto kern = score_all_kernel<K, W, QPL, NW>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = (n_qsets + NW - 1) / NW;
@@ -393,8 +464,7 @@ static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_s
                        const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
                        const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
                        double *scores, uint16_t *mc, int mc_stride, int mc_q0, cudaStream_t st) {
-    const size_t smem = kCandWarps * kBufs * kPieceBytes + kCandWarps * kBufs * sizeof(uint64_t) +
-                        (L + 1) * sizeof(double);
+    const size_t smem = cand_smem_static<QPL>() + (L + 1) * sizeof(double);
     auto kern = score_cand_kernel<K, W, QPL>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -467,7 +537,4 @@ int run_w(const ScoreArgs &a, int W, int qpl, cudaStream_t st) {
     return DSRT_EUNSUPPORTED;
 }
 
-
-template <int K>
-int run_w(const ScoreArgs &a, int W, int qpl, cudaStream_t st);
 }  // namespace dsrt
