@@ -342,6 +342,198 @@ def run_gpu(args):
     return 0
 
 
+
+# ------------------------------------------------------------- cfg4 / cfg3
+def _clocks_and_time(step_fn, steps, warmup, local, stream):
+    import torch
+
+    for _ in range(warmup):
+        step_fn(False)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step_fn(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / steps, clocks.stop()
+
+
+def run_cfg4(args):
+    """cfg4: 8M sets (m_i ~ N(70,25) clipped), codes only (L=32, C=8), 1,024 query sets,
+    exhaustive scoring, top-1,000 (chunked score buffer + top-k merge)."""
+    import torch
+
+    import paper_2210_15748_b200 as d
+    from paper_2210_15748_b200 import _lib, engine, workloads
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n_sets, n_q, m_q, L, C, top_k = args.sets or 8_000_000, 1024, 32, 32, 8, 1000
+    sizes = workloads.set_sizes(n_sets, 70, 25, seed=400)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
+    t_gen = time.perf_counter()
+    recs, Qv = workloads.gpu_codes_only(sizes, cfg, n_centroids=262_144, n_qsets=n_q, m_q=m_q,
+                                        seed=401, device=dev)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
+    Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
+    mode = d.lsh.default_mode(Q2.dtype)
+    planes = idx.family.device_planes(mode, dev)
+    stream = torch.cuda.current_stream()
+    chunk = max(1, min(n_sets, args.score_buffer // (8 * n_q)))
+    buf = torch.empty((n_q, chunk), dtype=torch.float64, device=dev)
+    kev = []
+
+    def step(timed):
+        _, qrecs, _ = engine.hash_vectors(Q2, planes, mode, L, C, want_codes=False,
+                                          check_zero=False)
+        ps, pi = [], []
+        for s0 in range(0, n_sets, chunk):
+            s1 = min(n_sets, s0 + chunk)
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            engine.score_all(idx.records, idx.set_off, qrecs, m_q, L, C, idx.lut_dev,
+                             set_begin=s0, set_end=s1, scores=buf, ld=chunk)
+            if timed:
+                e1.record(stream)
+                kev.append((e0, e1, s1 - s0))
+            a, b, _ = engine.topk(buf if s1 - s0 == chunk else buf[:, : s1 - s0].contiguous(),
+                                  top_k, ids=idx.doc_ids_dev[s0:s1])
+            ps.append(a)
+            pi.append(b)
+        return engine.topk(torch.cat(ps, 1).contiguous(), top_k, ids=torch.cat(pi, 1).contiguous())
+
+    ms, clk = _clocks_and_time(step, args.steps, max(3, args.warmup), local, stream)
+    off = idx.set_off
+    total_vec = int(off[-1].item())
+    so = idx.set_off.cpu().numpy()
+    kern = []
+    for e0, e1, w in kev:
+        kern.append((e0.elapsed_time(e1), w))
+    k_ms = float(np.sum([k for k, _ in kern])) / args.steps
+    launches_per_step = len(kern) // args.steps
+    compares = float(n_q) * m_q * L * total_vec
+    mb = engine.microbench_int()
+    p_int = mb["lop3_ops_per_s"] * 4.0
+    achieved = compares / (k_ms * 1e-3)
+    value = n_q * n_sets / (ms * 1e-3)
+    rec_bytes = total_vec * engine.record_words(L, C) * 4
+    line = {
+        "metric": "set-pair scores/sec (cfg4: 8M sets x 1024 query sets, L=32 C=8, exhaustive, top-1000)",
+        "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic (cfg4-shaped codes, generated on GPU)",
+        "config": {"workload": "cfg4", "n_sets": n_sets, "n_qsets": n_q, "m_q": m_q, "L": L, "C": C,
+                   "top_k": top_k, "vectors": total_vec, "score_chunk_sets": chunk,
+                   "l2": "inputs larger than L2 (17.9 GB records)", "generation_s": t_gen},
+        "roofline": {"bound": "int", "unit": "Gcompare/s", "achieved": achieved / 1e9,
+                     "peak": p_int / 1e9, "frac": achieved / p_int, "traffic": None,
+                     "kernel": "score_all_kernel<8,1,1,8>", "kernel_ms_per_step": k_ms,
+                     "launches_per_step": launches_per_step,
+                     "per_step": {"compares": compares, "code_bytes_per_pass": rec_bytes},
+                     "achieved_hbm_gbs_code_stream": rec_bytes / (k_ms * 1e-3) / 1e9,
+                     "peak_source": "measured in-run: LOP3 lane-ops/s x 4", "int_microbench": mb},
+        "clocks": clk, "gpu_launches": (2 + 2 * launches_per_step) * args.steps,
+    }
+    del so
+    print(json.dumps(line))
+    return 0
+
+
+def run_cfg3(args):
+    """cfg3: 1M sets (~70M fp16 vectors) from 65,536 centroids; prefilter probe 4,
+    k_filter 4,096; L=32, C=7; top-100.  Batch 256 throughput + batch-1 p50/p99."""
+    import torch
+
+    import paper_2210_15748_b200 as d
+    from paper_2210_15748_b200 import _lib, engine, prefilter, workloads
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n_sets, m_q, L, C, top_k, probe, k_filter = args.sets or 1_000_000, 32, 32, 7, 100, 4, 4096
+    n_cent = 65_536
+    sizes = workloads.set_sizes(n_sets, 70, 20, seed=500)
+    off = workloads.offsets(sizes)
+    t_gen = time.perf_counter()
+    X, cents = workloads.gpu_mixture(int(off[-1]), n_cent, 128, 0.05, seed=501,
+                                     dtype=torch.float16, device=dev)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0,
+                        filter=d.FilterConfig(enabled=True, centroids=n_cent, probe=probe,
+                                              k_filter=k_filter))
+    idx = d.build_from_vectors(X, sizes, np.arange(n_sets), cfg, keep_codes=False,
+                               hash_mode=_lib.HASH_F32)
+    cvec = cents.double()
+    cvec = cvec / cvec.norm(dim=1, keepdim=True)
+    centroids = prefilter.Centroids(k=n_cent, seed=0, vectors=cvec.cpu().numpy())
+    cindex = prefilter.build_centroid_index_fast(X, centroids, idx.set_off, n_sets)
+    idx.filter = (centroids, cindex)
+    Qall = workloads.gpu_queries(X, off, 256 + 1000, m_q, seed=502)
+    del X
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    stream = torch.cuda.current_stream()
+    Qb = Qall[:256]
+    kev = {"prefilter": [], "score": []}
+
+    def step(timed):
+        # one batch of 256 query sets through hash -> K5 -> K3 (candidates) -> K4
+        Q2 = Qb.reshape(-1, 128)
+        _, qrecs = d.lsh.hash_device(idx.family, Q2, want_codes=False, check_zero=False)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
+        if timed:
+            e[0].record(stream)
+        cand, n_cand = prefilter.filter_candidates_device(cindex, centroids, Q2, m_q, probe,
+                                                          k_filter)
+        if timed:
+            e[1].record(stream)
+        scores, _ = engine.score_candidates(idx.records, idx.set_off, qrecs, m_q, L, C,
+                                            idx.lut_dev, cand=cand, n_cand=n_cand)
+        if timed:
+            e[2].record(stream)
+            kev["prefilter"].append((e[0], e[1]))
+            kev["score"].append((e[1], e[2]))
+        return engine.topk(scores, top_k, ids=idx.doc_ids_dev[cand.clamp(min=0)], n_valid=n_cand)
+
+    ms, clk = _clocks_and_time(step, args.steps, max(3, args.warmup), local, stream)
+    pf_ms = float(np.mean([a.elapsed_time(b) for a, b in kev["prefilter"]]))
+    sc_ms = float(np.mean([a.elapsed_time(b) for a, b in kev["score"]]))
+    # batch-1 latency through the public API (host query in, host results out)
+    lat = []
+    Qh = Qall[256:].cpu()
+    for i in range(min(args.latency_queries, Qh.shape[0])):
+        t = time.perf_counter()
+        d.query(idx, Qh[i], top_k)
+        lat.append(time.perf_counter() - t)
+    lat = np.array(lat[5:]) * 1e3
+    tot_cand_vec = None
+    mb = engine.microbench_int()
+    line = {
+        "metric": "query sets/sec (cfg3: 1M sets, prefilter probe 4 / k_filter 4096, L=32 C=7, top-100, batch 256)",
+        "value": 256 / (ms * 1e-3), "unit": "query sets/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+u8", "data": "synthetic (cfg3-shaped, generated on GPU)",
+        "config": {"workload": "cfg3", "n_sets": n_sets, "vectors": int(off[-1]), "centroids": n_cent,
+                   "probe": probe, "k_filter": k_filter, "batch": 256, "top_k": top_k,
+                   "setup_s": t_gen},
+        "batch1_latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                              "n": int(lat.size)},
+        "kernel_ms": {"prefilter": pf_ms, "score_candidates": sc_ms},
+        "clocks": clk, "int_microbench": mb,
+    }
+    del tot_cand_vec
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -349,9 +541,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 3, 4])
+    ap.add_argument("--sets", type=int, default=0, help="override N (cfg3/cfg4)")
+    ap.add_argument("--score-buffer", type=int, default=8 << 30)
+    ap.add_argument("--latency-queries", type=int, default=1000)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 4:
+        return run_cfg4(args)
+    if args.config == 3:
+        return run_cfg3(args)
     return run_gpu(args)
 
 

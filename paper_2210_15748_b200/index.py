@@ -213,6 +213,20 @@ def build_from_codes(codes: torch.Tensor, sizes: np.ndarray, doc_ids, config: In
         doc_ids_dev=torch.from_numpy(ids.view(np.int64)).to(codes.device))
 
 
+def build_from_records(records: torch.Tensor, sizes: np.ndarray, doc_ids, config: IndexConfig,
+                       filt=None) -> DessertIndex:
+    """Adopt device plane records (sum m_i, R) directly (codes-only configs)."""
+    family = sample_srp_family(config.d, config.C, config.L, config.seed)
+    lookup = build_sim_lookup(config.C, config.L)
+    set_off = _layout(sizes, records.device)
+    ids = np.asarray(doc_ids, dtype=np.uint64)
+    return DessertIndex(
+        config=config, family=family, lookup=lookup, doc_ids=ids,
+        sizes=np.asarray(sizes, dtype=np.int64), filter=filt, records=records, set_off=set_off,
+        codes=None, lut_dev=torch.from_numpy(lookup.table).to(records.device),
+        doc_ids_dev=torch.from_numpy(ids.view(np.int64)).to(records.device))
+
+
 def build_index(docs, config: IndexConfig, device="cuda", keep_codes: bool = True,
                 hash_mode: int | None = None) -> DessertIndex:
     """Sketch every (doc_id, vector set) pair on the GPU and build the optional prefilter.
@@ -479,6 +493,7 @@ def score_matrix(index: DessertIndex, qcodes, sets=None, want_counts=False):
 
 
 __all__ = ["FilterConfig", "IndexConfig", "PROFILES", "apply_profile", "DessertIndex",
-           "RankedResults", "build_index", "build_from_vectors", "build_from_codes", "add_sets",
+           "RankedResults", "build_index", "build_from_vectors", "build_from_codes",
+           "build_from_records", "add_sets",
            "query", "query_batch", "query_codes_batch", "score_candidate", "score_matrix",
            "default_scorer"]

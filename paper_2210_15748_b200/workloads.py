@@ -125,3 +125,65 @@ def gpu_queries(X, off: np.ndarray, n_qsets: int, m_q: int, seed: int, noise: fl
     v = base + noise * torch.randn(base.shape, generator=g, device=X.device)
     v = (v / v.norm(dim=1, keepdim=True)).to(X.dtype)
     return v.reshape(n_qsets, m_q, X.shape[1])
+
+
+def gpu_codes_only(sizes, config, n_centroids: int, n_qsets: int, m_q: int, seed: int,
+                   device="cuda", chunk: int = 1 << 23, noise: float = 0.05):
+    """cfg4 synthesis: hash mixture vectors chunk by chunk straight into plane
+    records (no raw vectors kept), collecting the query-source rows on the way.
+
+    Returns (records (sum m_i, R) int32, query vectors (n_qsets, m_q, d) fp16).
+    Hashing uses the float32 SIMT kernel (input synthesis; parity is defined
+    on the resulting codes, which the oracle reads back from the records).
+    """
+    import torch
+
+    from . import _lib, engine
+    from .lsh import sample_srp_family
+
+    fam = sample_srp_family(config.d, config.C, config.L, config.seed)
+    planes = fam.device_planes(_lib.HASH_F32, device)
+    off = offsets(sizes)
+    n_vec = int(off[-1])
+    R = engine.record_words(config.L, config.C)
+    recs = torch.empty((n_vec, R), dtype=torch.int32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    cents = torch.randn(n_centroids, config.d, generator=g, device=device)
+    cents = cents / cents.norm(dim=1, keepdim=True)
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, len(sizes), size=n_qsets)
+    rows = (off[src][:, None] + (rng.random((n_qsets, m_q)) * sizes[src][:, None]).astype(np.int64))
+    flat = rows.reshape(-1)
+    order = np.argsort(flat, kind="stable")
+    sorted_rows = flat[order]
+    gathered = torch.empty((flat.size, config.d), dtype=torch.float32, device=device)
+    for lo in range(0, n_vec, chunk):
+        hi = min(n_vec, lo + chunk)
+        idx = torch.randint(0, n_centroids, (hi - lo,), generator=g, device=device)
+        v = cents[idx] + noise * torch.randn(hi - lo, config.d, generator=g, device=device)
+        X = (v / v.norm(dim=1, keepdim=True)).to(torch.float16)
+        _, r, _ = engine.hash_vectors(X, planes, _lib.HASH_F32, config.L, config.C,
+                                      want_codes=False, check_zero=False)
+        recs[lo:hi] = r
+        a, b = np.searchsorted(sorted_rows, [lo, hi])
+        if b > a:
+            sel = torch.from_numpy(sorted_rows[a:b] - lo).to(device)
+            dst = torch.from_numpy(order[a:b]).to(device)
+            gathered[dst] = X[sel].float()
+        del X, v, idx
+    q = gathered + 0.1 * torch.randn(gathered.shape, generator=g, device=device)
+    q = (q / q.norm(dim=1, keepdim=True)).to(torch.float16)
+    return recs, q.reshape(n_qsets, m_q, config.d)
+
+
+def records_to_codes(recs: np.ndarray, L: int, C: int) -> np.ndarray:
+    """Host inverse of the plane-record layout (test infrastructure / parity sampling)."""
+    W = (L + 31) // 32
+    recs = np.asarray(recs).view(np.uint32)
+    codes = np.zeros((recs.shape[0], L), dtype=np.int64)
+    for t in range(L):
+        w, bit = divmod(t, 32)
+        for b in range(C):
+            codes[:, t] |= ((recs[:, b * W + w] >> np.uint32(bit)) & np.uint32(1)).astype(np.int64) << b
+    return codes
