@@ -1,4 +1,6 @@
 // K3 dispatch + C ABI (kernels in score_kernels.cuh, instantiated in score_inst_*.cu).
+#include <cstdlib>
+
 #include "score_kernels.cuh"
 
 namespace dsrt {
@@ -79,6 +81,7 @@ static int run_k(const ScoreArgs &a, int C, int qpl, cudaStream_t st) {
 // m_q <= 128 runs in one pass; larger m_q runs 128-query slices writing
 // maxcounts, then finalize_kernel applies numpy's recursive pairwise sum.
 static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
+    if (const char *e = getenv("DSRT_QS")) a.qs_override = atoi(e);
     DSRT_REQUIRE(a.m_q >= 1, DSRT_EINVAL, "empty query: need at least one query vector");
     DSRT_REQUIRE(a.L >= 1 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", a.L, C);
     if (a.n_qsets == 0) return DSRT_OK;

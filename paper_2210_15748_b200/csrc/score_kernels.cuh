@@ -173,19 +173,20 @@ template <int K, int W>
 constexpr int tile_bytes() {
     return kTileVec * (((K * W) + 3) & ~3) * 4;
 }
-template <int K, int W, int QPL, int NW>
+template <int K, int W, int QPL, int NW, int QS>
 constexpr size_t all_smem_static() {
     return kStages * tile_bytes<K, W>() + 2 * kStages * sizeof(uint64_t) +
-           NW * SlotGeom<QPL>::kBytes;
+           NW * QS * SlotGeom<QPL>::kBytes;
 }
 
-// grid: (query-set groups of NW, set chunks).  One producer warp streams the
-// chunk's plane records through a kStages ring with cp.async.bulk (TMA);
-// NW consumer warps (one query set each) share every tile.
 #ifndef DSRT_ALL_MINB
-#define DSRT_ALL_MINB 3
+#define DSRT_ALL_MINB 2
 #endif
-template <int K, int W, int QPL, int NW>
+// grid: (query-set groups of NW*QS, set chunks).  One producer warp streams the
+// chunk's plane records through a kStages ring with cp.async.bulk (TMA);
+// NW consumer warps share every tile, each register-blocking QS query sets
+// (lane l holds query l of each), so one broadcast LDS feeds QS pairs.
+template <int K, int W, int QPL, int NW, int QS>
 __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     score_all_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
                      int64_t set_begin, int64_t set_end, const uint32_t *__restrict__ qrecs,
@@ -193,12 +194,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
                      double *__restrict__ scores, int64_t ld, uint16_t *__restrict__ maxcounts,
                      int mc_stride, int mc_q0, int n_chunks) {
     constexpr int R = ((K * W) + 3) & ~3;
+    constexpr int S = QS * QPL;  // register slots per lane
     extern __shared__ __align__(128) uint8_t smem[];
     uint32_t *tiles = reinterpret_cast<uint32_t *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * tile_bytes<K, W>());
     uint64_t *empty = full + kStages;
     uint8_t *slot_mem = reinterpret_cast<uint8_t *>(empty + kStages);
-    double *lut_s = reinterpret_cast<double *>(slot_mem + NW * SlotGeom<QPL>::kBytes);
+    double *lut_s = reinterpret_cast<double *>(slot_mem + NW * QS * SlotGeom<QPL>::kBytes);
     __shared__ int64_t bounds[2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -242,32 +244,50 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         return;
     }
 
-    // -------------------------------------- consumers: one query set per warp
-    const int64_t qset = static_cast<int64_t>(blockIdx.x) * NW + warp;
-    const bool active = qset < n_qsets;
-    uint32_t q[QPL][K * W];
-    load_queries<K, W, QPL>(q, qrecs, active ? qset : 0, m_q, active);
-    int rmin[QPL];
+    // ------------------------- consumers: QS query sets per warp, lane = query
+    const int64_t qset0 = (static_cast<int64_t>(blockIdx.x) * NW + warp) * QS;
+    const bool any_active = qset0 < n_qsets;
+    uint32_t q[S][K * W];
 #pragma unroll
-    for (int s = 0; s < QPL; ++s) rmin[s] = L;
-    Slots<QPL> slots{slot_mem + warp * SlotGeom<QPL>::kBytes};
-    double *out_row = (active && scores != nullptr) ? scores + qset * ld : nullptr;
-    uint16_t *mc = active ? maxcounts : nullptr;
+    for (int j = 0; j < QS; ++j) {
+        const bool act = qset0 + j < n_qsets;
+        load_queries<K, W, QPL>(*reinterpret_cast<uint32_t(*)[QPL][K * W]>(&q[j * QPL][0]), qrecs,
+                                act ? qset0 + j : 0, m_q, act);
+    }
+    int rmin[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) rmin[s] = L;
+    Slots<QPL> slots[QS];
+#pragma unroll
+    for (int j = 0; j < QS; ++j) slots[j].buf = slot_mem + (warp * QS + j) * SlotGeom<QPL>::kBytes;
     OffWindow win{set_off, 0, s_hi, 0};
     win.load(s_lo + 1);
 
     int64_t s = s_lo, slot_col = s_lo - set_begin;
     int64_t s_end_v = win.get(s + 1);
     int64_t v = vbeg;
-    auto finish_set = [&]() {
-        if (active) slots.push(rmin, L, m_q, true);
-        else ++slots.n;
+    auto flush_all = [&]() {
 #pragma unroll
-        for (int i = 0; i < QPL; ++i) rmin[i] = L;
+        for (int j = 0; j < QS; ++j) {
+            const int64_t qs = qset0 + j;
+            if (qs < n_qsets)
+                slots[j].flush(m_q, lut_s, scores ? scores + qs * ld : nullptr, slot_col, maxcounts,
+                               qs * ld, mc_stride, mc_q0);
+            slots[j].n = 0;
+            slots[j].valid = 0;
+        }
+    };
+    auto finish_set = [&]() {
+#pragma unroll
+        for (int j = 0; j < QS; ++j)
+            slots[j].push(*reinterpret_cast<const int(*)[QPL]>(&rmin[j * QPL]), L, m_q, true);
+#pragma unroll
+        for (int i = 0; i < S; ++i) rmin[i] = L;
         ++s;
-        if (slots.n == 32) {
-            if (active) slots.flush(m_q, lut_s, out_row, slot_col, mc, qset * ld, mc_stride, mc_q0);
-            slots.n = 0;
+        if (slots[0].n == 32) {
+            if (any_active) flush_all();
+#pragma unroll
+            for (int j = 0; j < QS; ++j) slots[j].n = 0;
             slot_col += 32;
         }
         if (s < s_hi) s_end_v = win.get(s + 1);
@@ -281,8 +301,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         const int64_t tv1 = tmin<int64_t>(tv0 + kTileVec, vend);
         while (v < tv1) {
             const int64_t stop = tmin(s_end_v, tv1);
-            if (active && stop > v)
-                scan_vectors<K, W, QPL>(q, rmin, tile + (v - tv0) * R, static_cast<int>(stop - v));
+            if (any_active && stop > v)
+                scan_vectors<K, W, S>(q, rmin, tile + (v - tv0) * R, static_cast<int>(stop - v));
             v = stop;
             while (s < s_hi && v == s_end_v) finish_set();
         }
@@ -290,8 +310,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         if (lane == 0) mbar_arrive(&empty[st]);
     }
     while (s < s_hi) finish_set();  // trailing empty sets (validated away upstream)
-    if (active && slots.n > 0)
-        slots.flush(m_q, lut_s, out_row, slot_col, mc, qset * ld, mc_stride, mc_q0);
+    if (any_active && slots[0].n > 0) flush_all();
 }
 
 // --------------------------------------------------------- candidate lists
@@ -432,16 +451,16 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
 }
 
 // ------------------------------------------------------------- dispatch
-template <int K, int W, int QPL>
+template <int K, int W, int QPL, int QS>
 static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, int64_t se,
                       const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
                       double *scores, int64_t ld, uint16_t *mc, int mc_stride, int mc_q0,
                       cudaStream_t st) {
     constexpr int NW = 8;
-    const size_t smem = all_smem_static<K, W, QPL, NW>() + (L + 1) * sizeof(double);
-    auto kern = score_all_kernel<K, W, QPL, NW>;
+    const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1) * sizeof(double);
+    auto kern = score_all_kernel<K, W, QPL, NW, QS>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t groups = (n_qsets + NW - 1) / NW;
+    const int64_t groups = (n_qsets + NW * QS - 1) / (NW * QS);
     int occ = 0;
     DSRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NW + 1) * 32, smem));
     occ = occ < 1 ? 1 : occ;
@@ -503,6 +522,7 @@ struct ScoreArgs {
     int64_t ld;
     uint16_t *mc;
     int mc_stride, mc_q0;
+    int qs_override;  // 0 = heuristic; else query sets per warp (1/2/4)
 };
 
 template <int K, int W, int QPL>
@@ -511,8 +531,18 @@ static int run_one(const ScoreArgs &a, cudaStream_t st) {
         return launch_cand<K, W, QPL>(a.recs, a.set_off, a.n_sets, a.cand, a.n_cand, a.cand_ld,
                                       a.qrecs, a.n_qsets, a.m_q, a.L, a.lut, a.scores, a.mc,
                                       a.mc_stride, a.mc_q0, st);
-    return launch_all<K, W, QPL>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q, a.L,
-                                 a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+    // register-block several query sets per warp when there are enough of them
+    if constexpr (QPL == 1 && W <= 2) {
+        const int qs = a.qs_override > 0 ? a.qs_override : (a.n_qsets >= 256 ? (W == 1 ? 4 : 2) : 1);
+        if (qs == 4)
+            return launch_all<K, W, QPL, 4>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
+                                            a.L, a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+        if (qs == 2)
+            return launch_all<K, W, QPL, 2>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
+                                            a.L, a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+    }
+    return launch_all<K, W, QPL, 1>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q, a.L,
+                                    a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
 }
 
 template <int K, int W>

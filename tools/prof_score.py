@@ -35,12 +35,21 @@ idx = d.build_from_codes(codes, sizes, np.arange(a.sets), cfg, keep_codes=False)
 q = torch.randint(0, 1 << a.C, (a.qsets * a.mq, a.L), generator=g, device=dev, dtype=torch.int32)
 qrecs, _ = engine.codes_to_records(q, a.L, a.C)
 torch.cuda.synchronize()
+ev = []
 for _ in range(a.reps):
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
     if a.mode == "all":
         s, _ = engine.score_all(idx.records, idx.set_off, qrecs, a.mq, a.L, a.C, idx.lut_dev)
     else:
         s, _ = engine.score_candidates(idx.records, idx.set_off, qrecs, a.mq, a.L, a.C,
                                        idx.lut_dev, cand_ld=a.sets, n_qsets=a.qsets)
+    e1.record()
+    ev.append((e0, e1))
     engine.topk(s, a.topk, ids=idx.doc_ids_dev)
 torch.cuda.synchronize()
-print("ok")
+ms = [x.elapsed_time(y) for x, y in ev]
+comp = a.qsets * a.mq * a.L * int(off[-1])
+best = min(ms)
+print(f"ok L={a.L} C={a.C} sets={a.sets} qsets={a.qsets} mode={a.mode} QS={os.environ.get('DSRT_QS','auto')} "
+      f"ms={best:.3f} Gcmp/s={comp / best / 1e6:.0f} frac={comp / best / 1e6 / 74100:.3f}")
