@@ -206,8 +206,8 @@ def run_gpu(args):
     del X
     torch.cuda.synchronize()
 
-    planes = idx.family.device_planes(d.lsh.default_mode(Q2.dtype), dev)
-    mode = d.lsh.default_mode(Q2.dtype)
+    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0])
+    planes = idx.family.device_planes(mode, dev)
     stream = torch.cuda.current_stream()
     ev = []
 
@@ -383,7 +383,7 @@ def run_cfg4(args):
     t_gen = time.perf_counter() - t_gen
     idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
     Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
-    mode = d.lsh.default_mode(Q2.dtype)
+    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0])
     planes = idx.family.device_planes(mode, dev)
     stream = torch.cuda.current_stream()
     chunk = max(1, min(n_sets, args.score_buffer // (8 * n_q)))
@@ -534,6 +534,95 @@ def run_cfg3(args):
     return 0
 
 
+def run_cfg2(args):
+    """cfg2: index build of 10M bf16 unit vectors (cfg1 mixture, cfg1 set sizes): hash
+    (tcgen05, bf16 hi/lo planes, fused sign/pack -> codes + plane records) + CSR layout."""
+    import torch
+
+    import paper_2210_15748_b200 as d
+    from oracle import dessert_oracle as O
+    from paper_2210_15748_b200 import _lib, engine, workloads
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n_vec, L, C = args.vectors or 10_000_000, 64, 7
+    rng = np.random.default_rng(600)
+    sizes = workloads.set_sizes(int(n_vec / 60), 70, 20, seed=600)
+    cs = np.cumsum(sizes)
+    n_sets = int(np.searchsorted(cs, n_vec)) + 1
+    sizes = sizes[:n_sets].copy()
+    sizes[-1] -= int(cs[n_sets - 1] - n_vec)
+    if sizes[-1] <= 0:
+        sizes = sizes[:-1]
+    X, _ = workloads.gpu_mixture(n_vec, 4096, 128, 0.05, seed=601, dtype=torch.bfloat16, device=dev)
+    fam = d.sample_srp_family(128, C, L, 0)
+    mode = _lib.HASH_TC_BF16X2
+    planes = fam.device_planes(mode, dev)
+    sizes_dev = torch.from_numpy(sizes).to(dev)
+    stream = torch.cuda.current_stream()
+    kev = []
+
+    def step(timed):
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        codes, recs, _ = engine.hash_vectors(X, planes, mode, L, C, check_zero=False)
+        if timed:
+            e1.record(stream)
+            kev.append((e0, e1))
+        set_off, _ = engine.sizes_to_offsets(sizes_dev)
+        return codes, recs, set_off
+
+    ms, clk = _clocks_and_time(step, args.steps, max(3, args.warmup), local, stream)
+    k_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    codes, recs, set_off = step(False)
+    torch.cuda.synchronize()
+    # flip rate vs the float64 oracle on a sample of vectors
+    samp = np.sort(rng.choice(n_vec, size=20000, replace=False))
+    Xs = X[torch.from_numpy(samp).to(dev)].double().cpu().numpy()
+    want = O.hash_matrix(fam.planes, L, C, Xs)
+    got = codes[torch.from_numpy(samp).to(dev)].cpu().numpy().astype(np.int64)
+    proj = O.projections(fam.planes, Xs)
+    band = np.abs(proj) < 1e-4 * np.linalg.norm(fam.planes, axis=1)[None, :] * \
+        np.linalg.norm(Xs, axis=1)[:, None]
+    bg = ((got[:, :, None] >> np.arange(C)) & 1).reshape(len(samp), L * C)
+    bw = ((want[:, :, None] >> np.arange(C)) & 1).reshape(len(samp), L * C)
+    flips = bg != bw
+    peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(REPO, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+    alg_flops = 2.0 * 128 * L * C * n_vec
+    mma_flops = 2 * alg_flops  # hi/lo planes: two MMA chains
+    hbm_bytes = n_vec * (128 * 2 + L + engine.record_words(L, C) * 4)
+    line = {
+        "metric": "index-build vectors/sec (cfg2: 10M bf16 vectors, L=64 C=7, hash + CSR layout)",
+        "value": n_vec / (ms * 1e-3), "unit": "vectors/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (cfg2-shaped, generated on GPU)",
+        "config": {"workload": "cfg2", "vectors": n_vec, "sets": int(len(sizes)), "L": L, "C": C,
+                   "hash_mode": "tcgen05 kind::f16, bf16 hi/lo planes (2 MMA chains)",
+                   "l2": "inputs larger than L2 (2.56 GB)"},
+        "roofline": {"bound": "tensor", "unit": "TFLOP/s", "kernel": "hash_tc_kernel<2,7,3>",
+                     "kernel_ms": k_ms,
+                     "achieved": alg_flops / (k_ms * 1e-3) / 1e12,
+                     "peak": peaks["bf16_tflops"], "frac": alg_flops / (k_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                     "mma_tflops_issued": mma_flops / (k_ms * 1e-3) / 1e12,
+                     "mma_frac": mma_flops / (k_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                     "hbm_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9,
+                     "hbm_frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "traffic": None,
+                     "algorithmic": "2*d*L*C flops per vector; bytes 2d in + L codes + 4R records out",
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst), hbm_gbs"},
+        "hash_bit_flips": {"sample_vectors": int(len(samp)), "bits": int(flips.size),
+                           "flips": int(flips.sum()), "outside_band": int((flips & ~band).sum()),
+                           "band_fraction": float(band.mean())},
+        "clocks": clk, "gpu_launches": 4 * args.steps,
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -541,7 +630,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[1, 3, 4])
+    ap.add_argument("--config", type=int, default=1, choices=[1, 2, 3, 4])
+    ap.add_argument("--vectors", type=int, default=0, help="override cfg2 vector count")
     ap.add_argument("--sets", type=int, default=0, help="override N (cfg3/cfg4)")
     ap.add_argument("--score-buffer", type=int, default=8 << 30)
     ap.add_argument("--latency-queries", type=int, default=1000)
@@ -552,6 +642,8 @@ def main():
         return run_cfg4(args)
     if args.config == 3:
         return run_cfg3(args)
+    if args.config == 2:
+        return run_cfg2(args)
     return run_gpu(args)
 
 

@@ -46,7 +46,8 @@ enum dsrt_hash_mode {
     DSRT_HASH_F64 = 0,      /* planes float64 (L*C, d); DFMA accumulation         */
     DSRT_HASH_F32 = 1,      /* planes float32 (L*C, d); FFMA accumulation         */
     DSRT_HASH_TC_F16 = 2,   /* tcgen05 kind::f16; planes fp16 (L*C, d), X fp16      */
-    DSRT_HASH_TC_BF16X2 = 3 /* tcgen05 kind::f16; planes bf16 hi/lo (2, L*C, d), X bf16 */
+    DSRT_HASH_TC_BF16X2 = 3, /* tcgen05 kind::f16; planes bf16 hi/lo (2, L*C, d), X bf16 */
+    DSRT_HASH_TC_F16X2 = 4   /* tcgen05 kind::f16; planes fp16 hi/lo (2, L*C, d), X fp16 */
 };
 
 const char *dsrt_last_error(void);
@@ -146,6 +147,12 @@ int dsrt_prefilter(const double *Q, int64_t n_qsets, int m_q, int d, const doubl
                    int probe, int k_filter, int64_t *cand, int32_t *n_cand, void *workspace,
                    size_t workspace_bytes, void *stream);
 size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
+
+/* Diagnostic: D(M,N) f32 = A(M,128) . B(N,128)^T on the tcgen05 path (TMA ->
+ * 128B-swizzled smem -> UMMA -> TMEM -> tcgen05.ld); fp16 (0) or bf16 (1)
+ * operands, 16 <= N <= 256.  Validates the tensor-core plumbing K1/K5 use. */
+int dsrt_tc_selftest(const void *A, int a_bf16, const void *B, int b_bf16, float *D, int M, int N,
+                     void *stream);
 
 /* Microbenchmark of the INT pipe (LOP3 / POPC / IMNMX lane-ops per second);
  * host call, synchronous.  Writes ops/s for {lop3, popc, imnmx, mixed}. */

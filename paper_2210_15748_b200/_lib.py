@@ -20,7 +20,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "dessert_b200.h")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED, ERANGE = 0, 1, 2, 3, 4
 F32, F64, F16, BF16 = 0, 1, 2, 3
-HASH_F64, HASH_F32, HASH_TC_F16, HASH_TC_BF16X2 = 0, 1, 2, 3
+HASH_F64, HASH_F32, HASH_TC_F16, HASH_TC_BF16X2, HASH_TC_F16X2 = 0, 1, 2, 3, 4
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -51,6 +51,7 @@ SIGNATURES = {
     "dsrt_prefilter_workspace": (_sz, [_i64, _i32, _i64, _i64, _i32]),
     "dsrt_tinytable": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "dsrt_microbench_int": (_i32, [_vp, _vp]),
+    "dsrt_tc_selftest": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp]),
 }
 
 _LIB = None

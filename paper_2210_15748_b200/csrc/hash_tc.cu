@@ -1,11 +1,257 @@
-// K1 tensor-core modes (tcgen05) -- see DESIGN.md.  Placeholder until the
-// tcgen05 kernel lands: reports EUNSUPPORTED so the host selects a SIMT mode.
-#include "common.cuh"
+// K1 tensor-core modes -- SRP hashing as a tcgen05 GEMM with a fused
+// sign-and-pack epilogue (replaces lsh.hash_matrix, lsh.py:90-106, for
+// fp16/bf16 inputs; the cfg-2 index-build throughput path).
+//
+//   D[row, p] = sum_k X[row, k] * W[p, k]      (fp32 accumulate in TMEM)
+//   bit[row, p] = D > 0;  code_t = sum_c bit[t*C + c] << c
+//
+// Planes are split into "parts" (hi/lo) so the fp16/bf16 operand rounding of
+// the float64 reference planes stays far inside the allowed band
+// |w.x| < 1e-4 |w||x|:  W = W_hi + W_lo, D = X.W_hi^T + X.W_lo^T (two MMA
+// chains into the same accumulator).  fp16/bf16 X is exact (the reference
+// hashes the same values cast to float64).
+//
+// Decomposition: the L tables split into column groups of <= 32 tables
+// (one plane word each, N_g = tables*C <= 256 MMA columns).  CTA c handles
+// group c % G for the 128-row tiles c/G, c/G + n_cta/G, ...  -- consecutive
+// CTAs share each X tile through L2.  Warp roles (192 threads):
+//   warp 0: TMA producer (3-stage ring of X tiles, planes loaded once),
+//   warp 1: MMA issuer (one thread, 8 K-steps x parts per tile),
+//   warps 2-5: epilogue (TMEM -> registers -> sign bits -> codes + plane
+//              records), TMEM double-buffered so it overlaps the next MMAs.
+#include "tc_common.cuh"
 
 namespace dsrt {
-int hash_tc(const void *, int, int64_t, int, const void *, int, int, int, void *, uint32_t *,
-            uint32_t *, cudaStream_t) {
-    set_error("unsupported: tensor-core hash mode not built");
+
+constexpr int kHThreads = 192;
+
+struct HashTcParams {
+    int64_t n_rows;
+    int L, Cr, groups, n_pad;  // n_pad = padded MMA N per group (multiple of 16)
+    int parts;
+    void *codes_out;          // uint8 (n, L)   (C <= 8)
+    uint32_t *recs_out;       // (n, R)
+    uint32_t *zero_rows;
+};
+
+template <int PARTS, int C, int kHStages>
+__global__ void __launch_bounds__(kHThreads, 1)
+    hash_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                   const __grid_constant__ CUtensorMap map_w, HashTcParams p, uint32_t idesc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int NP = p.n_pad;
+    constexpr int kTileA = 2 * 128 * 128;                 // two 64-column blocks
+    uint8_t *sa = smem;                                    // kHStages x kTileA
+    uint8_t *sb = smem + kHStages * kTileA;                // PARTS x 2 x (NP x 128 B)
+    __shared__ uint64_t full[kHStages], empty[kHStages], tfull[2], tempty[2], bar_b;
+    __shared__ uint32_t tmem_base;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int group = blockIdx.x % p.groups;
+    const int cta_in_group = blockIdx.x / p.groups;
+    const int ctas_per_group = gridDim.x / p.groups;
+    const int64_t n_tiles = (p.n_rows + 127) / 128;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&map_x);
+        tma_prefetch(&map_w);
+        for (int s = 0; s < kHStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // 4 epilogue warps
+        }
+        mbar_init(&bar_b, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(&tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const int prow = group * 32 * C;  // first plane row of this group
+            mbar_arrive_expect_tx(&bar_b, PARTS * 2 * NP * 128);
+            for (int part = 0; part < PARTS; ++part)
+                for (int kb = 0; kb < 2; ++kb)
+                    tma_load_2d(sb + (part * 2 + kb) * NP * 128, &map_w, kb * 64,
+                                part * (p.L * C) + prow, &bar_b);
+            int it = 0;
+            for (int64_t tile = cta_in_group; tile < n_tiles; tile += ctas_per_group, ++it) {
+                const int st = it % kHStages;
+                if (it >= kHStages) mbar_wait(&empty[st], ((it / kHStages) - 1) & 1);
+                mbar_arrive_expect_tx(&full[st], kTileA);
+                tma_load_2d(sa + st * kTileA, &map_x, 0, static_cast<int>(tile * 128), &full[st]);
+                tma_load_2d(sa + st * kTileA + 128 * 128, &map_x, 64, static_cast<int>(tile * 128),
+                            &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            mbar_wait(&bar_b, 0);
+            int it = 0;
+            for (int64_t tile = cta_in_group; tile < n_tiles; tile += ctas_per_group, ++it) {
+                const int st = it % kHStages, acc = it & 1;
+                mbar_wait(&full[st], (it / kHStages) & 1);
+                if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * 256;
+                for (int part = 0; part < PARTS; ++part)
+                    for (int kb = 0; kb < 2; ++kb) {
+                        const uint64_t ad = umma_desc_sw128(sa + st * kTileA + kb * 128 * 128);
+                        const uint64_t bd = umma_desc_sw128(sb + (part * 2 + kb) * NP * 128);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            umma_f16(d, ad + 2 * k, bd + 2 * k, idesc, (part | kb | k) != 0);
+                    }
+                umma_commit(&empty[st]);
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2..5)
+        const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+        const int L = p.L;
+        const int t0 = group * 32;
+        const int nt = min(32, L - t0);
+        const int ncols = nt * C;
+        const int W = (L + 31) >> 5, R = ((C * W) + 3) & ~3;
+        int it = 0;
+        for (int64_t tile = cta_in_group; tile < n_tiles; tile += ctas_per_group, ++it) {
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const int64_t row = tile * 128 + quarter * 32 + lane;
+            uint32_t plane[C];
+#pragma unroll
+            for (int b = 0; b < C; ++b) plane[b] = 0;
+            uint32_t codes_w[8];  // 32 tables x 8-bit codes
+#pragma unroll
+            for (int i = 0; i < 8; ++i) codes_w[i] = 0;
+            uint32_t any_nonzero = 0;
+            const uint32_t base = tmem + acc * 256 + (static_cast<uint32_t>(quarter * 32) << 16);
+            // 32 tables x C bits = C chunks of 32 columns; all indices static
+#pragma unroll
+            for (int ch = 0; ch < C; ++ch) {
+                uint32_t r[32];
+                tmem_ld32(base + ch * 32, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                                const int col = ch * 32 + j;
+                    const int t = col / C, b = col % C;
+                    const bool in = col < ncols;
+                    any_nonzero |= in ? (r[j] & 0x7fffffffu) : 0u;
+                    const uint32_t bit = (in && static_cast<int>(r[j]) > 0) ? 1u : 0u;  // +-0.0 -> 0
+                    codes_w[t >> 2] |= bit << (8 * (t & 3) + b);
+                    plane[b] |= bit << t;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (row < p.n_rows) {
+                if (p.codes_out) {
+                    uint8_t *dst = static_cast<uint8_t *>(p.codes_out) + row * L + t0;
+                    if (nt == 32 && (L & 15) == 0) {
+                        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+                        d4[0] = make_uint4(codes_w[0], codes_w[1], codes_w[2], codes_w[3]);
+                        d4[1] = make_uint4(codes_w[4], codes_w[5], codes_w[6], codes_w[7]);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 32; ++t)
+                            if (t < nt) dst[t] = (codes_w[t >> 2] >> (8 * (t & 3))) & 0xffu;
+                    }
+                }
+                if (p.recs_out) {
+                    uint32_t *rec = p.recs_out + row * R;
+#pragma unroll
+                    for (int b = 0; b < C; ++b) rec[b * W + group] = plane[b];
+                    if (group == 0)
+                        for (int i = C * W; i < R; ++i) rec[i] = 0;
+                }
+                if (group == 0 && p.zero_rows && any_nonzero == 0) atomicAdd(p.zero_rows, 1u);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+template <int PARTS, int C, int STAGES>
+static int launch_hash_tc(const CUtensorMap &mx, const CUtensorMap &mw, const HashTcParams &hp,
+                          uint32_t idesc, size_t smem, int ctas, cudaStream_t st);
+
+static int launch_hash_tc_c(int C, int parts, int stages, const CUtensorMap &mx,
+                            const CUtensorMap &mw, const HashTcParams &hp, uint32_t idesc,
+                            size_t smem, int ctas, cudaStream_t st) {
+#define DSRT_HC(c)                                                                            \
+    case c:                                                                                   \
+        if (parts == 1)                                                                       \
+            return stages == 3 ? launch_hash_tc<1, c, 3>(mx, mw, hp, idesc, smem, ctas, st)   \
+                               : launch_hash_tc<1, c, 2>(mx, mw, hp, idesc, smem, ctas, st);  \
+        return stages == 3 ? launch_hash_tc<2, c, 3>(mx, mw, hp, idesc, smem, ctas, st)       \
+                           : launch_hash_tc<2, c, 2>(mx, mw, hp, idesc, smem, ctas, st);
+    switch (C) {
+        DSRT_HC(1) DSRT_HC(2) DSRT_HC(3) DSRT_HC(4) DSRT_HC(5) DSRT_HC(6) DSRT_HC(7) DSRT_HC(8)
+        default: break;
+    }
+#undef DSRT_HC
+    set_error("invalid parameter: tensor-core hash needs C <= 8, got %d", C);
     return DSRT_EUNSUPPORTED;
 }
+
+int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, int mode, int L,
+            int C, void *codes_out, uint32_t *records_out, uint32_t *zero_rows, cudaStream_t st) {
+    const bool bf16 = mode == DSRT_HASH_TC_BF16X2;
+    const int parts = mode == DSRT_HASH_TC_F16 ? 1 : 2;
+    DSRT_REQUIRE(x_dtype == (bf16 ? DSRT_BF16 : DSRT_F16), DSRT_EINVAL,
+                 "invalid parameter: tensor-core hash mode %d needs %s vectors", mode,
+                 bf16 ? "bf16" : "fp16");
+    DSRT_REQUIRE(d == 128, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core hash needs d=128, got %d", d);
+    DSRT_REQUIRE(C <= 8, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core hash needs C <= 8, got %d", C);
+    DSRT_REQUIRE(n < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many rows for one call");
+    const int groups = (L + 31) / 32;
+    int n_pad = ((tmin(32, L) * C) + 15) & ~15;
+    n_pad = tmax(n_pad, 16);
+    DSRT_REQUIRE(n_pad <= 256, DSRT_EUNSUPPORTED, "invalid parameter: MMA N too large");
+    const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUtensorMap mx, mw;
+    int rc = make_tmap_2d(&mx, X, dt, 128, static_cast<uint64_t>(n), 256, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    rc = make_tmap_2d(&mw, planes, dt, 128, static_cast<uint64_t>(parts) * L * C, 256, 64, n_pad,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    HashTcParams hp{n, L, C, groups, n_pad, parts, codes_out, records_out, zero_rows};
+    const size_t b_bytes = static_cast<size_t>(parts) * 2 * n_pad * 128;
+    const int stages = (1024 + 3 * 2 * 128 * 128 + b_bytes <= 227 * 1024) ? 3 : 2;
+    const size_t smem = 1024 + stages * 2 * 128 * 128 + b_bytes;
+    const int64_t n_tiles = (n + 127) / 128;
+    int ctas = sm_count() * 1;
+    ctas = ctas - ctas % groups;
+    ctas = static_cast<int>(tmin<int64_t>(ctas, n_tiles * groups));
+    ctas = tmax(ctas, groups);
+    const uint32_t idesc = idesc_f16(128, n_pad, bf16, bf16);
+    return launch_hash_tc_c(C, parts, stages, mx, mw, hp, idesc, smem, ctas, st);
+}
+
+template <int PARTS, int C, int STAGES>
+static int launch_hash_tc(const CUtensorMap &mx, const CUtensorMap &mw, const HashTcParams &hp,
+                          uint32_t idesc, size_t smem, int ctas, cudaStream_t st) {
+    auto kern = hash_tc_kernel<PARTS, C, STAGES>;
+    DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<ctas, kHThreads, smem, st>>>(mx, mw, hp, idesc);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
 }  // namespace dsrt

@@ -216,6 +216,15 @@ def prefilter(Q, m_q: int, centroids, post_off, post_docs, n_docs: int, probe: i
     return cand, n_cand
 
 
+def tc_selftest(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """D = A . B^T (K = 128) through the tcgen05 path (diagnostic)."""
+    M, N = A.shape[0], B.shape[0]
+    D = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    _lib.call("dsrt_tc_selftest", _ptr(A.contiguous()), int(A.dtype == torch.bfloat16),
+              _ptr(B.contiguous()), int(B.dtype == torch.bfloat16), _ptr(D), M, N, _stream())
+    return D
+
+
 def microbench_int() -> dict:
     out = (ctypes.c_double * 4)()
     _lib.call("dsrt_microbench_int", out, _stream())

@@ -45,9 +45,10 @@ class SrpFamily:
                 t = p.to(device=device, dtype=torch.float32)
             elif mode == _lib.HASH_TC_F16:
                 t = p.to(dtype=torch.float16).to(device)
-            elif mode == _lib.HASH_TC_BF16X2:
-                hi = p.to(torch.bfloat16)
-                lo = (p - hi.to(torch.float64)).to(torch.bfloat16)
+            elif mode in (_lib.HASH_TC_BF16X2, _lib.HASH_TC_F16X2):
+                dt = torch.bfloat16 if mode == _lib.HASH_TC_BF16X2 else torch.float16
+                hi = p.to(dt)
+                lo = (p - hi.to(torch.float64)).to(dt)
                 t = torch.stack([hi, lo]).contiguous().to(device)
             else:
                 raise ValueError(f"invalid parameter: hash mode {mode}")
@@ -88,12 +89,19 @@ def build_sim_lookup(C: int, L: int) -> SimLookup:
     return SimLookup(C=C, L=L, table=table)
 
 
-def default_mode(dtype) -> int:
+def default_mode(dtype, d: int = 128, C: int = 7, n: int = 0) -> int:
     """Hash arithmetic per input dtype (K1).
 
-    float32/float64 inputs hash in float64 against the float64 planes.  fp16 /
-    bf16 inputs use the tensor-core kernel when it is built, else float64.
+    float32/float64 inputs hash in float64 against the float64 planes (exact).
+    fp16 / bf16 inputs with d = 128, C <= 8 use the tcgen05 kernel with hi/lo
+    split planes (operand rounding <= 2^-17 relative, far inside the
+    1e-4 band); small batches (< 4096 rows) use float64 SIMT.
     """
+    if d == 128 and C <= 8 and n >= 4096:
+        if dtype == torch.bfloat16:
+            return _lib.HASH_TC_BF16X2
+        if dtype == torch.float16:
+            return _lib.HASH_TC_F16X2
     return _lib.HASH_F64
 
 
@@ -116,7 +124,7 @@ def to_device_matrix(X, d: int, device="cuda") -> torch.Tensor:
 def hash_device(family: SrpFamily, X: torch.Tensor, mode: int | None = None, want_codes=True,
                 want_records=True, check_zero=True):
     """Hash a CUDA matrix; raises the reference's 'zero vector' error."""
-    mode = default_mode(X.dtype) if mode is None else mode
+    mode = default_mode(X.dtype, X.shape[1], family.C, X.shape[0]) if mode is None else mode
     planes = family.device_planes(mode, X.device)
     codes, recs, zero = engine.hash_vectors(X, planes, mode, family.L, family.C, want_codes,
                                             want_records, check_zero)

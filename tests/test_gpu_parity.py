@@ -117,6 +117,45 @@ def test_hash_modes_flip_only_in_band(mode, dtype):
     assert torch.equal(recs, recs2)
 
 
+TC_CASES = [(torch.float16, _lib.HASH_TC_F16X2), (torch.float16, _lib.HASH_TC_F16),
+            (torch.bfloat16, _lib.HASH_TC_BF16X2)]
+
+
+@pytest.mark.parametrize("dtype,mode", TC_CASES)
+@pytest.mark.parametrize("L,C", [(64, 7), (32, 8), (40, 5), (32, 7), (16, 3)])
+def test_hash_tensor_core_flip_only_in_band(dtype, mode, L, C):
+    """tcgen05 hash (TMA + UMMA + TMEM + fused sign/pack) vs the float64 oracle:
+    codes and plane records agree except inside |w.x| < 1e-4 |w||x|; counts reported."""
+    rng = np.random.default_rng(L * 10 + C)
+    n = 5000  # not a multiple of 128: exercises the ragged last tile
+    X = rng.standard_normal((n, 128))
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    Xt = torch.from_numpy(X).to(dtype)
+    Xexact = Xt.to(torch.float64).numpy()
+    fam = d.sample_srp_family(128, C, L, 5)
+    codes, recs = d.lsh.hash_device(fam, Xt.to(DEV).contiguous(), mode=mode)
+    want = O.hash_matrix(fam.planes, L, C, Xexact)
+    got = codes.cpu().numpy().astype(np.int64)
+    proj = O.projections(fam.planes, Xexact)
+    band = np.abs(proj) < 1e-4 * np.linalg.norm(fam.planes, axis=1)[None, :] * \
+        np.linalg.norm(Xexact, axis=1)[:, None]
+    bits_got = ((got[:, :, None] >> np.arange(C)) & 1).reshape(n, L * C)
+    bits_want = ((want[:, :, None] >> np.arange(C)) & 1).reshape(n, L * C)
+    flips = bits_got != bits_want
+    outside = int((flips & ~band).sum())
+    if mode != _lib.HASH_TC_F16:
+        assert outside == 0, f"{outside} flips outside the band ({int(flips.sum())} total)"
+    else:  # single fp16 rounding of the planes: report, allow a vanishing rate
+        assert outside <= 2, outside
+    recs2, _ = engine.codes_to_records(codes, L, C)
+    assert torch.equal(recs, recs2)
+    # zero rows are detected
+    Xz = Xt.clone()
+    Xz[17] = 0
+    with pytest.raises(ValueError, match="zero vector"):
+        d.lsh.hash_device(fam, Xz.to(DEV).contiguous(), mode=mode)
+
+
 # ------------------------------------------------------------------- layout
 def test_layout_roundtrip_and_tinytable_export(golden_small):
     g = golden_small
