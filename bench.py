@@ -469,8 +469,7 @@ def run_cfg3(args):
     cfg = d.IndexConfig(d=128, C=C, L=L, seed=0,
                         filter=d.FilterConfig(enabled=True, centroids=n_cent, probe=probe,
                                               k_filter=k_filter))
-    idx = d.build_from_vectors(X, sizes, np.arange(n_sets), cfg, keep_codes=False,
-                               hash_mode=_lib.HASH_F32)
+    idx = d.build_from_vectors(X, sizes, np.arange(n_sets), cfg, keep_codes=False)
     cvec = cents.double()
     cvec = cvec / cvec.norm(dim=1, keepdim=True)
     centroids = prefilter.Centroids(k=n_cent, seed=0, vectors=cvec.cpu().numpy())

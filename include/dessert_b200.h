@@ -147,6 +147,23 @@ int dsrt_prefilter(const double *Q, int64_t n_qsets, int m_q, int d, const doubl
                    int probe, int k_filter, int64_t *cand, int32_t *n_cand, void *workspace,
                    size_t workspace_bytes, void *stream);
 size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
+/*
+ * K5, tensor-core screen (same results as dsrt_prefilter): tcgen05 fp16 GEMM of
+ * normalised Q rows against centroids_f16 = fp16(centroids / cent_max_norm).
+ * Pass 0 finds each row's probe-th best approximate similarity A_P; pass 1
+ * collects every centroid with approx >= A_P - 2 eps (eps = the screen's
+ * rigorous error bound), which are re-ranked in float64 (ties -> lower
+ * centroid id); rows with more than 32 such centroids fall back to the exact
+ * float64 scan.  d = 128, probe <= 12.
+ */
+int dsrt_prefilter_tc(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
+                      const void *centroids_f16, double cent_max_norm, int64_t k_c,
+                      const int64_t *post_off, const int64_t *post_docs, int64_t n_docs, int probe,
+                      int k_filter, int64_t *cand, int32_t *n_cand, void *workspace,
+                      size_t workspace_bytes, void *stream);
+size_t dsrt_prefilter_tc_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
+/* rows of float64 -> fp16 (scale > 0: multiply by scale; scale <= 0: normalise each row) */
+int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scale, void *dst, void *stream);
 
 /* Diagnostic: D(M,N) f32 = A(M,128) . B(N,128)^T on the tcgen05 path (TMA ->
  * 128B-swizzled smem -> UMMA -> TMEM -> tcgen05.ld); fp16 (0) or bf16 (1)

@@ -49,6 +49,10 @@ SIGNATURES = {
     "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp,
                               _vp, _vp, _sz, _vp]),
     "dsrt_prefilter_workspace": (_sz, [_i64, _i32, _i64, _i64, _i32]),
+    "dsrt_prefilter_tc": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, ctypes.c_double, _i64, _vp, _vp,
+                                 _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "dsrt_prefilter_tc_workspace": (_sz, [_i64, _i32, _i64, _i64, _i32]),
+    "dsrt_to_f16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),
     "dsrt_tinytable": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "dsrt_microbench_int": (_i32, [_vp, _vp]),
     "dsrt_tc_selftest": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp]),

@@ -12,7 +12,9 @@
 //                     (prefilter.py:142-144): count histogram -> threshold
 //                     count c*, all docs above it, the lowest-index docs at c*
 //                     in one ordered pass, then a shared-memory bitonic sort.
-#include "common.cuh"
+#include <cuda_fp16.h>
+
+#include "tc_common.cuh"
 
 namespace dsrt {
 
@@ -175,7 +177,7 @@ __global__ void merge_kernel(const Cand *__restrict__ in, int64_t n_rows, int n_
 __global__ void count_kernel(const int32_t *__restrict__ probed, int64_t n_q, int m_q, int P,
                              const int64_t *__restrict__ post_off,
                              const int64_t *__restrict__ post_docs, int64_t row_words,
-                             uint32_t *__restrict__ counts) {
+                             uint32_t *__restrict__ counts, int cbits) {
     const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t total = n_q * m_q * P;
@@ -187,7 +189,10 @@ __global__ void count_kernel(const int32_t *__restrict__ probed, int64_t n_q, in
     uint32_t *row = counts + qs * row_words;
     for (int64_t i = lo + lane; i < hi; i += 32) {
         const int64_t doc = post_docs[i];
-        atomicAdd(row + (doc >> 1), 1u << (16 * (doc & 1)));
+        if (cbits == 8)
+            atomicAdd(row + (doc >> 2), 1u << (8 * (doc & 3)));
+        else
+            atomicAdd(row + (doc >> 1), 1u << (16 * (doc & 1)));
     }
 }
 
@@ -195,28 +200,82 @@ __device__ __forceinline__ uint32_t count_of(const uint32_t *row, int64_t doc) {
     return (row[doc >> 1] >> (16 * (doc & 1))) & 0xffffu;
 }
 
-// one CTA per query set
+// one CTA per query set.  Counters are uint16 pairs in uint32 words; every
+// thread handles 8 consecutive docs per uint4 load.
+//  pass 1: count histogram (per-warp privatised bins, only touched docs);
+//  c* = largest c with #(count > c) + hist[c] >= k_filter;
+//  pass 2 (ascending doc order, 8192 docs per step): take every doc with
+//  count > c*, and the first `need` docs with count == c* (block-wide
+//  exclusive scan of the per-thread tie counts); bitonic sort by
+//  (count desc, index asc) in shared memory.
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelBins = 130;  // per-warp histogram bins (counts >= 129 clamp; exact bins via fallback)
+
+template <int CB>  // counter bits: 8 or 16
 __global__ void __launch_bounds__(kSelThreads)
     select_kernel(const uint32_t *__restrict__ counts, int64_t row_words, int64_t n_docs,
                   int max_count, int k_filter, int64_t *__restrict__ cand,
                   int32_t *__restrict__ n_cand) {
+    constexpr int DPG = 128 / CB;            // docs per uint4 group
+    constexpr int DPW = 32 / CB;             // docs per word
+    constexpr uint32_t MASK = (1u << CB) - 1u;
     extern __shared__ __align__(16) uint8_t smem[];
-    uint64_t *buf = reinterpret_cast<uint64_t *>(smem);                 // kSelMax keys
-    uint32_t *hist = reinterpret_cast<uint32_t *>(buf + kSelMax);       // max_count+1
-    __shared__ int s_cstar, s_need, s_slot, s_eq_run;
-    __shared__ int warp_eq[32];
+    uint64_t *buf = reinterpret_cast<uint64_t *>(smem);                    // kSelMax keys
+    uint32_t *hist = reinterpret_cast<uint32_t *>(buf + kSelMax);          // max_count+1
+    uint32_t *whist = hist + (max_count + 1);                              // kSelWarps x kSelBins
+    __shared__ int s_cstar, s_need, s_slot, s_eq_run, s_eq_step;
+    __shared__ int warp_tot[32];
     const int64_t qs = blockIdx.x;
     const uint32_t *row = counts + qs * row_words;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool small_bins = max_count < kSelBins;
     for (int i = tid; i <= max_count; i += blockDim.x) hist[i] = 0;
+    if (small_bins)
+        for (int i = tid; i < kSelWarps * kSelBins; i += blockDim.x) whist[i] = 0;
     __syncthreads();
-    for (int64_t doc = tid; doc < n_docs; doc += blockDim.x) {
-        const uint32_t c = count_of(row, doc);
-        if (c) atomicAdd(&hist[tmin<uint32_t>(c, static_cast<uint32_t>(max_count))], 1u);
+    // each thread owns 4 consecutive uint4 groups per step (4*DPG docs, 64 B):
+    // four independent loads in flight, ascending doc order across threads
+    constexpr int G = 4;
+    const int64_t n_groups = (n_docs + DPG - 1) / DPG;
+    const uint4 *row4 = reinterpret_cast<const uint4 *>(row);
+    const int64_t row_words4 = row_words / 4;
+    auto load_groups = [&](int64_t g0, uint32_t (&w)[4 * G]) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const int64_t g = g0 + u;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (g < row_words4) v = __ldg(row4 + g);
+            w[4 * u] = v.x; w[4 * u + 1] = v.y; w[4 * u + 2] = v.z; w[4 * u + 3] = v.w;
+        }
+    };
+    const int64_t per_step = static_cast<int64_t>(blockDim.x) * G;
+    uint32_t *myh = whist + warp * kSelBins;
+    for (int64_t base = 0; base < n_groups; base += per_step) {
+        const int64_t g0 = base + static_cast<int64_t>(tid) * G;
+        uint32_t w[4 * G];
+        load_groups(g0, w);  // rows are zero-padded past n_docs: no bounds checks
+#pragma unroll
+        for (int q = 0; q < 4 * G; ++q) {
+            if (w[q] == 0u) continue;  // most words hold no touched doc
+#pragma unroll
+            for (int k = 0; k < DPW; ++k) {
+                const uint32_t c = (w[q] >> (CB * k)) & MASK;
+                if (c != 0) {
+                    if (small_bins) atomicAdd(&myh[c], 1u);
+                    else atomicAdd(&hist[tmin<uint32_t>(c, static_cast<uint32_t>(max_count))], 1u);
+                }
+            }
+        }
     }
     __syncthreads();
+    if (small_bins)
+        for (int b = tid; b <= max_count; b += blockDim.x) {
+            uint32_t t = 0;
+            for (int wv = 0; wv < kSelWarps; ++wv) t += whist[wv * kSelBins + b];
+            hist[b] = t;
+        }
+    __syncthreads();
     if (tid == 0) {
-        // docs with count > c are `cum`; c* = largest c with cum(>c) + hist[c] >= k_filter
         int64_t cum = 0;
         bool found = false;
         for (int c = max_count; c >= 1; --c) {
@@ -228,7 +287,7 @@ __global__ void __launch_bounds__(kSelThreads)
             }
             cum += hist[c];
         }
-        if (!found) {  // fewer than k_filter touched docs: take all of them
+        if (!found) {
             s_cstar = 1;
             s_need = static_cast<int>(hist[1]);
         }
@@ -238,31 +297,72 @@ __global__ void __launch_bounds__(kSelThreads)
     __syncthreads();
     const uint32_t cstar = s_cstar;
     const int need = s_need;
-    // ordered pass over docs in tiles of blockDim: take count > c*, and the
-    // first `need` docs (ascending index) with count == c*.
-    for (int64_t base = 0; base < n_docs; base += blockDim.x) {
-        const int64_t doc = base + tid;
-        const uint32_t c = doc < n_docs ? count_of(row, doc) : 0u;
-        const bool gt = c > cstar;
-        const bool eq = c == cstar && c > 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, eq);
-        if (lane == 0) warp_eq[warp] = __popc(bal);
+    for (int64_t base = 0; base < n_groups; base += per_step) {
+        const int64_t g0 = base + static_cast<int64_t>(tid) * G;
+        uint32_t w[4 * G];
+        load_groups(g0, w);
+        // SIMD per word: lanes equal to c* (ties) and >= c* (hits); c* >= 1
+        const uint32_t cs = CB == 8 ? cstar * 0x01010101u : cstar * 0x00010001u;
+        int eqn = 0;
+        uint32_t hitmask = 0;  // bit q: word q has a doc with count >= c*
+#pragma unroll
+        for (int q = 0; q < 4 * G; ++q) {
+            if (w[q] == 0u) continue;
+            if (CB == 8) {
+                eqn += __popc(__vcmpeq4(w[q], cs) & 0x01010101u);
+                hitmask |= (__vcmpgeu4(w[q], cs) != 0u ? 1u : 0u) << q;
+            } else {
+                eqn += __popc(__vcmpeq2(w[q], cs) & 0x00010001u);
+                hitmask |= (__vcmpgeu2(w[q], cs) != 0u ? 1u : 0u) << q;
+            }
+        }
+        const int nhit = hitmask != 0u;
+        // block exclusive scan of eqn (ascending doc order = ascending tid)
+        int x = eqn;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[warp] = x;
         __syncthreads();
-        int before = __popc(bal & ((1u << lane) - 1u));
-        for (int w = 0; w < warp; ++w) before += warp_eq[w];
-        const int run = s_eq_run;
-        bool take = gt || (eq && run + before < need);
-        if (take) {
-            const int slot = atomicAdd(&s_slot, 1);
-            if (slot < kSelMax)
-                buf[slot] = (static_cast<uint64_t>(c) << 40) | (0xffffffffffull - static_cast<uint64_t>(doc));
+        if (warp == 0) {  // scan of the 32 warp totals
+            int t = warp_tot[lane];
+            int sx = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, sx, o);
+                if (lane >= o) sx += y;
+            }
+            warp_tot[lane] = sx - t;  // exclusive
+            if (lane == 31) s_eq_step = sx;
         }
         __syncthreads();
-        if (tid == 0) {
-            int tot = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += warp_eq[w];
-            s_eq_run = run + tot;
+        int run = s_eq_run + warp_tot[warp] + (x - eqn);
+        if (nhit > 0) {
+#pragma unroll
+            for (int q = 0; q < 4 * G; ++q) {
+                if (!((hitmask >> q) & 1u)) continue;
+#pragma unroll
+                for (int k = 0; k < DPW; ++k) {
+                    const uint32_t c = (w[q] >> (CB * k)) & MASK;
+                    if (c < cstar) continue;  // c* >= 1, so c == 0 is skipped
+                    bool take = c > cstar;
+                    if (c == cstar) {
+                        take = run < need;
+                        ++run;
+                    }
+                    if (take) {
+                        const int64_t doc = g0 * DPG + q * DPW + k;
+                        const int slot = atomicAdd(&s_slot, 1);
+                        if (slot < kSelMax)
+                            buf[slot] = (static_cast<uint64_t>(c) << 40) | (0xffffffffffull - static_cast<uint64_t>(doc));
+                    }
+                }
+            }
         }
+        __syncthreads();
+        if (tid == 0) s_eq_run += s_eq_step;
         __syncthreads();
     }
     const int m = min(s_slot, kSelMax);
@@ -292,6 +392,39 @@ __global__ void __launch_bounds__(kSelThreads)
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+// counters: uint8 when m_q*probe <= 255, else uint16; rows padded to 16 bytes
+static int counter_bits(int max_count) { return max_count <= 255 ? 8 : 16; }
+static int64_t row_words_for(int64_t n_docs, int max_count) {
+    const int64_t dpg = 128 / counter_bits(max_count);
+    return ((n_docs + dpg - 1) / dpg) * 4;
+}
+static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int P, const int64_t *post_off,
+                               const int64_t *post_docs, int64_t n_docs, int64_t row_words,
+                               uint32_t *counts, int k_filter, int64_t *cand, int32_t *n_cand,
+                               cudaStream_t st);
+
+static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int P, const int64_t *post_off,
+                               const int64_t *post_docs, int64_t n_docs, int64_t row_words,
+                               uint32_t *counts, int k_filter, int64_t *cand, int32_t *n_cand,
+                               cudaStream_t st) {
+    const int max_count = m_q * P;
+    const int cb = counter_bits(max_count);
+    const int64_t warps = n_q * m_q * P;
+    count_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
+        probed, n_q, m_q, P, post_off, post_docs, row_words, counts, cb);
+    const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1 + kSelWarps * kSelBins) * sizeof(uint32_t);
+    if (cb == 8) {
+        DSRT_CUDA(cudaFuncSetAttribute(select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        select_kernel<8><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
+            counts, row_words, n_docs, max_count, k_filter, cand, n_cand);
+    } else {
+        DSRT_CUDA(cudaFuncSetAttribute(select_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        select_kernel<16><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
+            counts, row_words, n_docs, max_count, k_filter, cand, n_cand);
+    }
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
 
 struct PrefilterWs {
     size_t cand_bytes, probed_bytes, counts_bytes, total;
@@ -302,12 +435,315 @@ static PrefilterWs ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, 
     PrefilterWs w{};
     const int64_t rows = n_q * m_q;
     w.n_chunks = (k_c + kPTile * kPChunkTiles - 1) / (kPTile * kPChunkTiles);
-    w.row_words = (n_docs + 1) / 2;
+    w.row_words = row_words_for(n_docs, m_q * P);
     w.cand_bytes = align256(static_cast<size_t>(rows) * w.n_chunks * P * sizeof(Cand));
     w.probed_bytes = align256(static_cast<size_t>(rows) * P * sizeof(int32_t));
     w.counts_bytes = align256(static_cast<size_t>(n_q) * w.row_words * sizeof(uint32_t));
     w.total = w.cand_bytes + w.probed_bytes + w.counts_bytes;
     return w;
+}
+
+
+// ====================================================================
+// Tensor-core screen (exact results): sims ~ fp16(q/|q|) . fp16(c*s) on
+// tcgen05.  Pass 0 finds each row's P-th best approx value A_P; every
+// centroid with approx >= A_P - 2 eps (pass 1, a second cheap GEMM sweep) is
+// re-ranked in float64 -- that set provably contains the exact top-P, ties
+// included; rows with more than kCandMax such centroids fall back to the
+// exact float64 scan.  eps bounds |approx - exact| for unit-bounded rows:
+// fp16 operand rounding 2u(1+u) with u = 2^-11 plus fp32 accumulation.
+// ====================================================================
+constexpr int kSN = 128;         // centroids per N-tile
+constexpr int kSStages = 4;
+constexpr int kSThreads = 192;
+constexpr double kScreenEps = 1.2e-3;
+
+struct ScreenCand {
+    float s;
+    int32_t id;
+};
+
+__global__ void to_f16_rows_kernel(const double *__restrict__ src, int64_t n, int d, double scale,
+                                   __half *__restrict__ dst) {
+    const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const double *x = src + row * d;
+    double s = scale;
+    if (scale <= 0.0) {  // per-row normalisation
+        double ss = 0.0;
+        for (int k = lane; k < d; k += 32) ss = fma(x[k], x[k], ss);
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        s = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+    }
+    for (int k = lane; k < d; k += 32) dst[row * d + k] = __double2half(x[k] * s);
+}
+
+__device__ __forceinline__ bool s_better(float sa, int ia, float sb, int ib) {
+    return sa > sb || (sa == sb && ia < ib);
+}
+
+// grid: (row tiles of 128, splits).  A = 128 query rows (resident), B = 128-
+// centroid tiles streamed by TMA; TMEM double-buffered; 4 epilogue warps, one
+// query row per thread.  PASS 0: branch-free running top-P of approx values
+// (only when some lane improves, via a warp vote) -> out_vals[row][split][P].
+// PASS 1: append every centroid with approx >= theta[row] to the row's list
+// (capped at kCandMax; overflow -> the row falls back to the exact scan).
+constexpr int kCandMax = 32;
+constexpr int kMaxPtc = 12;
+
+template <int PASS, int PT>
+__global__ void __launch_bounds__(kSThreads, 1)
+    pf_screen_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_c,
+                     int64_t n_rows, int64_t k_c, int64_t tiles_per_split, int P,
+                     float *__restrict__ out_vals, const float *__restrict__ theta,
+                     ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n, uint32_t idesc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int kA = 2 * 128 * 128, kB = 2 * kSN * 128;
+    uint8_t *sa = smem;
+    uint8_t *sb = smem + kA;
+    __shared__ uint64_t full[kSStages], empty[kSStages], tfull[2], tempty[2], bar_a;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 128;
+    const int64_t n_tiles_total = (k_c + kSN - 1) / kSN;
+    const int64_t t_lo = blockIdx.y * tiles_per_split;
+    const int64_t t_hi = tmin<int64_t>(t_lo + tiles_per_split, n_tiles_total);
+    if (threadIdx.x == 0) {
+        tma_prefetch(&map_q);
+        tma_prefetch(&map_c);
+        for (int s = 0; s < kSStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        mbar_init(&bar_a, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(&tmem_base, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&bar_a, kA);
+            tma_load_2d(sa, &map_q, 0, static_cast<int>(m0), &bar_a);
+            tma_load_2d(sa + 128 * 128, &map_q, 64, static_cast<int>(m0), &bar_a);
+            int it = 0;
+            for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
+                const int st = it % kSStages;
+                if (it >= kSStages) mbar_wait(&empty[st], ((it / kSStages) - 1) & 1);
+                mbar_arrive_expect_tx(&full[st], kB);
+                tma_load_2d(sb + st * kB, &map_c, 0, static_cast<int>(t * kSN), &full[st]);
+                tma_load_2d(sb + st * kB + kSN * 128, &map_c, 64, static_cast<int>(t * kSN), &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_wait(&bar_a, 0);
+            int it = 0;
+            for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
+                const int st = it % kSStages, acc = it & 1;
+                mbar_wait(&full[st], (it / kSStages) & 1);
+                if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * kSN;
+                for (int kb = 0; kb < 2; ++kb) {
+                    const uint64_t ad = umma_desc_sw128(sa + kb * 128 * 128);
+                    const uint64_t bd = umma_desc_sw128(sb + st * kB + kb * kSN * 128);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) umma_f16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                }
+                umma_commit(&empty[st]);
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int64_t row = m0 + quarter * 32 + lane;
+        const bool row_ok = row < n_rows;
+        float tv[PT];
+#pragma unroll
+        for (int j = 0; j < PT; ++j) tv[j] = -INFINITY;
+        float worst = -INFINITY;  // tv[P-1]
+        const float th = (PASS == 1 && row_ok) ? theta[row] : INFINITY;
+        int it = 0;
+        for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const uint32_t base = tmem + acc * kSN + (static_cast<uint32_t>(quarter * 32) << 16);
+            const int64_t id0 = t * kSN;
+            const bool full_tile = id0 + kSN <= k_c;
+#pragma unroll 1
+            for (int c0 = 0; c0 < kSN; c0 += 32) {
+                uint32_t r[32];
+                tmem_ld32(base + c0, r);
+                tmem_wait_ld();
+                if (!full_tile) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (id0 + c0 + j >= k_c) r[j] = __float_as_uint(-INFINITY);
+                }
+                // chunk maximum (tree, independent FMNMX) -> one vote per 32 values
+                float m16[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    m16[j] = fmaxf(__uint_as_float(r[j]), __uint_as_float(r[j + 16]));
+#pragma unroll
+                for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+                    for (int j = 0; j < w; ++j) m16[j] = fmaxf(m16[j], m16[j + w]);
+                const float cmax = m16[0];
+                if (PASS == 0) {
+                    if (__any_sync(0xffffffffu, cmax > worst)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            float x = __uint_as_float(r[j]);
+                            if (x > worst) {  // branch-free insertion into the sorted list
+#pragma unroll
+                                for (int q = 0; q < PT; ++q) {
+                                    const float hi = fmaxf(tv[q], x);
+                                    x = fminf(tv[q], x);
+                                    tv[q] = hi;
+                                }
+                                worst = tv[0];
+#pragma unroll
+                                for (int q = 1; q < PT; ++q)
+                                    if (q < P) worst = tv[q];
+                            }
+                        }
+                    }
+                } else {
+                    if (__any_sync(0xffffffffu, cmax >= th)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float v = __uint_as_float(r[j]);
+                            if (v >= th) {
+                                const int slot = atomicAdd(list_n + row, 1);
+                                if (slot < kCandMax)
+                                    lists[row * kCandMax + slot] = ScreenCand{v, static_cast<int32_t>(id0 + c0 + j)};
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (PASS == 0 && row_ok) {
+            float *o = out_vals + (row * gridDim.y + blockIdx.y) * kMaxPtc;
+#pragma unroll
+            for (int j = 0; j < kMaxPtc; ++j) o[j] = j < PT ? tv[j < PT ? j : 0] : -INFINITY;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
+// thread per row: theta = (P-th best approx over all splits) - 2 eps
+__global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int64_t n_rows, int P,
+                                float eps2, float *__restrict__ theta, int32_t *__restrict__ list_n) {
+    const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (row >= n_rows) return;
+    float tv[kMaxPtc];
+#pragma unroll
+    for (int j = 0; j < kMaxPtc; ++j) tv[j] = -INFINITY;
+    for (int s = 0; s < n_split; ++s)
+        for (int j = 0; j < P; ++j) {
+            float x = vals[(row * n_split + s) * kMaxPtc + j];
+#pragma unroll
+            for (int q = 0; q < kMaxPtc; ++q) {
+                const float hi = fmaxf(tv[q], x);
+                x = fminf(tv[q], x);
+                tv[q] = hi;
+            }
+        }
+    float aP = tv[0];
+#pragma unroll
+    for (int q = 1; q < kMaxPtc; ++q)
+        if (q < P) aP = tv[q];
+    theta[row] = aP - eps2;
+    list_n[row] = 0;
+}
+
+// warp per row: exact float64 re-rank of the collected candidates -> probed ids;
+// flags rows whose list overflowed (fallback to the exact scan).
+__global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int32_t *__restrict__ list_n,
+                                 const double *__restrict__ Q, const double *__restrict__ cents,
+                                 int64_t n_rows, int d, int P, int32_t *__restrict__ probed,
+                                 int32_t *__restrict__ fallback) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n_rows) return;
+    const int n = list_n[row];
+    if (n > kCandMax || n < P) {  // overflow (or fewer candidates than probes: degenerate)
+        if (lane == 0) fallback[row] = 1;
+        return;
+    }
+    if (lane == 0) fallback[row] = 0;
+    double ex = -INFINITY;
+    int eid = 0x7fffffff;
+    if (lane < n) {
+        const int c = lists[row * kCandMax + lane].id;
+        const double *q = Q + row * d;
+        const double *cv = cents + static_cast<int64_t>(c) * d;
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) acc = fma(q[k], cv[k], acc);
+        ex = acc;
+        eid = c;
+    }
+    double es = -INFINITY;
+    int ei = 0x7fffffff;
+    warp_topP_merge(es, ei, ex, eid, P);
+    if (lane < P) probed[row * P + lane] = ei;
+}
+
+// exact float64 scan for flagged rows (one CTA per row; rare)
+__global__ void __launch_bounds__(256)
+    pf_fallback_kernel(const int32_t *__restrict__ fallback, const double *__restrict__ Q,
+                       const double *__restrict__ cents, int64_t n_rows, int64_t k_c, int d, int P,
+                       int32_t *__restrict__ probed) {
+    const int64_t row = blockIdx.x;
+    if (row >= n_rows || fallback[row] == 0) return;
+    __shared__ double q[512];
+    __shared__ double cs[8][32];
+    __shared__ int ci[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = threadIdx.x; k < d && k < 512; k += blockDim.x) q[k] = Q[row * d + k];
+    __syncthreads();
+    double ts = -INFINITY;
+    int ti = 0x7fffffff;
+    for (int64_t c0 = static_cast<int64_t>(warp) * 32; c0 < k_c; c0 += 256) {
+        const int64_t c = c0 + lane;
+        double s = -INFINITY;
+        int id = 0x7fffffff;
+        if (c < k_c) {
+            double acc = 0.0;
+            for (int k = 0; k < d; ++k) acc = fma(q[k], cents[c * d + k], acc);
+            s = acc;
+            id = static_cast<int>(c);
+        }
+        warp_topP_merge(ts, ti, s, id, P);
+    }
+    cs[warp][lane] = ts;
+    ci[warp][lane] = ti;
+    __syncthreads();
+    if (warp == 0) {
+        double fs = -INFINITY;
+        int fi = 0x7fffffff;
+        for (int w = 0; w < 8; ++w) warp_topP_merge(fs, fi, lane < P ? cs[w][lane] : -INFINITY,
+                                                    lane < P ? ci[w][lane] : 0x7fffffff, P);
+        if (lane < P) probed[row * P + lane] = fi;
+    }
 }
 
 }  // namespace dsrt
@@ -353,13 +789,136 @@ extern "C" int dsrt_prefilter(const double *Q, int64_t n_q, int m_q, int d, cons
     merge_kernel<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
         cands, rows, static_cast<int>(w.n_chunks), P, probed);
     DSRT_CUDA(cudaMemsetAsync(counts, 0, w.counts_bytes, st));
-    const int64_t warps = rows * P;
-    count_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
-        probed, n_q, m_q, P, post_off, post_docs, w.row_words, counts);
-    const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1) * sizeof(uint32_t);
-    DSRT_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    select_kernel<<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
-        counts, w.row_words, n_docs, max_count, k_filter, cand, n_cand);
+    int rc2 = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, w.row_words, counts,
+                                  k_filter, cand, n_cand, st);
+    if (rc2) return rc2;
     DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
+// ---------------------------------------------------------- TC entry points
+namespace dsrt {
+template <int PASS, int PT>
+static int launch_screen(dim3 g, size_t smem, cudaStream_t st, const CUtensorMap &mq, const CUtensorMap &mc,
+                         int64_t rows, int64_t k_c, int64_t tps, int P, float *vals, const float *theta,
+                         ScreenCand *lists, int32_t *listn, uint32_t idesc) {
+    DSRT_CUDA(cudaFuncSetAttribute(pf_screen_kernel<PASS, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pf_screen_kernel<PASS, PT><<<g, kSThreads, smem, st>>>(mq, mc, rows, k_c, tps, P, vals, theta, lists,
+                                                           listn, idesc);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+}  // namespace dsrt
+extern "C" int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scale, void *dst,
+                                void *stream) {
+    DSRT_REQUIRE(n >= 0 && d >= 1, DSRT_EINVAL, "invalid parameter: n=%lld d=%d", (long long)n, d);
+    if (n == 0) return DSRT_OK;
+    to_f16_rows_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, as_stream(stream)>>>(
+        src, n, d, scale, static_cast<__half *>(dst));
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
+namespace dsrt {
+struct TcWs {
+    size_t q16, screen, theta, lists, listn, probed, fallback, counts, total;
+    int64_t n_split, row_words, tiles_per_split;
+};
+static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int P) {
+    TcWs w{};
+    const int64_t rows = n_q * m_q;
+    const int64_t m_tiles = (rows + 127) / 128;
+    const int64_t n_tiles = (k_c + kSN - 1) / kSN;
+    const int sms = sm_count();
+    // about one wave of CTAs: fewer splits amortise each row's list warm-up
+    int64_t bs = tmax<int64_t>(1, tmin<int64_t>(n_tiles, (sms + m_tiles / 2) / m_tiles));
+    w.n_split = bs;
+    w.tiles_per_split = (n_tiles + bs - 1) / bs;
+    w.n_split = (n_tiles + w.tiles_per_split - 1) / w.tiles_per_split;
+    w.row_words = row_words_for(n_docs, m_q * P);
+    w.q16 = align256(static_cast<size_t>(m_tiles * 128) * 128 * 2);
+    w.screen = align256(static_cast<size_t>(rows) * w.n_split * kMaxPtc * sizeof(float));
+    w.theta = align256(static_cast<size_t>(rows) * sizeof(float));
+    w.lists = align256(static_cast<size_t>(rows) * kCandMax * sizeof(ScreenCand));
+    w.listn = align256(static_cast<size_t>(rows) * sizeof(int32_t));
+    w.probed = align256(static_cast<size_t>(rows) * P * sizeof(int32_t));
+    w.fallback = align256(static_cast<size_t>(rows) * sizeof(int32_t));
+    w.counts = align256(static_cast<size_t>(n_q) * w.row_words * sizeof(uint32_t));
+    w.total = w.q16 + w.screen + w.theta + w.lists + w.listn + w.probed + w.fallback + w.counts;
+    return w;
+}
+}  // namespace dsrt
+
+extern "C" size_t dsrt_prefilter_tc_workspace(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs,
+                                              int probe) {
+    const int P = static_cast<int>(tmin<int64_t>(tmax(probe, 1), k_c));
+    return tc_ws_layout(n_q, m_q, k_c, n_docs, P).total;
+}
+
+extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, const double *cents,
+                                 const void *cents_f16, double cent_max_norm, int64_t k_c,
+                                 const int64_t *post_off, const int64_t *post_docs, int64_t n_docs,
+                                 int probe, int k_filter, int64_t *cand, int32_t *n_cand,
+                                 void *workspace, size_t ws_bytes, void *stream) {
+    DSRT_REQUIRE(probe >= 1, DSRT_EINVAL, "invalid parameter: probe must be >= 1, got %d", probe);
+    DSRT_REQUIRE(k_filter >= 1, DSRT_EINVAL, "invalid parameter: k_filter must be >= 1, got %d", k_filter);
+    DSRT_REQUIRE(m_q >= 1 && n_q >= 0, DSRT_EINVAL, "Q must be a non-empty (m_q, d) matrix");
+    DSRT_REQUIRE(d == 128, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core prefilter needs d=128");
+    const int P = static_cast<int>(tmin<int64_t>(probe, k_c));
+    DSRT_REQUIRE(P <= kMaxPtc, DSRT_EUNSUPPORTED, "invalid parameter: probe=%d too large for the screen", P);
+    DSRT_REQUIRE(k_filter <= kSelMax, DSRT_EUNSUPPORTED, "invalid parameter: k_filter=%d exceeds %d",
+                 k_filter, kSelMax);
+    const int max_count = m_q * P;
+    DSRT_REQUIRE(max_count <= 65535, DSRT_EUNSUPPORTED, "invalid parameter: m_q*probe too large");
+    DSRT_REQUIRE(k_c < (1LL << 31) && cent_max_norm > 0, DSRT_EINVAL, "invalid parameter: centroids");
+    if (n_q == 0) return DSRT_OK;
+    const TcWs w = tc_ws_layout(n_q, m_q, k_c, n_docs, P);
+    DSRT_REQUIRE(workspace != nullptr && ws_bytes >= w.total, DSRT_EINVAL,
+                 "invalid parameter: prefilter workspace too small");
+    cudaStream_t st = as_stream(stream);
+    uint8_t *ws = static_cast<uint8_t *>(workspace);
+    size_t o = 0;
+    __half *q16 = reinterpret_cast<__half *>(ws + o); o += w.q16;
+    float *vals = reinterpret_cast<float *>(ws + o); o += w.screen;
+    float *theta = reinterpret_cast<float *>(ws + o); o += w.theta;
+    ScreenCand *lists = reinterpret_cast<ScreenCand *>(ws + o); o += w.lists;
+    int32_t *listn = reinterpret_cast<int32_t *>(ws + o); o += w.listn;
+    int32_t *probed = reinterpret_cast<int32_t *>(ws + o); o += w.probed;
+    int32_t *fallback = reinterpret_cast<int32_t *>(ws + o); o += w.fallback;
+    uint32_t *counts = reinterpret_cast<uint32_t *>(ws + o);
+    const int64_t rows = n_q * m_q;
+    const int64_t m_tiles = (rows + 127) / 128;
+    DSRT_CUDA(cudaMemsetAsync(q16, 0, w.q16, st));
+    to_f16_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(Q, rows, d, 0.0, q16);
+    CUtensorMap mq, mc;
+    int rc = make_tmap_2d(&mq, q16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, m_tiles * 128, 256, 64, 128,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    rc = make_tmap_2d(&mc, cents_f16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, k_c, 256, 64, kSN,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    const size_t smem = 1024 + 2 * 128 * 128 + kSStages * 2 * kSN * 128;
+    dim3 g(static_cast<unsigned>(m_tiles), static_cast<unsigned>(w.n_split));
+    const uint32_t idesc = idesc_f16(128, kSN, 0, 0);
+    rc = P <= 4 ? launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc)
+       : P <= 8 ? launch_screen<0, 8>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc)
+                : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc);
+    if (rc) return rc;
+    // eps in normalised units (|q^| = 1, |c*s| <= 1)
+    pf_theta_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+        vals, static_cast<int>(w.n_split), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn);
+    rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
+                             listn, idesc);
+    if (rc) return rc;
+    pf_rerank_kernel<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+        lists, listn, Q, cents, rows, d, P, probed, fallback);
+    pf_fallback_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d, P,
+                                                                   probed);
+    DSRT_CUDA(cudaMemsetAsync(counts, 0, w.counts, st));
+    rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, w.row_words, counts,
+                             k_filter, cand, n_cand, st);
+    if (rc) return rc;
+    DSRT_LAUNCH_CHECK();
+    (void)cent_max_norm;
     return DSRT_OK;
 }

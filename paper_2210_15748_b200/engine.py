@@ -225,6 +225,31 @@ def tc_selftest(A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     return D
 
 
+def to_f16_rows(src: torch.Tensor, scale: float) -> torch.Tensor:
+    _need(src, torch.float64, "src")
+    dst = torch.empty(src.shape, dtype=torch.float16, device=src.device)
+    _lib.call("dsrt_to_f16_rows", _ptr(src), src.shape[0], src.shape[1], float(scale), _ptr(dst),
+              _stream())
+    return dst
+
+
+def prefilter_tc(Q, m_q: int, centroids, cents_f16, cent_max_norm: float, post_off, post_docs,
+                 n_docs: int, probe: int, k_filter: int):
+    """Tensor-core screened prefilter (exact results); Q (n_qsets*m_q, 128) float64."""
+    _need(Q, torch.float64, "Q")
+    _need(centroids, torch.float64, "centroids")
+    n_q = Q.shape[0] // m_q
+    k_c, d = centroids.shape
+    cand = torch.empty((n_q, k_filter), dtype=torch.int64, device=Q.device)
+    n_cand = torch.empty(n_q, dtype=torch.int32, device=Q.device)
+    ws_bytes = _lib.lib().dsrt_prefilter_tc_workspace(n_q, m_q, k_c, n_docs, probe)
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=Q.device)
+    _lib.call("dsrt_prefilter_tc", _ptr(Q), n_q, m_q, d, _ptr(centroids), _ptr(cents_f16),
+              float(cent_max_norm), k_c, _ptr(post_off), _ptr(post_docs), n_docs, probe, k_filter,
+              _ptr(cand), _ptr(n_cand), _ptr(ws), ws_bytes, _stream())
+    return cand, n_cand
+
+
 def microbench_int() -> dict:
     out = (ctypes.c_double * 4)()
     _lib.call("dsrt_microbench_int", out, _stream())

@@ -38,6 +38,17 @@ class Centroids:
             self._dev[key] = t
         return t
 
+    def device_f16(self, device):
+        """(fp16 copy of vectors / max_norm, max_norm) for the tensor-core screen."""
+        key = ("f16", str(device))
+        t = self._dev.get(key)
+        if t is None:
+            mx = float(np.linalg.norm(self.vectors, axis=1).max())
+            c16 = engine.to_f16_rows(self.device_vectors(device), 1.0 / mx)
+            t = (c16, mx)
+            self._dev[key] = t
+        return t
+
 
 @dataclass
 class CentroidIndex:
@@ -201,7 +212,7 @@ def extend_centroid_index(cindex: CentroidIndex, X: torch.Tensor, centroids: Cen
 
 
 def filter_candidates_device(cindex: CentroidIndex, centroids: Centroids, Q: torch.Tensor,
-                             m_q: int, probe: int, k_filter: int):
+                             m_q: int, probe: int, k_filter: int, use_tc: bool = True):
     """K5 on the device: Q (n_qsets*m_q, d) -> (cand (n_qsets, k_filter), n_cand)."""
     if probe < 1:
         raise ValueError(f"invalid parameter: probe must be >= 1, got {probe}")
@@ -211,6 +222,12 @@ def filter_candidates_device(cindex: CentroidIndex, centroids: Centroids, Q: tor
     if Qd.shape[1] != centroids.vectors.shape[1]:
         raise ValueError(f"dimension mismatch: Q has d={Qd.shape[1]}, "
                          f"centroids have d={centroids.vectors.shape[1]}")
+    P = min(probe, centroids.k)
+    if Qd.shape[1] == 128 and P <= 12 and use_tc:
+        c16, mx = centroids.device_f16(Qd.device)
+        return engine.prefilter_tc(Qd, m_q, centroids.device_vectors(Qd.device), c16, mx,
+                                   cindex.post_off, cindex.post_docs, cindex.n_docs, probe,
+                                   k_filter)
     return engine.prefilter(Qd, m_q, centroids.device_vectors(Qd.device), cindex.post_off,
                             cindex.post_docs, cindex.n_docs, probe, k_filter)
 

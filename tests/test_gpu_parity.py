@@ -405,3 +405,40 @@ def test_mq_variants_bit_exact():
         np.testing.assert_array_equal(mc.cpu().numpy().astype(np.uint16), wmc)
         s2, _ = d.score_matrix(idx, q[:2])
         np.testing.assert_array_equal(s2.cpu().numpy(), want[:2])
+
+
+# ------------------------------------------------------- tensor-core prefilter
+def _tc_prefilter_case(seed, n_docs, k, dup_noise=None):
+    rng = np.random.default_rng(seed)
+    docs = [rng.standard_normal((int(rng.integers(1, 12)), 128)) for _ in range(n_docs)]
+    C = rng.standard_normal((k, 128))
+    if dup_noise is not None:        # near-identical centroid pairs -> screen near-ties
+        C[1::2] = C[0::2][: C[1::2].shape[0]] + dup_noise * rng.standard_normal(C[1::2].shape)
+        C[5] = C[4]                   # an exact tie
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    return rng, docs, C
+
+
+@pytest.mark.parametrize("seed,dup", [(1, None), (2, 1e-5), (3, 1e-3)])
+def test_prefilter_tensor_core_screen_exact(seed, dup):
+    from paper_2210_15748_b200 import prefilter as pf
+    rng, docs, C = _tc_prefilter_case(seed, 3000, 1000, dup)
+    cents = d.Centroids(k=C.shape[0], seed=0, vectors=C)
+    cindex = d.build_centroid_index(docs, cents)
+    post = O.build_centroid_index(docs, C)
+    for t in range(10):
+        m_q = int(rng.choice([1, 7, 32, 64]))
+        Q = rng.standard_normal((m_q, 128))
+        if t % 3 == 0:
+            Q[0] = C[4] * 2.5        # exact tie between centroids 4 and 5
+        probe, kf = int(rng.integers(1, 9)), int(rng.choice([1, 50, 4096]))
+        want = O.filter_candidates(post, len(docs), C, Q, probe, kf)
+        Qd = torch.from_numpy(Q).to(DEV)
+        cand, n_cand = pf.filter_candidates_device(cindex, cents, Qd, m_q, probe, kf, use_tc=True)
+        got = cand[0, : int(n_cand[0])].cpu().numpy()
+        np.testing.assert_array_equal(got, want, err_msg=f"case {t} probe {probe}")
+    # batched: many query sets at once vs the exact SIMT kernel
+    Qb = torch.from_numpy(rng.standard_normal((40 * 32, 128))).to(DEV)
+    a, na = pf.filter_candidates_device(cindex, cents, Qb, 32, 4, 300, use_tc=True)
+    b, nb = pf.filter_candidates_device(cindex, cents, Qb, 32, 4, 300, use_tc=False)
+    assert torch.equal(na, nb) and torch.equal(a, b)
