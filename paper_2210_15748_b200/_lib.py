@@ -15,7 +15,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libdessert_b200.so")
+LIB_PATH = os.environ.get("DSRT_LIB") or os.path.join(_HERE, "csrc", "libdessert_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "dessert_b200.h")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED, ERANGE = 0, 1, 2, 3, 4

@@ -327,11 +327,39 @@ constexpr size_t cand_smem_static() {
     return kCandWarps * (kBufs * kPieceBytes + kBufs * sizeof(uint64_t) + SlotGeom<QPL>::kBytes);
 }
 
+// Candidate metadata through a lane window: lane l holds (vbeg, vend) of
+// candidate base + l (vend = -1 for an invalid set index), loaded in one batch
+// per 32 candidates instead of a dependent load chain per candidate.
+struct CandWin {
+    int32_t base = -(1 << 30), len = 0;  // base: candidate index of lane 0
+    int64_t vb = 0;
+    __device__ __forceinline__ void load(int64_t b, int64_t e_hi, const int64_t *cand_row,
+                                         const int64_t *set_off, int64_t n_sets) {
+        base = static_cast<int32_t>(b);
+        const int64_t e = b + (threadIdx.x & 31);
+        int64_t sidx = -1;
+        if (e < e_hi) sidx = cand_row ? __ldg(cand_row + e) : e;
+        const bool ok = sidx >= 0 && sidx < n_sets;
+        vb = ok ? __ldg(set_off + sidx) : 0;
+        len = ok ? static_cast<int32_t>(__ldg(set_off + sidx + 1) - vb) : -1;
+    }
+    // (vbeg, vend) of candidate e; vend = -1 marks an invalid set index
+    __device__ __forceinline__ void get(int64_t e, int64_t e_hi, const int64_t *cand_row,
+                                        const int64_t *set_off, int64_t n_sets, int64_t &ovb,
+                                        int64_t &ove) {
+        if (e - base >= 32) load(e, e_hi, cand_row, set_off, n_sets);
+        const int l = static_cast<int>(e - base);
+        ovb = __shfl_sync(0xffffffffu, vb, l);
+        const int32_t n = __shfl_sync(0xffffffffu, len, l);
+        ove = n < 0 ? -1 : ovb + n;
+    }
+};
+
 // One warp = (query set, run of candidate slots).  Each warp streams its
 // candidates' records through a private kBufs-deep ring filled by
 // cp.async.bulk issued from lane 0.
 #ifndef DSRT_CAND_MINB
-#define DSRT_CAND_MINB 3
+#define DSRT_CAND_MINB 2
 #endif
 template <int K, int W, int QPL>
 __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
@@ -375,13 +403,15 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     Slots<QPL> slots{slot_mem + warp * SlotGeom<QPL>::kBytes};
     double *out_row = scores != nullptr ? scores + qset * cand_ld : nullptr;
 
-    auto set_of = [&](int64_t e) -> int64_t {
-        return cand ? __ldg(cand + qset * cand_ld + e) : e;
-    };
+    // candidate metadata through lane windows: lane l holds (vbeg, vend) of
+    // candidate base + l (vbeg = vend = 0 for an invalid set index), loaded in
+    // one batch per 32 candidates instead of a dependent load chain per set.
+    const int64_t *cand_row = cand ? cand + qset * cand_ld : nullptr;
+    CandWin pwin, cwin;
     // producer iterator (lane-uniform state; lane 0 issues the copies)
-    int64_t pe = e_lo, ps = set_of(pe);
-    bool pvalid = ps >= 0 && ps < n_sets;
-    int64_t pv = pvalid ? __ldg(set_off + ps) : 0, pvend = pvalid ? __ldg(set_off + ps + 1) : 0;
+    int64_t pe = e_lo, pv, pvend;
+    pwin.get(pe, e_hi, cand_row, set_off, n_sets, pv, pvend);
+    if (pvend < 0) { pv = 0; pvend = 0; }
     int64_t issued = 0;
     auto issue = [&]() {  // issue the next piece (pe, [pv, ..)) into buffer issued % kBufs
         const int b = static_cast<int>(issued % kBufs);
@@ -401,17 +431,16 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         if (pe < e_hi && pv >= pvend) {  // advance to the next candidate
             ++pe;
             if (pe < e_hi) {
-                ps = set_of(pe);
-                pvalid = ps >= 0 && ps < n_sets;
-                pv = pvalid ? __ldg(set_off + ps) : 0;
-                pvend = pvalid ? __ldg(set_off + ps + 1) : 0;
+                pwin.get(pe, e_hi, cand_row, set_off, n_sets, pv, pvend);
+                if (pvend < 0) { pv = 0; pvend = 0; }
             }
         }
     };
     // consumer iterator
-    int64_t ce = e_lo, cs = set_of(ce), slot_col = e_lo;
-    bool cvalid = cs >= 0 && cs < n_sets;
-    int64_t cv = cvalid ? __ldg(set_off + cs) : 0, cvend = cvalid ? __ldg(set_off + cs + 1) : 0;
+    int64_t ce = e_lo, cv, cvend, slot_col = e_lo;
+    cwin.get(ce, e_hi, cand_row, set_off, n_sets, cv, cvend);
+    bool cvalid = cvend >= 0;
+    if (!cvalid) { cv = 0; cvend = 0; }
     int64_t consumed = 0;
     for (int i = 0; i < kBufs; ++i) issue();
     while (ce < e_hi) {
@@ -431,10 +460,9 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
             }
             ++ce;
             if (ce < e_hi) {
-                cs = set_of(ce);
-                cvalid = cs >= 0 && cs < n_sets;
-                cv = cvalid ? __ldg(set_off + cs) : 0;
-                cvend = cvalid ? __ldg(set_off + cs + 1) : 0;
+                cwin.get(ce, e_hi, cand_row, set_off, n_sets, cv, cvend);
+                cvalid = cvend >= 0;
+                if (!cvalid) { cv = 0; cvend = 0; }
             }
         }
         __syncwarp();
@@ -532,7 +560,7 @@ static int run_one(const ScoreArgs &a, cudaStream_t st) {
                                       a.qrecs, a.n_qsets, a.m_q, a.L, a.lut, a.scores, a.mc,
                                       a.mc_stride, a.mc_q0, st);
     // register-block several query sets per warp when there are enough of them
-    if constexpr (QPL == 1 && W <= 2) {
+    if constexpr (QPL == 1 && W <= 2 && K <= 8) {
         const int qs = a.qs_override > 0 ? a.qs_override : (a.n_qsets >= 256 ? (W == 1 ? 4 : 2) : 1);
         if (qs == 4)
             return launch_all<K, W, QPL, 4>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
