@@ -76,8 +76,8 @@ int dsrt_hash(const void *X, int x_dtype, int64_t n, int d, const void *planes, 
  *     bad (may be NULL) counts sizes < 1 ("empty set") or > 65535 ("set too large").
  *   dsrt_counting_sort: vectors tagged with set ids (any order) -> set_off (N+1)
  *     and a stable permutation perm (n) grouping vectors by set (counting sort:
- *     histogram, scan, scatter, per-set stabilisation).  workspace from
- *     dsrt_counting_sort_workspace.
+ *     histogram + scan for the offsets, stable LSD radix scatter for perm).
+ *     workspace from dsrt_counting_sort_workspace.
  *   dsrt_gather_rows: dst[i] = src[perm[i]] for rows of row_bytes (multiple of 4).
  */
 int dsrt_codes_to_records(const void *codes, int code_bytes, int64_t n, int L, int C,
@@ -164,6 +164,31 @@ int dsrt_prefilter_tc(const double *Q, int64_t n_qsets, int m_q, int d, const do
 size_t dsrt_prefilter_tc_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
 /* rows of float64 -> fp16 (scale > 0: multiply by scale; scale <= 0: normalise each row) */
 int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scale, void *dst, void *stream);
+/* rows of float64 -> bf16 times scale (> 0) */
+int dsrt_to_bf16_rows(const double *src, int64_t n, int d, double scale, void *dst, void *stream);
+
+/*
+ * K6 -- centroid assignment for build_centroid_index (prefilter.py:85-108):
+ * assign[i] = argmax_c <X[i], centroids[c]> (lowest c on ties, as np.argmax),
+ * exact: tensor-core screen + float64 re-rank + exact fallback.  X of
+ * x_dtype (fp16/bf16 rows are read in place; f32/f64 are normalised into an
+ * fp16 staging buffer); cents_lp = fp16 (bf16 for bf16 X) copy of
+ * centroids / max_c |c|.  d = 128.
+ */
+int dsrt_assign_centroids(const void *X, int x_dtype, int64_t n, int d, const double *centroids,
+                          const void *cents_lp, int64_t k_c, int32_t *assign_out, void *workspace,
+                          size_t workspace_bytes, void *stream);
+size_t dsrt_assign_centroids_workspace(int64_t n, int64_t k_c);
+/*
+ * Postings from assignments: vectors grouped by document (set_off, N+1);
+ * post_off (k_c + 1), post_docs (capacity n_vec), *n_post (device int64):
+ * posting c = ascending, deduplicated documents having a vector assigned to c.
+ */
+int dsrt_postings_from_assign(const int32_t *assign, int64_t n_vec, const int64_t *set_off,
+                              int64_t n_docs, int64_t k_c, int64_t *post_off, int64_t *post_docs,
+                              int64_t *n_post, void *workspace, size_t workspace_bytes,
+                              void *stream);
+size_t dsrt_postings_workspace(int64_t n_vec, int64_t k_c);
 
 /* Diagnostic: D(M,N) f32 = A(M,128) . B(N,128)^T on the tcgen05 path (TMA ->
  * 128B-swizzled smem -> UMMA -> TMEM -> tcgen05.ld); fp16 (0) or bf16 (1)

@@ -53,6 +53,11 @@ SIGNATURES = {
                                  _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "dsrt_prefilter_tc_workspace": (_sz, [_i64, _i32, _i64, _i64, _i32]),
     "dsrt_to_f16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),
+    "dsrt_to_bf16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),
+    "dsrt_assign_centroids": (_i32, [_vp, _i32, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "dsrt_assign_centroids_workspace": (_sz, [_i64, _i64]),
+    "dsrt_postings_from_assign": (_i32, [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "dsrt_postings_workspace": (_sz, [_i64, _i64]),
     "dsrt_tinytable": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "dsrt_microbench_int": (_i32, [_vp, _vp]),
     "dsrt_tc_selftest": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, _vp]),

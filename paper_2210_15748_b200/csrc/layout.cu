@@ -146,6 +146,17 @@ static int exclusive_scan(const int64_t *in, int64_t n, int64_t *out, uint32_t *
     return DSRT_OK;
 }
 
+int exclusive_scan_i64(const int64_t *in, int64_t n, int64_t *out, void *ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    return exclusive_scan(in, n, out, nullptr, 0, ws, ws_bytes, st);
+}
+size_t scan_ws_bytes(int64_t n) {
+    return static_cast<size_t>((n + kScanTile - 1) / kScanTile + 1) * sizeof(int64_t);
+}
+size_t radix_sort_ws(int64_t n);
+int radix_sort_perm(const int64_t *keys, int64_t n, int key_bits, int64_t *perm_out, void *ws,
+                    size_t ws_bytes, cudaStream_t st);
+
 // ---------------------------------------------------------- counting sort
 __global__ void histogram_kernel(const int64_t *__restrict__ set_of, int64_t n, int64_t n_sets,
                                  unsigned long long *__restrict__ counts, uint32_t *bad) {
@@ -157,54 +168,6 @@ __global__ void histogram_kernel(const int64_t *__restrict__ set_of, int64_t n, 
         return;
     }
     atomicAdd(counts + s, 1ull);
-}
-
-__global__ void scatter_kernel(const int64_t *__restrict__ set_of, int64_t n, int64_t n_sets,
-                               const int64_t *__restrict__ set_off,
-                               unsigned long long *__restrict__ cursor, int64_t *__restrict__ perm) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const int64_t s = set_of[i];
-    if (s < 0 || s >= n_sets) return;
-    const int64_t pos = set_off[s] + static_cast<int64_t>(atomicAdd(cursor + s, 1ull));
-    perm[pos] = i;
-}
-
-// Stabilise: sort each set's slice of perm ascending (block per set, smem
-// bitonic for sets up to kStableMax; larger sets flag EUNSUPPORTED).
-constexpr int kStableMax = 4096;
-__global__ void stabilise_kernel(const int64_t *__restrict__ set_off, int64_t n_sets,
-                                 int64_t *__restrict__ perm, uint32_t *too_big) {
-    __shared__ int64_t buf[kStableMax];
-    for (int64_t s = blockIdx.x; s < n_sets; s += gridDim.x) {
-        const int64_t lo = set_off[s], m = set_off[s + 1] - lo;
-        if (m <= 1) continue;
-        if (m > kStableMax) {
-            if (threadIdx.x == 0) atomicAdd(too_big, 1u);
-            continue;
-        }
-        int p2 = 1;
-        while (p2 < m) p2 <<= 1;
-        for (int i = threadIdx.x; i < p2; i += blockDim.x) buf[i] = i < m ? perm[lo + i] : INT64_MAX;
-        __syncthreads();
-        for (int size = 2; size <= p2; size <<= 1)
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int i = threadIdx.x; i < p2; i += blockDim.x) {
-                    const int j = i ^ stride;
-                    if (j > i) {
-                        const bool up = (i & size) == 0;
-                        if ((buf[i] > buf[j]) == up) {
-                            const int64_t t = buf[i];
-                            buf[i] = buf[j];
-                            buf[j] = t;
-                        }
-                    }
-                }
-                __syncthreads();
-            }
-        for (int i = threadIdx.x; i < m; i += blockDim.x) perm[lo + i] = buf[i];
-        __syncthreads();
-    }
 }
 
 __global__ void gather_rows_kernel(const uint32_t *__restrict__ src, int64_t row_words,
@@ -293,9 +256,8 @@ extern "C" int dsrt_sizes_to_offsets(const int64_t *sizes, int64_t n_sets, int64
 }
 
 extern "C" size_t dsrt_counting_sort_workspace(int64_t n, int64_t n_sets) {
-    (void)n;
-    // counts (n_sets u64) + cursor (n_sets u64) + scan tiles + 2 flags
-    return static_cast<size_t>(n_sets) * 16 + dsrt_scan_workspace(n_sets) + 16;
+    // counts (n_sets u64) + scan tiles + flags + radix sort workspace
+    return static_cast<size_t>(n_sets) * 8 + dsrt_scan_workspace(n_sets) + 256 + radix_sort_ws(n);
 }
 
 extern "C" int dsrt_counting_sort(const int64_t *set_of_vec, int64_t n, int64_t n_sets,
@@ -308,10 +270,10 @@ extern "C" int dsrt_counting_sort(const int64_t *set_of_vec, int64_t n, int64_t 
     cudaStream_t st = as_stream(stream);
     uint8_t *ws = static_cast<uint8_t *>(workspace);
     unsigned long long *counts = reinterpret_cast<unsigned long long *>(ws);
-    unsigned long long *cursor = counts + n_sets;
-    uint8_t *scan_ws = ws + n_sets * 16;
+    uint8_t *scan_ws = ws + n_sets * 8;
     uint32_t *flags = reinterpret_cast<uint32_t *>(scan_ws + dsrt_scan_workspace(n_sets));
-    DSRT_CUDA(cudaMemsetAsync(ws, 0, n_sets * 16, st));
+    void *rws = scan_ws + dsrt_scan_workspace(n_sets) + 256;
+    DSRT_CUDA(cudaMemsetAsync(ws, 0, n_sets * 8, st));
     DSRT_CUDA(cudaMemsetAsync(flags, 0, 16, st));
     const unsigned blocks = static_cast<unsigned>((n + 255) / 256);
     if (n > 0) histogram_kernel<<<blocks, 256, 0, st>>>(set_of_vec, n, n_sets, counts, flags);
@@ -319,18 +281,14 @@ extern "C" int dsrt_counting_sort(const int64_t *set_of_vec, int64_t n, int64_t 
     int rc = exclusive_scan(reinterpret_cast<const int64_t *>(counts), n_sets, set_off_out, nullptr,
                             0, scan_ws, dsrt_scan_workspace(n_sets), st);
     if (rc != DSRT_OK) return rc;
-    if (n > 0) scatter_kernel<<<blocks, 256, 0, st>>>(set_of_vec, n, n_sets, set_off_out, cursor, perm_out);
-    stabilise_kernel<<<static_cast<unsigned>(tmin<int64_t>(n_sets, 4 * 148)), 512, 0, st>>>(
-        set_off_out, n_sets, perm_out, flags + 1);
-    DSRT_LAUNCH_CHECK();
-    uint32_t h[2];
-    DSRT_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));
+    uint32_t h = 0;
+    DSRT_CUDA(cudaMemcpyAsync(&h, flags, sizeof(h), cudaMemcpyDeviceToHost, st));
     DSRT_CUDA(cudaStreamSynchronize(st));
-    DSRT_REQUIRE(h[0] == 0, DSRT_ERANGE, "set index out of range: %u vectors name a set outside [0, %lld)",
-                 h[0], (long long)n_sets);
-    DSRT_REQUIRE(h[1] == 0, DSRT_EUNSUPPORTED, "set too large: %u sets exceed %d vectors for the stable counting sort",
-                 h[1], kStableMax);
-    return DSRT_OK;
+    DSRT_REQUIRE(h == 0, DSRT_ERANGE, "set index out of range: %u vectors name a set outside [0, %lld)",
+                 h, (long long)n_sets);
+    int bits = 1;
+    while (bits < 63 && (1LL << bits) < n_sets) ++bits;
+    return radix_sort_perm(set_of_vec, n, bits, perm_out, rws, radix_sort_ws(n), st);
 }
 
 extern "C" int dsrt_gather_rows(const void *src, int64_t row_bytes, const int64_t *perm, int64_t n,

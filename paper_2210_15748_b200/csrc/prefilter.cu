@@ -12,6 +12,7 @@
 //                     (prefilter.py:142-144): count histogram -> threshold
 //                     count c*, all docs above it, the lowest-index docs at c*
 //                     in one ordered pass, then a shared-memory bitonic sort.
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include "tc_common.cuh"
@@ -463,20 +464,34 @@ struct ScreenCand {
     int32_t id;
 };
 
-__global__ void to_f16_rows_kernel(const double *__restrict__ src, int64_t n, int d, double scale,
+template <typename T>
+__device__ __forceinline__ double as_f64(T v);
+template <>
+__device__ __forceinline__ double as_f64<double>(double v) { return v; }
+template <>
+__device__ __forceinline__ double as_f64<float>(float v) { return static_cast<double>(v); }
+template <>
+__device__ __forceinline__ double as_f64<__half>(__half v) { return static_cast<double>(__half2float(v)); }
+template <>
+__device__ __forceinline__ double as_f64<__nv_bfloat16>(__nv_bfloat16 v) {
+    return static_cast<double>(__bfloat162float(v));
+}
+
+template <typename TS>
+__global__ void to_f16_rows_kernel(const TS *__restrict__ src, int64_t n, int d, double scale,
                                    __half *__restrict__ dst) {
     const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
-    const double *x = src + row * d;
+    const TS *x = src + row * d;
     double s = scale;
     if (scale <= 0.0) {  // per-row normalisation
         double ss = 0.0;
-        for (int k = lane; k < d; k += 32) ss = fma(x[k], x[k], ss);
+        for (int k = lane; k < d; k += 32) ss = fma(as_f64(x[k]), as_f64(x[k]), ss);
         for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
         s = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
     }
-    for (int k = lane; k < d; k += 32) dst[row * d + k] = __double2half(x[k] * s);
+    for (int k = lane; k < d; k += 32) dst[row * d + k] = __double2half(as_f64(x[k]) * s);
 }
 
 __device__ __forceinline__ bool s_better(float sa, int ia, float sb, int ib) {
@@ -650,10 +665,21 @@ __global__ void __launch_bounds__(kSThreads, 1)
 }
 
 // thread per row: theta = (P-th best approx over all splits) - 2 eps
+// (theta scaled by |x| when the screen ran on raw, unnormalised rows Xraw)
+template <typename TQ>
 __global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int64_t n_rows, int P,
-                                float eps2, float *__restrict__ theta, int32_t *__restrict__ list_n) {
+                                float eps2, float *__restrict__ theta, int32_t *__restrict__ list_n,
+                                const TQ *__restrict__ Xraw, int d) {
     const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (row >= n_rows) return;
+    if (Xraw != nullptr) {
+        double ss = 0.0;
+        for (int k = 0; k < d; ++k) {
+            const double v = as_f64(Xraw[row * d + k]);
+            ss = fma(v, v, ss);
+        }
+        eps2 = static_cast<float>(eps2 * sqrt(ss) * 1.0001);
+    }
     float tv[kMaxPtc];
 #pragma unroll
     for (int j = 0; j < kMaxPtc; ++j) tv[j] = -INFINITY;
@@ -677,8 +703,9 @@ __global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int
 
 // warp per row: exact float64 re-rank of the collected candidates -> probed ids;
 // flags rows whose list overflowed (fallback to the exact scan).
+template <typename TQ>
 __global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int32_t *__restrict__ list_n,
-                                 const double *__restrict__ Q, const double *__restrict__ cents,
+                                 const TQ *__restrict__ Q, const double *__restrict__ cents,
                                  int64_t n_rows, int d, int P, int32_t *__restrict__ probed,
                                  int32_t *__restrict__ fallback) {
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -694,10 +721,10 @@ __global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int
     int eid = 0x7fffffff;
     if (lane < n) {
         const int c = lists[row * kCandMax + lane].id;
-        const double *q = Q + row * d;
+        const TQ *q = Q + row * d;
         const double *cv = cents + static_cast<int64_t>(c) * d;
         double acc = 0.0;
-        for (int k = 0; k < d; ++k) acc = fma(q[k], cv[k], acc);
+        for (int k = 0; k < d; ++k) acc = fma(as_f64(q[k]), cv[k], acc);
         ex = acc;
         eid = c;
     }
@@ -708,8 +735,9 @@ __global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int
 }
 
 // exact float64 scan for flagged rows (one CTA per row; rare)
+template <typename TQ>
 __global__ void __launch_bounds__(256)
-    pf_fallback_kernel(const int32_t *__restrict__ fallback, const double *__restrict__ Q,
+    pf_fallback_kernel(const int32_t *__restrict__ fallback, const TQ *__restrict__ Q,
                        const double *__restrict__ cents, int64_t n_rows, int64_t k_c, int d, int P,
                        int32_t *__restrict__ probed) {
     const int64_t row = blockIdx.x;
@@ -718,7 +746,7 @@ __global__ void __launch_bounds__(256)
     __shared__ double cs[8][32];
     __shared__ int ci[8][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int k = threadIdx.x; k < d && k < 512; k += blockDim.x) q[k] = Q[row * d + k];
+    for (int k = threadIdx.x; k < d && k < 512; k += blockDim.x) q[k] = as_f64(Q[row * d + k]);
     __syncthreads();
     double ts = -INFINITY;
     int ti = 0x7fffffff;
@@ -813,7 +841,7 @@ extern "C" int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scal
                                 void *stream) {
     DSRT_REQUIRE(n >= 0 && d >= 1, DSRT_EINVAL, "invalid parameter: n=%lld d=%d", (long long)n, d);
     if (n == 0) return DSRT_OK;
-    to_f16_rows_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, as_stream(stream)>>>(
+    to_f16_rows_kernel<double><<<static_cast<unsigned>((n + 7) / 8), 256, 0, as_stream(stream)>>>(
         src, n, d, scale, static_cast<__half *>(dst));
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
@@ -889,7 +917,7 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     const int64_t rows = n_q * m_q;
     const int64_t m_tiles = (rows + 127) / 128;
     DSRT_CUDA(cudaMemsetAsync(q16, 0, w.q16, st));
-    to_f16_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(Q, rows, d, 0.0, q16);
+    to_f16_rows_kernel<double><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(Q, rows, d, 0.0, q16);
     CUtensorMap mq, mc;
     int rc = make_tmap_2d(&mq, q16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, m_tiles * 128, 256, 64, 128,
                           CU_TENSOR_MAP_SWIZZLE_128B);
@@ -905,20 +933,150 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
                 : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc);
     if (rc) return rc;
     // eps in normalised units (|q^| = 1, |c*s| <= 1)
-    pf_theta_kernel<<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
-        vals, static_cast<int>(w.n_split), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn);
+    pf_theta_kernel<double><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+        vals, static_cast<int>(w.n_split), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn,
+        nullptr, d);
     rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
                              listn, idesc);
     if (rc) return rc;
-    pf_rerank_kernel<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+    pf_rerank_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
         lists, listn, Q, cents, rows, d, P, probed, fallback);
-    pf_fallback_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d, P,
-                                                                   probed);
+    pf_fallback_kernel<double><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d,
+                                                                           P, probed);
     DSRT_CUDA(cudaMemsetAsync(counts, 0, w.counts, st));
     rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, w.row_words, counts,
                              k_filter, cand, n_cand, st);
     if (rc) return rc;
     DSRT_LAUNCH_CHECK();
     (void)cent_max_norm;
+    return DSRT_OK;
+}
+
+// ===================================================================
+// Exact centroid assignment (build_centroid_index, prefilter.py:85-108):
+// argmax_c <x, c> with np.argmax's first-index tie rule, via the same
+// tensor-core screen (P = 1) + float64 re-rank + exact fallback.  fp16/bf16
+// rows feed TMA directly (no copy; the screen error then scales with |x|);
+// float32/float64 rows are normalised into an fp16 staging buffer.
+// ===================================================================
+namespace dsrt {
+constexpr int64_t kAssignChunk = 1 << 22;
+
+static size_t assign_ws_layout(int64_t n, size_t *parts) {
+    const int64_t ch = tmin<int64_t>(n, kAssignChunk);
+    const int64_t tiles = (ch + 127) / 128;
+    parts[0] = align256(static_cast<size_t>(tiles * 128) * 128 * 2);        // q16 staging
+    parts[1] = align256(static_cast<size_t>(ch) * kMaxPtc * sizeof(float));  // pass-0 values (1 split)
+    parts[2] = align256(static_cast<size_t>(ch) * sizeof(float));            // theta
+    parts[3] = align256(static_cast<size_t>(ch) * kCandMax * sizeof(ScreenCand));
+    parts[4] = align256(static_cast<size_t>(ch) * sizeof(int32_t));          // list counts
+    parts[5] = align256(static_cast<size_t>(ch) * sizeof(int32_t));          // fallback flags
+    size_t t = 0;
+    for (int i = 0; i < 6; ++i) t += parts[i];
+    return t;
+}
+
+template <typename TQ>
+static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const void *cents_lp,
+                       int64_t k_c, bool raw, bool bf16, int32_t *assign_out, void *ws,
+                       cudaStream_t st) {
+    size_t part[6];
+    assign_ws_layout(n, part);
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    __half *q16 = reinterpret_cast<__half *>(w);
+    float *vals = reinterpret_cast<float *>(w + part[0]);
+    float *theta = reinterpret_cast<float *>(w + part[0] + part[1]);
+    ScreenCand *lists = reinterpret_cast<ScreenCand *>(w + part[0] + part[1] + part[2]);
+    int32_t *listn = reinterpret_cast<int32_t *>(w + part[0] + part[1] + part[2] + part[3]);
+    int32_t *fallback = reinterpret_cast<int32_t *>(w + part[0] + part[1] + part[2] + part[3] + part[4]);
+    const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUtensorMap mc;
+    int rc = make_tmap_2d(&mc, cents_lp, dt, 128, k_c, 256, 64, kSN, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    const size_t smem = 1024 + 2 * 128 * 128 + kSStages * 2 * kSN * 128;
+    const uint32_t idesc = idesc_f16(128, kSN, bf16, bf16);
+    const int64_t n_tiles_c = (k_c + kSN - 1) / kSN;
+    const double eps = raw ? (bf16 ? 8e-3 : 1.2e-3) : kScreenEps;
+    for (int64_t r0 = 0; r0 < n; r0 += kAssignChunk) {
+        const int64_t rows = tmin<int64_t>(kAssignChunk, n - r0);
+        const int64_t m_tiles = (rows + 127) / 128;
+        CUtensorMap mq;
+        if (raw) {
+            rc = make_tmap_2d(&mq, X + r0 * d, dt, 128, rows, 256, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        } else {
+            DSRT_CUDA(cudaMemsetAsync(q16, 0, part[0], st));
+            to_f16_rows_kernel<TQ><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(X + r0 * d, rows, d, 0.0, q16);
+            rc = make_tmap_2d(&mq, q16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, m_tiles * 128, 256, 64, 128,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+        }
+        if (rc) return rc;
+        const int sms = sm_count();
+        int64_t n_split = tmax<int64_t>(1, tmin<int64_t>(n_tiles_c, (sms + m_tiles / 2) / m_tiles));
+        const int64_t tps = (n_tiles_c + n_split - 1) / n_split;
+        n_split = (n_tiles_c + tps - 1) / tps;
+        dim3 g(static_cast<unsigned>(m_tiles), static_cast<unsigned>(n_split));
+        // vals is sized for one split; more splits only happen for small chunks
+        float *v = vals;
+        float *vtmp = nullptr;
+        if (n_split > 1) {
+            DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&vtmp), rows * n_split * kMaxPtc * sizeof(float), st));
+            v = vtmp;
+        }
+        rc = launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, v, nullptr, nullptr, nullptr, idesc);
+        if (rc) return rc;
+        pf_theta_kernel<TQ><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+            v, static_cast<int>(n_split), rows, 1, static_cast<float>(2.0 * eps), theta, listn,
+            raw ? X + r0 * d : nullptr, d);
+        rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, nullptr, theta, lists, listn, idesc);
+        if (rc) return rc;
+        pf_rerank_kernel<TQ><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+            lists, listn, X + r0 * d, cents, rows, d, 1, assign_out + r0, fallback);
+        pf_fallback_kernel<TQ><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, X + r0 * d, cents, rows,
+                                                                             k_c, d, 1, assign_out + r0);
+        if (vtmp) cudaFreeAsync(vtmp, st);
+        DSRT_LAUNCH_CHECK();
+    }
+    return DSRT_OK;
+}
+}  // namespace dsrt
+
+extern "C" size_t dsrt_assign_centroids_workspace(int64_t n, int64_t k_c) {
+    size_t parts[6];
+    (void)k_c;
+    return assign_ws_layout(tmax<int64_t>(n, 1), parts);
+}
+
+extern "C" int dsrt_assign_centroids(const void *X, int x_dtype, int64_t n, int d, const double *cents,
+                                     const void *cents_lp, int64_t k_c, int32_t *assign_out,
+                                     void *workspace, size_t ws_bytes, void *stream) {
+    DSRT_REQUIRE(d == 128, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core assignment needs d=128");
+    DSRT_REQUIRE(k_c >= 1 && k_c < (1LL << 31), DSRT_EINVAL, "invalid parameter: k=%lld", (long long)k_c);
+    DSRT_REQUIRE(ws_bytes >= dsrt_assign_centroids_workspace(n, k_c), DSRT_EINVAL,
+                 "invalid parameter: assignment workspace too small");
+    if (n == 0) return DSRT_OK;
+    cudaStream_t st = as_stream(stream);
+    switch (x_dtype) {
+        case DSRT_F16: return assign_impl<__half>(static_cast<const __half *>(X), n, d, cents, cents_lp, k_c, true, false, assign_out, workspace, st);
+        case DSRT_BF16: return assign_impl<__nv_bfloat16>(static_cast<const __nv_bfloat16 *>(X), n, d, cents, cents_lp, k_c, true, true, assign_out, workspace, st);
+        case DSRT_F32: return assign_impl<float>(static_cast<const float *>(X), n, d, cents, cents_lp, k_c, false, false, assign_out, workspace, st);
+        case DSRT_F64: return assign_impl<double>(static_cast<const double *>(X), n, d, cents, cents_lp, k_c, false, false, assign_out, workspace, st);
+        default: break;
+    }
+    set_error("invalid parameter: x dtype %d", x_dtype);
+    return DSRT_EINVAL;
+}
+
+__global__ void to_bf16_rows_kernel(const double *__restrict__ src, int64_t n, int d, double scale,
+                                    __nv_bfloat16 *__restrict__ dst) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n * d) dst[i] = __double2bfloat16(src[i] * scale);
+}
+
+extern "C" int dsrt_to_bf16_rows(const double *src, int64_t n, int d, double scale, void *dst, void *stream) {
+    DSRT_REQUIRE(n >= 0 && d >= 1 && scale > 0, DSRT_EINVAL, "invalid parameter: n=%lld d=%d", (long long)n, d);
+    if (n == 0) return DSRT_OK;
+    to_bf16_rows_kernel<<<static_cast<unsigned>((n * d + 255) / 256), 256, 0, as_stream(stream)>>>(
+        src, n, d, scale, static_cast<__nv_bfloat16 *>(dst));
+    DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }

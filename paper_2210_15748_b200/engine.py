@@ -250,6 +250,44 @@ def prefilter_tc(Q, m_q: int, centroids, cents_f16, cent_max_norm: float, post_o
     return cand, n_cand
 
 
+def to_bf16_rows(src: torch.Tensor, scale: float) -> torch.Tensor:
+    _need(src, torch.float64, "src")
+    dst = torch.empty(src.shape, dtype=torch.bfloat16, device=src.device)
+    _lib.call("dsrt_to_bf16_rows", _ptr(src), src.shape[0], src.shape[1], float(scale), _ptr(dst),
+              _stream())
+    return dst
+
+
+def assign_centroids(X: torch.Tensor, centroids: torch.Tensor, cents_lp: torch.Tensor):
+    """Exact argmax centroid per row of X (n, 128) -> int32 (n,)."""
+    if X.dtype not in _DT:
+        raise ValueError(f"invalid parameter: unsupported vector dtype {X.dtype}")
+    X = X.contiguous()
+    _need(centroids, torch.float64, "centroids")
+    n, d = X.shape
+    out = torch.empty(n, dtype=torch.int32, device=X.device)
+    ws_bytes = _lib.lib().dsrt_assign_centroids_workspace(n, centroids.shape[0])
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=X.device)
+    _lib.call("dsrt_assign_centroids", _ptr(X), _DT[X.dtype], n, d, _ptr(centroids),
+              _ptr(cents_lp), centroids.shape[0], _ptr(out), _ptr(ws), ws_bytes, _stream())
+    return out
+
+
+def postings_from_assign(assign: torch.Tensor, set_off: torch.Tensor, n_docs: int, k_c: int):
+    """-> (post_off (k_c+1) int64, post_docs int64) with deduplicated ascending docs."""
+    _need(assign, torch.int32, "assign")
+    _need(set_off, torch.int64, "set_off")
+    n = assign.shape[0]
+    post_off = torch.empty(k_c + 1, dtype=torch.int64, device=assign.device)
+    post_docs = torch.empty(n, dtype=torch.int64, device=assign.device)
+    n_post = torch.zeros(1, dtype=torch.int64, device=assign.device)
+    ws_bytes = _lib.lib().dsrt_postings_workspace(n, k_c)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=assign.device)
+    _lib.call("dsrt_postings_from_assign", _ptr(assign), n, _ptr(set_off), n_docs, k_c,
+              _ptr(post_off), _ptr(post_docs), _ptr(n_post), _ptr(ws), ws_bytes, _stream())
+    return post_off, post_docs[: int(n_post.item())].clone()
+
+
 def microbench_int() -> dict:
     out = (ctypes.c_double * 4)()
     _lib.call("dsrt_microbench_int", out, _stream())

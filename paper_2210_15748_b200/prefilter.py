@@ -38,16 +38,27 @@ class Centroids:
             self._dev[key] = t
         return t
 
-    def device_f16(self, device):
-        """(fp16 copy of vectors / max_norm, max_norm) for the tensor-core screen."""
-        key = ("f16", str(device))
+    def device_lowp(self, device, bf16: bool):
+        """fp16 / bf16 copy of vectors / max_norm (the screen's B operand)."""
+        key = ("bf16" if bf16 else "f16", str(device))
         t = self._dev.get(key)
         if t is None:
-            mx = float(np.linalg.norm(self.vectors, axis=1).max())
-            c16 = engine.to_f16_rows(self.device_vectors(device), 1.0 / mx)
-            t = (c16, mx)
+            mx = self.max_norm()
+            dv = self.device_vectors(device)
+            t = engine.to_bf16_rows(dv, 1.0 / mx) if bf16 else engine.to_f16_rows(dv, 1.0 / mx)
             self._dev[key] = t
         return t
+
+    def max_norm(self) -> float:
+        mx = self._dev.get("max_norm")
+        if mx is None:
+            mx = float(np.linalg.norm(self.vectors, axis=1).max())
+            self._dev["max_norm"] = mx
+        return mx
+
+    def device_f16(self, device):
+        """(fp16 copy of vectors / max_norm, max_norm) for the tensor-core screen."""
+        return self.device_lowp(device, bf16=False), self.max_norm()
 
 
 @dataclass
@@ -137,6 +148,17 @@ def _assign(X: torch.Tensor, cvec: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def _check_nonzero_rows(X: torch.Tensor, off: torch.Tensor, chunk: int = 1 << 22) -> None:
+    """prefilter.py:37-44 error ("zero vector in document i"), chunked (no float64 copy)."""
+    for lo in range(0, X.shape[0], chunk):
+        blk = X[lo:lo + chunk]
+        z = (blk == 0).all(dim=1)
+        if bool(z.any()):
+            row = lo + int(torch.nonzero(z)[0].item())
+            doc = int(torch.searchsorted(off, torch.tensor([row], device=off.device), right=True)[0]) - 1
+            raise ValueError(f"zero vector in document {doc}: cannot assign to a centroid")
+
+
 def build_centroid_index(docs, centroids: Centroids, set_off: torch.Tensor | None = None,
                          n_docs: int | None = None, device="cuda") -> CentroidIndex:
     """Invert centroid assignment (prefilter.py:85-108): posting c = docs with a
@@ -146,7 +168,7 @@ def build_centroid_index(docs, centroids: Centroids, set_off: torch.Tensor | Non
     vectors grouped by set with ``set_off``.
     """
     if isinstance(docs, torch.Tensor) and set_off is not None:
-        X = docs.to(torch.float64)
+        X = docs
         off = set_off
         N = int(n_docs)
     else:
@@ -160,9 +182,12 @@ def build_centroid_index(docs, centroids: Centroids, set_off: torch.Tensor | Non
                     f"dimension mismatch: document {i} has d={S.shape[1]}, "
                     f"centroids have d={centroids.vectors.shape[1]}")
         sizes = np.array([S.shape[0] for S in mats], dtype=np.int64)
-        X = torch.cat([_as_dev(S, device) for S in mats]).to(torch.float64)
+        X = torch.cat([_as_dev(S, device).to(torch.float64) for S in mats])
         off = torch.from_numpy(np.concatenate([[0], np.cumsum(sizes)])).to(X.device)
         N = len(mats)
+    _check_nonzero_rows(X, off)
+    if X.shape[1] == 128:
+        return build_centroid_index_native(X, centroids, off, N)
     Xu = _unit_rows_dev(X, "documents")
     cvec = centroids.device_vectors(X.device)
     assign = _assign(Xu, cvec)
@@ -170,6 +195,20 @@ def build_centroid_index(docs, centroids: Centroids, set_off: torch.Tensor | Non
     doc_of = torch.repeat_interleave(torch.arange(N, device=X.device), sizes_dev)
     post_off, post_docs = _postings_from_assign(doc_of, assign, centroids.k, N)
     return CentroidIndex(n_docs=N, post_off=post_off, post_docs=post_docs)
+
+
+def build_centroid_index_native(X: torch.Tensor, centroids: Centroids, set_off: torch.Tensor,
+                                n_docs: int) -> CentroidIndex:
+    """K6 on the device (d = 128): exact argmax assignment (tcgen05 screen + float64
+    re-rank, np.argmax tie rule) and postings by stable radix counting sort."""
+    if X.dtype not in (torch.float16, torch.bfloat16, torch.float32, torch.float64):
+        X = X.to(torch.float64)
+    cvec = centroids.device_vectors(X.device)
+    lowp = centroids.device_lowp(X.device, bf16=X.dtype == torch.bfloat16)
+    assign = engine.assign_centroids(X, cvec, lowp)
+    post_off, post_docs = engine.postings_from_assign(assign, set_off.contiguous(), n_docs,
+                                                      centroids.k)
+    return CentroidIndex(n_docs=n_docs, post_off=post_off, post_docs=post_docs)
 
 
 def build_centroid_index_fast(X: torch.Tensor, centroids: Centroids, set_off: torch.Tensor,

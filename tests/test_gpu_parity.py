@@ -442,3 +442,35 @@ def test_prefilter_tensor_core_screen_exact(seed, dup):
     a, na = pf.filter_candidates_device(cindex, cents, Qb, 32, 4, 300, use_tc=True)
     b, nb = pf.filter_candidates_device(cindex, cents, Qb, 32, 4, 300, use_tc=False)
     assert torch.equal(na, nb) and torch.equal(a, b)
+
+
+# ------------------------------------------------ native centroid assignment (K6)
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32, torch.float64])
+def test_native_centroid_index_matches_oracle(dtype):
+    rng = np.random.default_rng(40)
+    k = 700
+    C = rng.standard_normal((k, 128))
+    C[1::2] = C[0::2] + 1e-4 * rng.standard_normal(C[0::2].shape)   # near-ties
+    C[9] = C[8]                                                       # exact tie -> lower id
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    docs = [rng.standard_normal((int(rng.integers(1, 40)), 128)) for _ in range(1500)]
+    docs[3][0] = C[8] * 3.0                                           # lands exactly on the tie
+    docs_t = [torch.from_numpy(x).to(dtype) for x in docs]
+    exact = [x.to(torch.float64).numpy() for x in docs_t]             # values the device sees
+    cents = d.Centroids(k=k, seed=0, vectors=C)
+    got = d.build_centroid_index(docs_t, cents)
+    want = O.build_centroid_index(exact, C)
+    off = got.post_off.cpu().numpy()
+    pd = got.post_docs.cpu().numpy()
+    for c in range(k):
+        np.testing.assert_array_equal(pd[off[c]:off[c + 1]], want[c], err_msg=f"centroid {c}")
+
+
+def test_counting_sort_large_sets_and_keys():
+    rng = np.random.default_rng(41)
+    n_sets, n = 70_000, 600_000
+    set_of = rng.integers(0, n_sets, size=n)
+    set_of[:20_000] = 17                                              # one huge set (> 4096)
+    rng.shuffle(set_of)
+    so, perm = engine.counting_sort(torch.from_numpy(set_of).to(DEV), n_sets)
+    np.testing.assert_array_equal(perm.cpu().numpy(), np.argsort(set_of, kind="stable"))
