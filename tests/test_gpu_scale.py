@@ -1,0 +1,139 @@
+"""Parity at BASELINE.json sizes (GPU).
+
+* cfg1 at full size: all 100,000 sets x 8 query sets, bit-exact vs the C oracle
+  (scores and top-100), plus top-k invariants for all 1,000 query sets.
+* cfg3 pipeline at full size (1M sets, 65,536 centroids): prefilter candidates
+  (oracle filter_candidates over the device postings), candidate scores and
+  top-100 for 4 query sets.
+* cfg4 shape (L=32, C=8 codes from records): 2 query sets x 300k sets exact,
+  and sampled (query set, set) pairs for 1,024 query sets.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2210_15748_b200 as d
+from oracle import c_oracle
+from oracle import dessert_oracle as O
+from paper_2210_15748_b200 import engine, prefilter, workloads
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda")
+
+
+def _records_to_codes_dev(recs: torch.Tensor, L: int, C: int) -> torch.Tensor:
+    """Inverse of the plane-record layout on the device (test helper), int32 (n, L)."""
+    W = (L + 31) // 32
+    r = recs.to(torch.int64) & 0xFFFFFFFF
+    t = torch.arange(L, device=recs.device)
+    codes = torch.zeros((recs.shape[0], L), dtype=torch.int64, device=recs.device)
+    for b in range(C):
+        words = r[:, b * W + t // 32]
+        codes |= ((words >> (t % 32)) & 1) << b
+    return codes.to(torch.int32)
+
+
+def test_cfg1_full_size_parity():
+    n_sets, L, C = 100_000, 64, 7
+    sizes = workloads.set_sizes(n_sets, 70, 20, seed=100)
+    off = workloads.offsets(sizes)
+    X, _ = workloads.gpu_mixture(int(off[-1]), 4096, 128, 0.05, seed=200, dtype=torch.float16,
+                                 device=DEV)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
+    idx = d.build_from_vectors(X, sizes, np.arange(n_sets), cfg)
+    Qv = workloads.gpu_queries(X, off, 1000, 32, seed=300)
+    del X
+    scores_t, ids_t = d.query_batch(idx, Qv, 100, return_tensors=True)
+    # oracle on 8 query sets over all sets, with the device's own codes
+    qc, _ = d.lsh.hash_device(idx.family, Qv[:8].reshape(-1, 128).contiguous(), want_records=False)
+    qcodes = qc.cpu().numpy().astype(np.int64).reshape(8, 32, L)
+    codes = idx.codes.cpu().numpy()
+    want = c_oracle.score(codes, off, qcodes, idx.lookup.table)
+    got, _ = d.score_matrix(idx, qcodes)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    S = scores_t.cpu().numpy()
+    I = ids_t.cpu().numpy()
+    for r in range(8):
+        top = O.rank_topk(want[r], np.arange(n_sets), 100)
+        assert [x for x, _ in top] == list(I[r]) and [v for _, v in top] == list(S[r])
+    # invariants for all 1000 rows: sorted by (score desc, id asc), unique ids
+    assert np.all((S[:, :-1] > S[:, 1:]) | ((S[:, :-1] == S[:, 1:]) & (I[:, :-1] < I[:, 1:])))
+    assert all(len(set(row)) == 100 for row in I)
+
+
+def test_cfg3_pipeline_full_size_parity():
+    n_sets, L, C, n_cent, probe, k_filter = 1_000_000, 32, 7, 65536, 4, 4096
+    sizes = workloads.set_sizes(n_sets, 70, 20, seed=500)
+    off = workloads.offsets(sizes)
+    X, cents = workloads.gpu_mixture(int(off[-1]), n_cent, 128, 0.05, seed=501,
+                                     dtype=torch.float16, device=DEV)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0,
+                        filter=d.FilterConfig(enabled=True, centroids=n_cent, probe=probe,
+                                              k_filter=k_filter))
+    idx = d.build_from_vectors(X, sizes, np.arange(n_sets), cfg)
+    cvec = cents.double()
+    cvec = cvec / cvec.norm(dim=1, keepdim=True)
+    centroids = prefilter.Centroids(k=n_cent, seed=0, vectors=cvec.cpu().numpy())
+    cindex = prefilter.build_centroid_index(X, centroids, set_off=idx.set_off, n_docs=n_sets)
+    idx.filter = (centroids, cindex)
+    Qv = workloads.gpu_queries(X, off, 4, 32, seed=502)
+    # spot-check the native postings: argmax of a vector sample, float64
+    samp = torch.arange(0, X.shape[0], 997, device=DEV)
+    Xs = X[samp].double()
+    am = torch.argmax(Xs @ cvec.T, dim=1).cpu().numpy()
+    po = cindex.post_off.cpu().numpy()
+    pdocs = cindex.post_docs.cpu().numpy()
+    doc_of = np.searchsorted(off, samp.cpu().numpy(), side="right") - 1
+    for c, doc in zip(am[:2000], doc_of[:2000]):
+        seg = pdocs[po[c]:po[c + 1]]
+        assert doc in seg
+    del X
+    postings = [pdocs[po[c]:po[c + 1]] for c in range(n_cent)]
+    res = d.query_batch(idx, Qv, 100)
+    qc, _ = d.lsh.hash_device(idx.family, Qv.reshape(-1, 128).contiguous(), want_records=False)
+    qcodes = qc.cpu().numpy().astype(np.int64).reshape(4, 32, L)
+    records = idx.records.cpu().numpy()
+    lut = idx.lookup.table
+    for r in range(4):
+        Qr = Qv[r].double().cpu().numpy()
+        cand = O.filter_candidates(postings, n_sets, centroids.vectors, Qr, probe, k_filter)
+        got_c, n_c = prefilter.filter_candidates_device(cindex, centroids, Qv[r].double(), 32,
+                                                        probe, k_filter)
+        np.testing.assert_array_equal(got_c[0, : int(n_c[0])].cpu().numpy(), cand)
+        vec_rows = np.concatenate([np.arange(off[s], off[s + 1]) for s in cand])
+        codes = workloads.records_to_codes(records[vec_rows], L, C)
+        sub_sizes = sizes[cand]
+        scores = c_oracle.score(codes, workloads.offsets(sub_sizes), qcodes[r:r + 1], lut)[0]
+        want = O.rank_topk(scores, cand, 100)
+        assert res[r] == want
+
+
+def test_cfg4_shape_sampled_parity():
+    n_sets, L, C = 300_000, 32, 8
+    sizes = workloads.set_sizes(n_sets, 70, 25, seed=400)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
+    recs, Qv = workloads.gpu_codes_only(sizes, cfg, n_centroids=262_144, n_qsets=1024, m_q=32,
+                                        seed=401, device=DEV)
+    idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
+    qc, qrecs = d.lsh.hash_device(idx.family, Qv.reshape(-1, 128).contiguous())
+    qcodes = qc.cpu().numpy().astype(np.int64).reshape(1024, 32, L)
+    off = workloads.offsets(sizes)
+    codes = _records_to_codes_dev(recs, L, C).cpu().numpy()      # int32, converted once
+    lut = idx.lookup.table
+    # 2 query sets exhaustively
+    got, _ = engine.score_all(idx.records, idx.set_off, qrecs, 32, L, C, idx.lut_dev)
+    want2 = c_oracle.score(codes, off, qcodes[:2], lut)
+    np.testing.assert_array_equal(got[:2].cpu().numpy(), want2)
+    # 4096 random (query set, set) pairs across all 1024 query sets
+    rng = np.random.default_rng(9)
+    qs = rng.integers(0, 1024, size=4096)
+    ss = rng.integers(0, n_sets, size=4096)
+    g = got.cpu().numpy()
+    w = c_oracle.score(codes, off, qcodes[qs], lut, sets=ss[:, None])[:, 0]   # one batched call
+    np.testing.assert_array_equal(g[qs, ss], w)
+    # top-1000 for 2 query sets
+    out_s, out_i, _ = engine.topk(got, 1000, ids=idx.doc_ids_dev)
+    for r in range(2):
+        top = O.rank_topk(want2[r], np.arange(n_sets), 1000)
+        assert [x for x, _ in top] == list(out_i[r].cpu().numpy())
