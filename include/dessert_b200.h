@@ -124,6 +124,25 @@ int dsrt_score_candidates(const uint32_t *records, const int64_t *set_off, int64
                           const double *lut, double *scores, uint16_t *maxcounts, void *stream);
 
 /*
+ * K3g -- general aggregation (index.py:170-216 _sim_table_for/_score_one for
+ * every Scorer): inner_kind 0 = sigma max, 1 = avg-phi; weights (m_q float64,
+ * NULL = all ones, scoring.py:93-97 Scorer.weights).  table = (L+1) float64:
+ * the lookup table for max, phi(lookup table) for avg-phi (host-computed).
+ *   max:     per_query[q] = table[max_j c_qj]
+ *   avg-phi: per_query[q] = reduceat-sum(table[c_qj] : c_qj > 0, j ascending) / m
+ *   score    = mean(w * per_query)   (numpy pairwise order throughout)
+ * Targets as dsrt_score_candidates (cand NULL: identity; n_cand NULL: all
+ * cand_ld; entries e >= n_cand[q] are written as -1).  m_cap bounds the
+ * target set size for avg-phi (its per-lane count scratch), L <= 128, C <= 16.
+ */
+size_t dsrt_score_agg_workspace(int64_t n_qsets, int64_t cand_ld, int m_q, int64_t m_cap);
+int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                   const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                   const uint32_t *qrecords, int64_t n_qsets, int m_q, int L, int C,
+                   int inner_kind, const double *table, const double *weights, int64_t m_cap,
+                   double *scores, void *workspace, size_t ws_bytes, void *stream);
+
+/*
  * K4 -- replaces heapq.nsmallest(top_k, ..., key=(-score, doc_id)) (index.py:314-319).
  * Row r: scores[r * ld + i], i < n (n_valid[r] if given).  ids: doc id of
  * element i -- shared (ids[i]) if ids_ld == 0, else ids[r * ids_ld + i]; NULL

@@ -166,10 +166,17 @@ def collision_keys(table: TinyTable, query_codes) -> np.ndarray:
     return np.repeat(cell_keys, lens) + members
 
 
-def score_port(table: TinyTable, query_codes, lut: np.ndarray) -> float:
-    """sigma=max, default weights: index.py:183-216 (_score_one), ported."""
+def score_port(table: TinyTable, query_codes, lut: np.ndarray, kind: str = "max",
+               weights=None) -> float:
+    """index.py:183-216 (_score_one), ported.
+
+    ``lut`` is the aggregand table (_sim_table_for, index.py:170-180): the
+    lookup table for kind "max", phi(lookup table) for "avg-phi".  weights
+    None means all ones (index.py:219-221).
+    """
     keys = collision_keys(table, query_codes)
     m_q = np.asarray(query_codes).shape[0]
+    w = np.ones(m_q) if weights is None else np.asarray(weights, dtype=np.float64)
     per_query = np.zeros(m_q)
     if keys.size:
         keys.sort()
@@ -179,8 +186,11 @@ def score_port(table: TinyTable, query_codes, lut: np.ndarray) -> float:
         row_bounds = np.searchsorted(rows, np.arange(m_q + 1))
         occupied = row_bounds[:-1] < row_bounds[1:]
         seg_starts = row_bounds[:-1][occupied]
-        per_query[occupied] = lut[np.maximum.reduceat(counts, seg_starts)]
-    return float(np.mean(np.ones(m_q) * per_query))
+        if kind == "max":
+            per_query[occupied] = lut[np.maximum.reduceat(counts, seg_starts)]
+        else:
+            per_query[occupied] = np.add.reduceat(lut[counts], seg_starts) / table.m
+    return float(np.mean(w * per_query))
 
 
 # --------------------------------------------------------------------------
@@ -242,6 +252,50 @@ def score_sets_dense(query_codes, codes, set_off, lut, sets=None) -> np.ndarray:
     sets = range(n) if sets is None else sets
     return np.array([score_dense(query_codes, codes[set_off[i]:set_off[i + 1]], lut)
                      for i in sets], dtype=np.float64)
+
+
+def reduceat_sum(vals) -> float:
+    """One np.add.reduceat segment: first element + pairwise(rest).
+
+    numpy's reduceat seeds the output with the segment's first element and
+    runs the add reduce loop (pairwise_sum_DOUBLE) over the remainder;
+    tests/test_oracle.py pins this against np.add.reduceat.
+    """
+    v = [float(x) for x in vals]
+    if not v:
+        raise ValueError("empty segment")
+    return v[0] + pairwise_sum(v[1:])
+
+
+def score_dense_agg(query_codes, set_codes, table: np.ndarray, kind: str = "max",
+                    weights=None) -> float:
+    """Dense restatement of _score_one for any Scorer (what K3g computes).
+
+    per_query[q] = table[max_j c_qj]                                 (max)
+                 = reduceat_sum(table[c_qj] : c_qj > 0, j asc) / m   (avg-phi)
+    score = pairwise_sum(w_q * per_query[q]) / m_q
+    """
+    q = np.asarray(query_codes)
+    x = np.asarray(set_codes)
+    m_q, m = q.shape[0], x.shape[0]
+    w = np.ones(m_q) if weights is None else np.asarray(weights, dtype=np.float64)
+    eq = (q[:, None, :] == x[None, :, :]).sum(axis=2) if m else np.zeros((m_q, 0), np.int64)
+    pq = np.zeros(m_q)
+    for i in range(m_q):
+        if kind == "max":
+            pq[i] = table[eq[i].max()] if m else 0.0
+        else:
+            nz = eq[i][eq[i] > 0]
+            pq[i] = reduceat_sum(table[nz]) / m if nz.size else 0.0
+    return pairwise_sum(w * pq) / m_q
+
+
+def score_sets_dense_agg(query_codes, codes, set_off, table, kind="max", weights=None,
+                         sets=None) -> np.ndarray:
+    n = len(set_off) - 1
+    sets = range(n) if sets is None else sets
+    return np.array([score_dense_agg(query_codes, codes[set_off[i]:set_off[i + 1]], table, kind,
+                                     weights) for i in sets], dtype=np.float64)
 
 
 # --------------------------------------------------------------------------

@@ -1,0 +1,252 @@
+// K3g -- general inner/outer aggregation: sigma = max
+// or avg-phi, optional per-query-vector weights.  Follows _score_one
+// (index.py:183-216) with _sim_table_for (index.py:170-180):
+//
+//   max:     per_query[q] = table[max_j c_qj]
+//   avg-phi: per_query[q] = add.reduceat(table[c_qj] for c_qj > 0, j ascending) / m
+//            (numpy reduceat segment = first element + pairwise(rest))
+//   score  = mean(w * per_query) = (0.0 + pairwise(w_q * per_query[q])) / m_q
+//
+// with table = lut (max) or phi(lut) (avg-phi), host-computed bytes.  The
+// sigma = max, unit-weight north-star path stays on the register-blocked
+// kernels in score_kernels.cuh; this kernel is the general path.
+//
+// Work item = (query set, target).  One warp per item, persistent grid; lane
+// = query vector (32-wide slices of m_q).  Target records are warp-uniform
+// (broadcast loads); the avg-phi counts c_qj > 0 are compacted per lane into
+// warp scratch [k][lane] (uint8, c <= L <= 255) and summed in the reference's
+// order afterwards.
+#include "common.cuh"
+
+namespace dsrt {
+
+constexpr int kAggWarps = 8;
+constexpr int kAggMaxC = 16;
+
+// numpy pairwise_sum_DOUBLE over v(start..start+n) where v(k) = table[s[k * 32]]
+__device__ double pw_counts(const uint8_t *s, int n, const double *__restrict__ table) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r = __dadd_rn(r, __ldg(table + s[i * 32]));
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __ldg(table + s[j * 32]);
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], __ldg(table + s[(i + j) * 32]));
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, __ldg(table + s[i * 32]));
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pw_counts(s, n2, table), pw_counts(s + n2 * 32, n - n2, table));
+}
+
+// numpy pairwise_sum_DOUBLE over a contiguous double array
+__device__ double pw_doubles(const double *a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int i;
+        for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pw_doubles(a, n2), pw_doubles(a + n2, n - n2));
+}
+
+struct AggArgs {
+    const uint32_t *records;
+    const int64_t *set_off;
+    int64_t n_sets;
+    const int64_t *cand;    // NULL: identity
+    const int32_t *n_cand;  // NULL: all cand_ld
+    int64_t cand_ld;
+    const uint32_t *qrecs;
+    int64_t n_qsets;
+    int m_q, L, C, R;
+    int kind;               // 0 max, 1 avg-phi
+    const double *table;    // (L+1)
+    const double *weights;  // (m_q) or NULL
+    double *scores;         // (n_qsets, cand_ld)
+    uint8_t *scratch;       // per warp: 32 * m_cap count bytes, then m_q doubles
+    int64_t m_cap;
+    size_t warp_bytes;
+    uint32_t *status;       // bit 0: target set larger than m_cap
+};
+
+template <int W>
+__global__ void __launch_bounds__(kAggWarps * 32)
+    score_agg_kernel(const AggArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * static_cast<int64_t>(kAggWarps) + (threadIdx.x >> 5);
+    const int64_t n_warps = static_cast<int64_t>(gridDim.x) * kAggWarps;
+    uint8_t *cnt = a.scratch + gw * a.warp_bytes;
+    double *pq = reinterpret_cast<double *>(cnt + 32 * a.m_cap);
+    const int64_t items = a.n_qsets * a.cand_ld;
+    const uint32_t tail = (a.L % 32) ? ((1u << (a.L % 32)) - 1u) : 0xffffffffu;
+    for (int64_t it = gw; it < items; it += n_warps) {
+        const int64_t qs = it / a.cand_ld, e = it - qs * a.cand_ld;
+        double *out = a.scores + qs * a.cand_ld + e;
+        if (a.n_cand != nullptr && e >= tmin<int64_t>(a.n_cand[qs], a.cand_ld)) {
+            if (lane == 0) *out = -1.0;
+            continue;
+        }
+        const int64_t s = a.cand ? a.cand[qs * a.cand_ld + e] : e;
+        const bool valid = s >= 0 && s < a.n_sets;  // invalid index: empty set, as score_cand_kernel
+        const int64_t v0 = valid ? a.set_off[s] : 0, m = valid ? a.set_off[s + 1] - v0 : 0;
+        if (a.kind == 1 && m > a.m_cap) {
+            if (lane == 0) {
+                atomicOr(a.status, 1u);
+                *out = -1.0;
+            }
+            continue;
+        }
+        const uint32_t *xr = a.records + v0 * a.R;
+        for (int q0 = 0; q0 < a.m_q; q0 += 32) {
+            const int q = q0 + lane;
+            const bool act = q < a.m_q;
+            uint32_t qw[kAggMaxC][W];
+            const uint32_t *qr = a.qrecs + (qs * a.m_q + (act ? q : 0)) * static_cast<int64_t>(a.R);
+#pragma unroll
+            for (int b = 0; b < kAggMaxC; ++b)
+#pragma unroll
+                for (int w = 0; w < W; ++w) qw[b][w] = (b < a.C) ? __ldg(qr + b * W + w) : 0u;
+            int cmax = 0, nz = 0;
+            for (int64_t j = 0; j < m; ++j) {
+                const uint32_t *x = xr + j * a.R;
+                int mm = 0;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int b = 0; b < kAggMaxC; ++b)
+                        if (b < a.C) acc |= qw[b][w] ^ __ldg(x + b * W + w);
+                    if (w == W - 1) acc &= tail;
+                    mm += __popc(acc);
+                }
+                const int c = a.L - mm;
+                cmax = tmax(cmax, c);
+                if (a.kind == 1 && c > 0 && act) {
+                    cnt[nz * 32 + lane] = static_cast<uint8_t>(c);
+                    ++nz;
+                }
+            }
+            __syncwarp();
+            if (act) {
+                double v;
+                if (a.kind == 0) {
+                    v = __ldg(a.table + cmax);
+                } else if (nz == 0) {
+                    v = 0.0;
+                } else {  // reduceat: first + pairwise(rest), then / m
+                    const double first = __ldg(a.table + cnt[lane]);
+                    v = __ddiv_rn(__dadd_rn(first, pw_counts(cnt + 32 + lane, nz - 1, a.table)),
+                                  static_cast<double>(m));
+                }
+                pq[q] = a.weights ? __dmul_rn(__ldg(a.weights + q), v) : v;
+            }
+            __syncwarp();
+        }
+        if (lane == 0)
+            *out = __ddiv_rn(__dadd_rn(0.0, pw_doubles(pq, a.m_q)), static_cast<double>(a.m_q));
+        __syncwarp();
+    }
+}
+
+static int64_t agg_warps(int64_t items) {
+    return tmax<int64_t>(1, tmin<int64_t>(items, 148LL * 4 * kAggWarps));
+}
+
+static size_t agg_warp_bytes(int m_q, int64_t m_cap) {
+    return (static_cast<size_t>(32 * m_cap) + 15) / 16 * 16 + static_cast<size_t>(m_q) * 8;
+}
+
+}  // namespace dsrt
+
+using namespace dsrt;
+
+extern "C" size_t dsrt_score_agg_workspace(int64_t n_qsets, int64_t cand_ld, int m_q, int64_t m_cap) {
+    if (n_qsets < 0 || cand_ld < 0 || m_q < 1 || m_cap < 0) return 0;
+    const int64_t warps = (agg_warps(n_qsets * cand_ld) + kAggWarps - 1) / kAggWarps * kAggWarps;
+    return static_cast<size_t>(warps) * agg_warp_bytes(m_q, m_cap) + 256;
+}
+
+extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                              const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                              const uint32_t *qrecords, int64_t n_qsets, int m_q, int L, int C,
+                              int inner_kind, const double *table, const double *weights,
+                              int64_t m_cap, double *scores, void *workspace, size_t ws_bytes,
+                              void *stream) {
+    DSRT_REQUIRE(m_q >= 1, DSRT_EINVAL, "empty query: need at least one query vector");
+    DSRT_REQUIRE(L >= 1 && L <= 255 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", L, C);
+    DSRT_REQUIRE(C <= kAggMaxC, DSRT_EUNSUPPORTED, "invalid parameter: C=%d > %d", C, kAggMaxC);
+    DSRT_REQUIRE(inner_kind == 0 || inner_kind == 1, DSRT_EINVAL,
+                 "invalid parameter: inner_kind=%d (0 max, 1 avg-phi)", inner_kind);
+    DSRT_REQUIRE(n_qsets >= 0 && cand_ld >= 0 && n_sets >= 0 && m_cap >= 0, DSRT_EINVAL,
+                 "invalid parameter: negative size");
+    DSRT_REQUIRE(cand != nullptr || cand_ld <= n_sets, DSRT_EINVAL,
+                 "invalid parameter: cand_ld > n_sets without a candidate list");
+    const int W = plane_words(L);
+    DSRT_REQUIRE(W <= 4, DSRT_EUNSUPPORTED, "invalid parameter: L=%d > 128 for the aggregation kernel", L);
+    const int64_t items = n_qsets * cand_ld;
+    if (items == 0) return DSRT_OK;
+    DSRT_REQUIRE(ws_bytes >= dsrt_score_agg_workspace(n_qsets, cand_ld, m_q, m_cap), DSRT_EINVAL,
+                 "invalid parameter: aggregation workspace too small");
+    cudaStream_t st = as_stream(stream);
+    AggArgs a{};
+    a.records = records;
+    a.set_off = set_off;
+    a.n_sets = n_sets;
+    a.cand = cand;
+    a.n_cand = n_cand;
+    a.cand_ld = cand_ld;
+    a.qrecs = qrecords;
+    a.n_qsets = n_qsets;
+    a.m_q = m_q;
+    a.L = L;
+    a.C = C;
+    a.R = record_words(L, C);
+    a.kind = inner_kind;
+    a.table = table;
+    a.weights = weights;
+    a.scores = scores;
+    a.m_cap = m_cap;
+    a.warp_bytes = agg_warp_bytes(m_q, m_cap);
+    uint8_t *w = static_cast<uint8_t *>(workspace);
+    a.status = reinterpret_cast<uint32_t *>(w);
+    a.scratch = w + 256;
+    DSRT_CUDA(cudaMemsetAsync(a.status, 0, 4, st));
+    const unsigned blocks = static_cast<unsigned>((agg_warps(items) + kAggWarps - 1) / kAggWarps);
+    switch (W) {
+        case 1: score_agg_kernel<1><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
+        case 2: score_agg_kernel<2><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
+        case 3: score_agg_kernel<3><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
+        default: score_agg_kernel<4><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
+    }
+    DSRT_LAUNCH_CHECK();
+    uint32_t h = 0;
+    DSRT_CUDA(cudaMemcpyAsync(&h, a.status, 4, cudaMemcpyDeviceToHost, st));
+    DSRT_CUDA(cudaStreamSynchronize(st));
+    DSRT_REQUIRE((h & 1u) == 0, DSRT_EINVAL, "invalid parameter: set larger than m_cap=%lld",
+                 static_cast<long long>(m_cap));
+    return DSRT_OK;
+}

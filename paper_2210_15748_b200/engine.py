@@ -172,6 +172,32 @@ def score_candidates(records, set_off, qrecords, m_q: int, L: int, C: int, lut, 
     return scores, mc
 
 
+def score_agg(records, set_off, qrecords, m_q: int, L: int, C: int, table, inner_kind: int,
+              weights=None, m_cap: int = 0, cand=None, n_cand=None, cand_ld=None, n_qsets=None):
+    """General aggregation scores (sigma max / avg-phi, optional weights): (n_qsets, cand_ld)."""
+    _need(table, torch.float64, "table")
+    n_sets = set_off.shape[0] - 1
+    n_q = n_qsets if n_qsets is not None else (qrecords.shape[0] // m_q)
+    if cand is not None:
+        _need(cand, torch.int64, "cand")
+        cand_ld = cand.shape[-1]
+    elif cand_ld is None:
+        cand_ld = n_sets
+    if n_cand is not None:
+        _need(n_cand, torch.int32, "n_cand")
+    if weights is not None:
+        _need(weights, torch.float64, "weights")
+        if weights.numel() != m_q:
+            raise ValueError(f"length mismatch: {weights.numel()} weights for {m_q} query vectors")
+    scores = torch.empty((n_q, cand_ld), dtype=torch.float64, device=records.device)
+    ws_bytes = _lib.lib().dsrt_score_agg_workspace(n_q, cand_ld, m_q, m_cap)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=records.device)
+    _lib.call("dsrt_score_agg", _ptr(records), _ptr(set_off), n_sets, _ptr(cand), _ptr(n_cand),
+              cand_ld, _ptr(qrecords), n_q, m_q, L, C, inner_kind, _ptr(table), _ptr(weights),
+              m_cap, _ptr(scores), _ptr(ws), ws_bytes, _stream())
+    return scores
+
+
 # ------------------------------------------------------------------- K4
 def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None):
     """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D)."""

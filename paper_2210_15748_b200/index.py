@@ -28,7 +28,8 @@ import torch
 from . import engine
 from .lsh import (SimLookup, SrpFamily, build_sim_lookup, hash_device, sample_srp_family,
                   to_device_matrix)
-from .scoring import Scorer, default_scorer, max_aggregation, require_device_scorer
+from . import scoring
+from .scoring import Scorer, avg_phi_aggregation, default_scorer, max_aggregation
 from .sketch import SketchView
 
 RankedResults = list[tuple[int, float]]
@@ -66,11 +67,8 @@ class IndexConfig:
         return 1 << self.C
 
     def scorer(self) -> Scorer:
-        if self.inner_kind == "max":
-            return Scorer(inner=max_aggregation(), weights=None)
-        from .scoring import InnerAggregation
-
-        return Scorer(inner=InnerAggregation(kind="avg", alpha=1.0, beta=1.0, phi=self.phi))
+        inner = max_aggregation() if self.inner_kind == "max" else avg_phi_aggregation(self.phi)
+        return Scorer(inner=inner, weights=None)
 
 
 PROFILES: dict[str, dict] = {  # index.py:66-71 (paper App. B)
@@ -342,9 +340,76 @@ def _candidates(index: DessertIndex, Qdev: torch.Tensor, m_q: int, probe, k_filt
                                     cfg.k_filter if k_filter is None else k_filter)
 
 
+@dataclass
+class ScorePlan:
+    """A non-default Scorer resolved for the device (K3g, dsrt_score_agg)."""
+
+    kind: int                    # 0 max, 1 avg-phi
+    table: torch.Tensor          # (L+1) float64: lut or phi(lut)
+    weights: torch.Tensor | None  # (m_q) float64 or None (all ones)
+    m_cap: int                   # largest set size (avg-phi count scratch)
+
+
+def score_plan(index: DessertIndex, scorer: Scorer | None, m_q: int) -> ScorePlan | None:
+    """Resolve ``scorer or index.config.scorer()`` (index.py:285-287); None = fast path."""
+    scorer = scorer or index.config.scorer()
+    weights = scoring.resolve_weights(scorer, m_q)
+    kind = scoring.inner_kind_code(scorer)
+    if kind == 0 and weights is None:
+        return None
+    table = scoring.table_for(index.lookup.table, scorer)
+    return ScorePlan(
+        kind=kind,
+        table=torch.from_numpy(np.ascontiguousarray(table, dtype=np.float64)).to(index.device),
+        weights=(None if weights is None else
+                 torch.from_numpy(np.ascontiguousarray(weights)).to(index.device)),
+        m_cap=index.m_max if kind == 1 else 0)
+
+
+def _score_plan_sets(index: DessertIndex, qrecs, m_q: int, plan: ScorePlan, cand=None,
+                     n_cand=None, n_q=None, cand_ld=None):
+    return engine.score_agg(index.records, index.set_off, qrecs, m_q, index.config.L,
+                            index.config.C, plan.table, plan.kind, weights=plan.weights,
+                            m_cap=plan.m_cap, cand=cand, n_cand=n_cand, cand_ld=cand_ld,
+                            n_qsets=n_q)
+
+
+def _rank_records_plan(index: DessertIndex, qrecs, m_q: int, top_k: int, plan: ScorePlan,
+                       cand, n_cand):
+    n_q = qrecs.shape[0] // m_q
+    N = index.n_docs
+    if cand is not None:
+        scores = _score_plan_sets(index, qrecs, m_q, plan, cand=cand, n_cand=n_cand)
+        ids = index.doc_ids_dev[cand.clamp(min=0)]
+        out_s, out_i, _ = _rank(scores, top_k, ids, n_valid=n_cand)
+        return out_s, out_i
+    chunk = max(1, min(N, SCORE_BUFFER_BYTES // (8 * n_q)))
+    if chunk >= N:
+        scores = _score_plan_sets(index, qrecs, m_q, plan, n_q=n_q, cand_ld=N)
+        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev)
+        return out_s, out_i
+    parts_s, parts_i = [], []
+    for s0 in range(0, N, chunk):
+        s1 = min(N, s0 + chunk)
+        sets = torch.arange(s0, s1, device=index.device).expand(n_q, s1 - s0).contiguous()
+        scores = _score_plan_sets(index, qrecs, m_q, plan, cand=sets)
+        ps, pi, _ = _rank(scores, top_k, index.doc_ids_dev[s0:s1])
+        parts_s.append(ps)
+        parts_i.append(pi)
+    out_s, out_i, _ = _rank(torch.cat(parts_s, dim=1).contiguous(), top_k,
+                            torch.cat(parts_i, dim=1).contiguous())
+    return out_s, out_i
+
+
 def rank_records(index: DessertIndex, qrecs: torch.Tensor, m_q: int, top_k: int,
-                 cand=None, n_cand=None):
-    """Score query-set records (n_qsets*m_q, R) and rank; returns (scores, ids) (n_qsets, k)."""
+                 cand=None, n_cand=None, plan: ScorePlan | None = None):
+    """Score query-set records (n_qsets*m_q, R) and rank; returns (scores, ids) (n_qsets, k).
+
+    ``plan`` (from ``score_plan``) selects the general aggregation kernel for
+    a non-default Scorer; None runs the sigma=max / unit-weight kernels.
+    """
+    if plan is not None:
+        return _rank_records_plan(index, qrecs, m_q, top_k, plan, cand, n_cand)
     n_q = qrecs.shape[0] // m_q
     L, C = index.config.L, index.config.C
     N = index.n_docs
@@ -398,16 +463,16 @@ def query(index: DessertIndex, Q, top_k: int, probe: int | None = None,
     Qa = Q if isinstance(Q, torch.Tensor) else np.asarray(Q, dtype=np.float64)
     if Qa.ndim != 2 or Qa.shape[0] == 0:
         raise ValueError("empty query: need at least one query vector")
-    require_device_scorer(scorer)
     Qdev = to_device_matrix(Qa, index.config.d, index.device)
     _, qrecs = hash_device(index.family, Qdev, want_codes=False)
     m_q = Qdev.shape[0]
+    plan = score_plan(index, scorer, m_q)
     cand = n_cand = None
     if index.filter is not None:
         cand, n_cand = _candidates(index, Qdev, m_q, probe, k_filter)
         if int(n_cand[0].item()) == 0:
             return []
-    out_s, out_i = rank_records(index, qrecs, m_q, top_k, cand, n_cand)
+    out_s, out_i = rank_records(index, qrecs, m_q, top_k, cand, n_cand, plan)
     return _results(out_s, out_i)[0]
 
 
@@ -421,7 +486,6 @@ def query_batch(index: DessertIndex, Qs, top_k: int, probe: int | None = None,
     """
     if top_k < 1:
         raise ValueError(f"invalid parameter: top_k must be >= 1, got {top_k}")
-    require_device_scorer(scorer)
     if isinstance(Qs, torch.Tensor):
         t = Qs
     else:
@@ -429,18 +493,20 @@ def query_batch(index: DessertIndex, Qs, top_k: int, probe: int | None = None,
     if t.dim() != 3 or t.shape[1] == 0:
         raise ValueError("empty query: need at least one query vector")
     n_q, m_q, d = t.shape
+    plan = score_plan(index, scorer, m_q)
     Qdev = to_device_matrix(t.reshape(n_q * m_q, d), index.config.d, index.device)
     _, qrecs = hash_device(index.family, Qdev, want_codes=False)
     cand = n_cand = None
     if index.filter is not None:
         cand, n_cand = _candidates(index, Qdev, m_q, probe, k_filter)
-    out_s, out_i = rank_records(index, qrecs, m_q, top_k, cand, n_cand)
+    out_s, out_i = rank_records(index, qrecs, m_q, top_k, cand, n_cand, plan)
     if return_tensors:
         return out_s, out_i
     return _results(out_s, out_i)
 
 
-def query_codes_batch(index: DessertIndex, qcodes, top_k: int, return_tensors=False):
+def query_codes_batch(index: DessertIndex, qcodes, top_k: int, return_tensors=False,
+                      scorer: Scorer | None = None):
     """Rank from precomputed query codes (n_qsets, m_q, L) -- the parity hook
     ("both sides given the same hash codes")."""
     t = qcodes if isinstance(qcodes, torch.Tensor) else torch.from_numpy(np.asarray(qcodes))
@@ -449,7 +515,7 @@ def query_codes_batch(index: DessertIndex, qcodes, top_k: int, return_tensors=Fa
         raise ValueError(f"expected (m_q, {index.config.L}) code matrix, got shape {tuple(t.shape)}")
     codes = t.reshape(n_q * m_q, L).to(index.device).to(torch.int32).contiguous()
     qrecs, bad = engine.codes_to_records(codes, L, index.config.C)
-    out_s, out_i = rank_records(index, qrecs, m_q, top_k)
+    out_s, out_i = rank_records(index, qrecs, m_q, top_k, plan=score_plan(index, scorer, m_q))
     if return_tensors:
         return out_s, out_i
     return _results(out_s, out_i)
@@ -462,23 +528,37 @@ def score_candidate(index: DessertIndex, i: int, query_codes, scorer: Scorer | N
     qc = np.asarray(query_codes)
     if qc.ndim != 2 or qc.shape[1] != index.config.L:
         raise ValueError(f"expected (m_q, {index.config.L}) code matrix, got shape {qc.shape}")
-    require_device_scorer(scorer)
     if qc.shape[0] == 0:
+        scoring.resolve_weights(scorer or index.config.scorer(), 0)
         return float("nan")  # np.mean of an empty array (reference warns and returns nan)
+    plan = score_plan(index, scorer, qc.shape[0])
     codes = torch.from_numpy(qc.astype(np.int32)).to(index.device)
     qrecs, _ = engine.codes_to_records(codes, index.config.L, index.config.C, check=False)
     cand = torch.tensor([[i]], dtype=torch.int64, device=index.device)
+    if plan is not None:
+        return float(_score_plan_sets(index, qrecs, qc.shape[0], plan, cand=cand)[0, 0].item())
     scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, qc.shape[0],
                                         index.config.L, index.config.C, index.lut_dev, cand=cand)
     return float(scores[0, 0].item())
 
 
-def score_matrix(index: DessertIndex, qcodes, sets=None, want_counts=False):
-    """Scores (and optional integer max counts c_q) of query code sets vs sets (parity API)."""
+def score_matrix(index: DessertIndex, qcodes, sets=None, want_counts=False,
+                 scorer: Scorer | None = None):
+    """Scores (and optional integer max counts c_q) of query code sets vs sets (parity API).
+
+    With a non-default ``scorer`` returns (scores, None) from the general kernel."""
     t = qcodes if isinstance(qcodes, torch.Tensor) else torch.from_numpy(np.asarray(qcodes))
     n_q, m_q, L = t.shape
     codes = t.reshape(n_q * m_q, L).to(index.device).to(torch.int32).contiguous()
     qrecs, _ = engine.codes_to_records(codes, L, index.config.C, check=False)
+    plan = score_plan(index, scorer, m_q)
+    if plan is not None:
+        if want_counts:
+            raise ValueError("invalid parameter: want_counts needs the default scorer")
+        if sets is None:
+            return _score_plan_sets(index, qrecs, m_q, plan, n_q=n_q, cand_ld=index.n_docs), None
+        cand = sets if isinstance(sets, torch.Tensor) else torch.from_numpy(np.asarray(sets, np.int64))
+        return _score_plan_sets(index, qrecs, m_q, plan, cand=cand.to(index.device).contiguous()), None
     if sets is None:
         if n_q >= 8:
             return engine.score_all(index.records, index.set_off, qrecs, m_q, L, index.config.C,
@@ -496,4 +576,4 @@ __all__ = ["FilterConfig", "IndexConfig", "PROFILES", "apply_profile", "DessertI
            "RankedResults", "build_index", "build_from_vectors", "build_from_codes",
            "build_from_records", "add_sets",
            "query", "query_batch", "query_codes_batch", "score_candidate", "score_matrix",
-           "default_scorer"]
+           "default_scorer", "ScorePlan", "score_plan"]

@@ -48,6 +48,28 @@ def golden_e2e():
     return load_golden("end_to_end.npz")
 
 
+@pytest.fixture(scope="session")
+def golden_agg():
+    return load_golden("agg.npz")
+
+
+def agg_case(g, n):
+    L, C, m_q = (int(x) for x in g[f"a{n}_shape"])
+    sizes = g[f"a{n}_sizes"].astype(np.int64)
+    return dict(L=L, C=C, m_q=m_q, sizes=sizes,
+                off=np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64),
+                codes=g[f"a{n}_codes"], qcodes=g[f"a{n}_qcodes"], weights=g[f"a{n}_weights"],
+                lut=g[f"a{n}_lut"])
+
+
+def agg_scorer(name, weights):
+    """Scorer for a golden scorer name: max_w, <phi>, <phi>_w."""
+    import paper_2210_15748_b200 as d
+    base, _, wt = name.rpartition("_") if name.endswith("_w") else (name, "", "")
+    inner = d.max_aggregation() if base == "max" else d.avg_phi_aggregation(base)
+    return d.Scorer(inner=inner, weights=weights if wt == "w" else None)
+
+
 def small_case(g, n):
     L, C, m_q = (int(x) for x in g[f"s{n}_shape"])
     sizes = g[f"s{n}_sizes"].astype(np.int64)

@@ -196,13 +196,93 @@ def make_prefilter():
     np.savez_compressed(os.path.join(HERE, "prefilter.npz"), **out)
 
 
+AGG_SHAPES = [  # (L, C, m_q, n_sets, m_max)
+    (32, 6, 32, 20, 120), (64, 7, 40, 16, 300), (16, 3, 5, 20, 200), (8, 2, 70, 12, 260),
+    (128, 4, 9, 10, 40), (33, 9, 33, 12, 60),
+]
+
+
+def _agg_scorers(m_q, rng):
+    """(name, Scorer) pairs covering every inner kind, with and without weights."""
+    from dessert.scoring import Scorer, avg_phi_aggregation, max_aggregation
+    w = rng.uniform(0.0, 1.0, size=m_q)
+    w[rng.random(m_q) < 0.2] = 0.0
+    out = [("max_w", Scorer(inner=max_aggregation(), weights=w))]
+    for phi in ("identity", "exp-minus-one", "debiased-sigmoid"):
+        out.append((f"{phi}", Scorer(inner=avg_phi_aggregation(phi), weights=None)))
+        out.append((f"{phi}_w", Scorer(inner=avg_phi_aggregation(phi), weights=w)))
+    return out, w
+
+
+def make_agg():
+    """Scores for every Scorer kind (index.py:183-216) on code-level cases, plus
+    query() end to end with avg-phi configs -- row f3."""
+    rng = np.random.default_rng(4321)
+    out = {}
+    for n, (L, C, m_q, n_sets, m_max) in enumerate(AGG_SHAPES):
+        r = 1 << C
+        sizes = rng.integers(1, m_max + 1, size=n_sets)
+        sizes[0] = m_max  # long rows: > 128 non-zero counts for the recursive pairwise split
+        hot = rng.integers(0, r, size=(L,))
+        codes = rng.integers(0, r, size=(int(sizes.sum()), L))
+        mask = rng.random(codes.shape) < 0.6
+        codes[mask] = np.broadcast_to(hot, codes.shape)[mask]
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        tables = [dessert.build_tiny_table(codes[off[i]:off[i + 1]], L, r) for i in range(n_sets)]
+        fam = dessert.sample_srp_family(4, C, L, 0)
+        index = ref_index.DessertIndex(config=no_filter(d=4, C=C, L=L), family=fam,
+                                       lookup=dessert.build_sim_lookup(C, L), sketches=tables,
+                                       doc_ids=np.arange(n_sets, dtype=np.uint64),
+                                       sizes=sizes.astype(np.int64), filter=None)
+        qcodes = rng.integers(0, r, size=(2, m_q, L))
+        qm = rng.random(qcodes.shape) < 0.6
+        qcodes[qm] = np.broadcast_to(hot, qcodes.shape)[qm]
+        scorers, w = _agg_scorers(m_q, rng)
+        out[f"a{n}_shape"] = np.array([L, C, m_q])
+        out[f"a{n}_sizes"] = sizes
+        out[f"a{n}_codes"] = codes.astype(np.int32)
+        out[f"a{n}_qcodes"] = qcodes.astype(np.int32)
+        out[f"a{n}_weights"] = w
+        out[f"a{n}_lut"] = index.lookup.table
+        for name, sc in scorers:
+            weights = ref_index._resolve_weights(sc, m_q)
+            out[f"a{n}_{name}"] = np.stack([
+                np.array(ref_index._score_chunk(index, np.arange(n_sets), qc, sc, weights))
+                for qc in qcodes])
+    out["n_shapes"] = np.array(len(AGG_SHAPES))
+    out["scorers"] = np.array([name for name, _ in _agg_scorers(4, rng)[0]])
+    # end to end: vectors -> build_index(avg-phi config) -> query
+    cases = [(16, 4, 32, 3, 30, 16, 10, "identity"), (32, 6, 32, 5, 40, 20, 8, "exp-minus-one"),
+             (24, 5, 64, 7, 25, 33, 6, "debiased-sigmoid")]
+    for n, (d, C, L, seed, n_sets, m_q, top_k, phi) in enumerate(cases):
+        sizes = rng.integers(1, 30, size=n_sets)
+        X = rng.standard_normal((int(sizes.sum()), d))
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        ids = rng.permutation(500)[:n_sets]
+        docs = [(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(n_sets)]
+        cfg = dessert.IndexConfig(d=d, C=C, L=L, seed=seed, inner_kind="avg-phi", phi=phi,
+                                  filter=dessert.FilterConfig(enabled=False))
+        index = dessert.build_index(docs, cfg)
+        Q = rng.standard_normal((2, m_q, d))
+        res = [dessert.query(index, q, top_k=top_k) for q in Q]
+        out[f"e{n}_shape"] = np.array([d, C, L, seed, top_k])
+        out[f"e{n}_phi"] = np.array(phi)
+        out[f"e{n}_sizes"] = sizes
+        out[f"e{n}_X"] = X
+        out[f"e{n}_ids"] = ids
+        out[f"e{n}_Q"] = Q
+        out[f"e{n}_top_ids"] = np.array([[d_ for d_, _ in r_] for r_ in res])
+        out[f"e{n}_top_scores"] = np.array([[s_ for _, s_ in r_] for r_ in res])
+    out["n_e2e"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(HERE, "agg.npz"), **out)
+
+
 if __name__ == "__main__":
     assert "reference" in dessert.__file__, dessert.__file__
-    make_lsh()
-    make_small()
-    make_end_to_end()
-    make_prefilter()
-    make_cfg0()
+    makers = {"lsh": make_lsh, "agg": make_agg, "small": make_small, "end_to_end": make_end_to_end,
+              "prefilter": make_prefilter, "cfg0": make_cfg0}
+    for name in (sys.argv[1:] or list(makers)):  # e.g. `make_golden.py agg` for one fixture
+        makers[name]()
     print("golden vectors written to", HERE)
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -293,6 +293,93 @@ def test_end_to_end_golden_build_and_query(golden_e2e):
             assert [v for _, v in r] == list(g[f"e{n}_top_scores"][q])
 
 
+# ------------------------------------------------ general aggregation (f3)
+def test_agg_golden_all_scorers(golden_agg):
+    """K3g vs the reference's _score_chunk for every Scorer kind, bit-exact, through
+    score_matrix (all sets and an explicit candidate list) and score_candidate."""
+    from conftest import agg_case, agg_scorer
+    g = golden_agg
+    for n in range(int(g["n_shapes"])):
+        c = agg_case(g, n)
+        cfg = d.IndexConfig(d=4, C=c["C"], L=c["L"], filter=d.FilterConfig(enabled=False))
+        idx = d.build_from_codes(torch.from_numpy(c["codes"]).to(DEV), c["sizes"],
+                                 np.arange(len(c["sizes"])), cfg)
+        N = len(c["sizes"])
+        for name in (str(x) for x in g["scorers"]):
+            sc = agg_scorer(name, c["weights"])
+            want = g[f"a{n}_{name}"]
+            got, _ = d.score_matrix(idx, c["qcodes"], scorer=sc)
+            np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"{n} {name}")
+            sets = np.stack([np.arange(N)[::-1], np.roll(np.arange(N), 3)])
+            got2, _ = d.score_matrix(idx, c["qcodes"], sets=sets, scorer=sc)
+            np.testing.assert_array_equal(got2.cpu().numpy(),
+                                          np.take_along_axis(want, sets, axis=1))
+            assert d.score_candidate(idx, 1, c["qcodes"][0], scorer=sc) == want[0, 1]
+
+
+def test_agg_default_scorer_matches_fast_path(golden_small):
+    """max with explicit unit weights (general kernel) == sigma max fast kernels."""
+    g = golden_small
+    for n in range(int(g["n_shapes"])):
+        c = small_case(g, n)
+        if c["L"] > 128:
+            continue
+        cfg = d.IndexConfig(d=4, C=c["C"], L=c["L"], filter=d.FilterConfig(enabled=False))
+        idx = d.build_from_codes(torch.from_numpy(c["codes"]).to(DEV), c["sizes"],
+                                 c["doc_ids"], cfg)
+        sc = d.Scorer(inner=d.max_aggregation(), weights=np.ones(c["m_q"]))
+        got, _ = d.score_matrix(idx, c["qcodes"], scorer=sc)
+        np.testing.assert_array_equal(got.cpu().numpy(), c["scores"])
+
+
+def test_agg_end_to_end_query(golden_agg):
+    """build_index with inner_kind='avg-phi' -> query / query_batch vs the reference."""
+    g = golden_agg
+    for n in range(int(g["n_e2e"])):
+        dd, C, L, seed, top_k = (int(x) for x in g[f"e{n}_shape"])
+        phi = str(g[f"e{n}_phi"])
+        sizes = g[f"e{n}_sizes"]
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        X, ids = g[f"e{n}_X"], g[f"e{n}_ids"]
+        docs = [(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+        cfg = d.IndexConfig(d=dd, C=C, L=L, seed=seed, inner_kind="avg-phi", phi=phi,
+                            filter=d.FilterConfig(enabled=False))
+        idx = d.build_index(docs, cfg)
+        for q in range(2):
+            r = d.query(idx, g[f"e{n}_Q"][q], top_k=top_k)
+            assert [x for x, _ in r] == list(g[f"e{n}_top_ids"][q]), f"case {n} q {q}"
+            assert [v for _, v in r] == list(g[f"e{n}_top_scores"][q])
+        out_s, out_i = d.query_batch(idx, g[f"e{n}_Q"], top_k, return_tensors=True)
+        np.testing.assert_array_equal(out_i.cpu().numpy(), g[f"e{n}_top_ids"])
+        np.testing.assert_array_equal(out_s.cpu().numpy(), g[f"e{n}_top_scores"])
+
+
+def test_agg_random_long_sets_vs_oracle():
+    """Sets with up to 600 vectors (several recursive pairwise levels), m_q = 70,
+    avg-phi with weights, against the dense restatement."""
+    from oracle import dessert_oracle as O
+    from paper_2210_15748_b200 import scoring
+    rng = np.random.default_rng(5)
+    L, C, m_q = 24, 3, 70
+    sizes = np.array([600, 1, 257, 129, 130, 8, 9, 450])
+    hot = rng.integers(0, 8, size=L)
+    codes = rng.integers(0, 8, size=(int(sizes.sum()), L))
+    mask = rng.random(codes.shape) < 0.5
+    codes[mask] = np.broadcast_to(hot, codes.shape)[mask]
+    qc = rng.integers(0, 8, size=(1, m_q, L))
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    cfg = d.IndexConfig(d=4, C=C, L=L, filter=d.FilterConfig(enabled=False))
+    idx = d.build_from_codes(torch.from_numpy(codes.astype(np.int32)).to(DEV), sizes,
+                             np.arange(len(sizes)), cfg)
+    w = rng.uniform(0, 1, size=m_q)
+    for phi in d.PHI_KINDS:
+        sc = d.Scorer(inner=d.avg_phi_aggregation(phi), weights=w)
+        table = scoring.table_for(idx.lookup.table, sc)
+        want = O.score_sets_dense_agg(qc[0], codes, off, table, "avg-phi", w)
+        got, _ = d.score_matrix(idx, qc, scorer=sc)
+        np.testing.assert_array_equal(got.cpu().numpy()[0], want)
+
+
 def test_reference_index_semantics():  # pkg/tests/test_index.py restated
     nf = d.FilterConfig(enabled=False)
     rng = np.random.default_rng(0)

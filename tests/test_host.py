@@ -53,8 +53,70 @@ def test_tiny_table_bytes():  # pkg/tests/test_sketch.py:149-155
     assert d.tiny_table_bytes(m=1, r=2, L=1) == 28
 
 
-def test_unsupported_scorer_is_loud():
-    from paper_2210_15748_b200.scoring import InnerAggregation, Scorer, require_device_scorer
-    with pytest.raises(NotImplementedError):
-        require_device_scorer(Scorer(inner=InnerAggregation("avg", 1, 1, "identity")))
-    require_device_scorer(d.default_scorer())
+# ---------------------------------------------- scoring descriptors (f3)
+# behaviour of pkg/tests/test_scoring.py, restated
+
+
+def test_sigma_max_and_bounds():
+    assert d.sigma_max([0.2, 0.9, 0.5]) == pytest.approx(0.9)
+    with pytest.raises(ValueError, match="empty"):
+        d.sigma_max([])
+    agg = d.max_aggregation()
+    assert (agg.alpha, agg.beta, agg.beta_for(17)) == (1.0, 1.0, 1.0)
+
+
+def test_sigma_avg_phi_kinds():
+    assert d.sigma_avg_phi([0.5, 0.1], "identity") == pytest.approx(0.3)
+    v = d.sigma_avg_phi([1.0, 1.0], "exp-minus-one")
+    assert v == pytest.approx(np.e - 1.0)
+    agg = d.avg_phi_aggregation("exp-minus-one")
+    assert agg.beta_for(2) - 1e-12 <= v <= agg.alpha + 1e-12
+    assert d.sigma_avg_phi([0.0, 0.0, 0.0], "debiased-sigmoid") == pytest.approx(0.0)
+    ds = d.avg_phi_aggregation("debiased-sigmoid")
+    assert ds.alpha == pytest.approx(0.25)
+    assert ds.beta == pytest.approx(1.0 / (1.0 + np.exp(-1.0)) - 0.5, abs=1e-6)
+    with pytest.raises(ValueError, match="range"):
+        d.sigma_avg_phi([0.5, 1.2], "identity")
+    with pytest.raises(ValueError, match="empty"):
+        d.sigma_avg_phi([], "identity")
+    with pytest.raises(ValueError, match="phi"):
+        d.sigma_avg_phi([0.5], "cubic")
+    with pytest.raises(ValueError, match="phi"):
+        d.avg_phi_aggregation("cubic")
+
+
+def test_outer_aggregate():
+    assert d.outer_aggregate([0.4, 0.8], [1, 1]) == pytest.approx(0.6)
+    assert d.outer_aggregate([0.4, 0.8], [0, 1]) == pytest.approx(0.4)
+    with pytest.raises(ValueError, match="mismatch"):
+        d.outer_aggregate([0.4, 0.8], [1.0])
+    with pytest.raises(ValueError, match="range"):
+        d.outer_aggregate([0.5], [1.5])
+
+
+def test_maximality_sandwich():
+    rng = np.random.default_rng(0)
+    for agg in [d.max_aggregation()] + [d.avg_phi_aggregation(p) for p in d.PHI_KINDS]:
+        for _ in range(100):
+            m = int(rng.integers(1, 65))
+            x = rng.uniform(0.0, 1.0, size=m)
+            got = agg.apply(x)
+            assert agg.beta_for(m) * x.max() - 1e-12 <= got <= agg.alpha * x.max() + 1e-12
+            np.testing.assert_allclose(agg.apply_rows(x[None, :])[0], got, rtol=1e-15)
+
+
+def test_score_plan_resolution():
+    from paper_2210_15748_b200 import scoring
+    assert scoring.is_default(None) and scoring.is_default(d.default_scorer())
+    s = d.Scorer(inner=d.avg_phi_aggregation("identity"))
+    assert not scoring.is_default(s) and scoring.inner_kind_code(s) == 1
+    lut = np.linspace(0.0, 1.0, 9)
+    np.testing.assert_array_equal(scoring.table_for(lut, s), lut)
+    e = d.Scorer(inner=d.avg_phi_aggregation("exp-minus-one"))
+    np.testing.assert_array_equal(scoring.table_for(lut, e), np.expm1(lut))
+    with pytest.raises(ValueError, match="mismatch"):
+        scoring.resolve_weights(d.Scorer(d.max_aggregation(), np.ones(3)), 4)
+    with pytest.raises(ValueError, match="range"):
+        scoring.resolve_weights(d.Scorer(d.max_aggregation(), np.full(4, 2.0)), 4)
+    cfg = d.IndexConfig(d=8, inner_kind="avg-phi", phi="debiased-sigmoid")
+    assert cfg.scorer().inner == d.avg_phi_aggregation("debiased-sigmoid")

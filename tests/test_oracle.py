@@ -121,6 +121,56 @@ def test_small_golden_port_and_dense(golden_small):
             np.testing.assert_array_equal(mc, c["maxcounts"][q])
 
 
+def test_agg_golden_port_and_dense(golden_agg):
+    """Row f3: every Scorer kind (max+weights, avg-phi x 3 phis, +-weights) bit-exact
+    against the reference's _score_chunk, by the port and the dense restatement."""
+    from conftest import agg_case
+    from paper_2210_15748_b200 import scoring
+    g = golden_agg
+    names = [str(x) for x in g["scorers"]]
+    assert len(names) == 7
+    long_rows = 0
+    for n in range(int(g["n_shapes"])):
+        c = agg_case(g, n)
+        r = 1 << c["C"]
+        tables = [O.build_tiny_table(c["codes"][c["off"][i]:c["off"][i + 1]], c["L"], r)
+                  for i in range(len(c["sizes"]))]
+        for name in names:
+            sc = agg_scorer_for(name, c["weights"])
+            table = scoring.table_for(c["lut"], sc)
+            kind = sc.inner.kind
+            w = sc.weights
+            want = g[f"a{n}_{name}"]
+            for q in range(c["qcodes"].shape[0]):
+                qc = c["qcodes"][q]
+                port = np.array([O.score_port(t, qc, table, kind, w) for t in tables])
+                np.testing.assert_array_equal(port, want[q], err_msg=f"{n} {name}")
+                dense = O.score_sets_dense_agg(qc, c["codes"], c["off"], table, kind, w)
+                np.testing.assert_array_equal(dense, want[q], err_msg=f"{n} {name}")
+        # the long-row case really exercises > 128 non-zero counts per query row
+        x = c["codes"][c["off"][0]:c["off"][1]]
+        nz = ((c["qcodes"][0][:, None, :] == x[None, :, :]).sum(axis=2) > 0).sum(axis=1)
+        long_rows += int((nz > 129).sum())
+    assert long_rows > 0
+
+
+def agg_scorer_for(name, weights):
+    from conftest import agg_scorer
+    return agg_scorer(name, weights)
+
+
+def test_reduceat_restatement():
+    rng = np.random.default_rng(11)
+    for _ in range(500):
+        n = int(rng.integers(1, 600))
+        a = rng.random(n)
+        cuts = np.unique(np.concatenate([[0], rng.integers(0, n, size=3)]))
+        got = np.add.reduceat(a, cuts)
+        b = list(cuts) + [n]
+        for i in range(len(cuts)):
+            assert O.reduceat_sum(a[b[i]:b[i + 1]]) == got[i]
+
+
 def test_small_golden_c_oracle(golden_small):
     g = golden_small
     for n in range(int(g["n_shapes"])):
