@@ -132,8 +132,10 @@ int dsrt_score_candidates(const uint32_t *records, const int64_t *set_off, int64
  *   avg-phi: per_query[q] = reduceat-sum(table[c_qj] : c_qj > 0, j ascending) / m
  *   score    = mean(w * per_query)   (numpy pairwise order throughout)
  * Targets as dsrt_score_candidates (cand NULL: identity; n_cand NULL: all
- * cand_ld; entries e >= n_cand[q] are written as -1).  m_cap bounds the
- * target set size for avg-phi (its per-lane count scratch), L <= 128, C <= 16.
+ * cand_ld; entries e >= n_cand[q] unwritten; invalid set index -> NaN).
+ * inner_kind 0 runs on the K3 kernels (weights folded into their epilogue);
+ * avg-phi on a general kernel.  m_cap bounds the target set size for avg-phi
+ * (its per-lane count scratch); L <= 128, C <= 16.
  */
 size_t dsrt_score_agg_workspace(int64_t n_qsets, int64_t cand_ld, int m_q, int64_t m_cap);
 int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, int64_t n_sets,

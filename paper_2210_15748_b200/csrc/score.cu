@@ -31,12 +31,16 @@ __device__ double pw_rec(const double *a, int n) {
 // One thread per (row): LUT[maxcounts] -> numpy pairwise mean; a = per-thread
 // scratch in global memory (rows * m_q doubles).
 __global__ void finalize_kernel(const uint16_t *__restrict__ mc, int64_t rows, int m_q,
-                                const double *__restrict__ lut, double *__restrict__ scratch,
-                                double *__restrict__ scores, int64_t row_len, int64_t ld) {
+                                const double *__restrict__ lut, const double *__restrict__ weights,
+                                double *__restrict__ scratch, double *__restrict__ scores,
+                                int64_t row_len, int64_t ld) {
     const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (r >= rows) return;
     double *a = scratch + r * m_q;
-    for (int i = 0; i < m_q; ++i) a[i] = __ldg(lut + mc[r * m_q + i]);
+    for (int i = 0; i < m_q; ++i) {
+        const double v = __ldg(lut + mc[r * m_q + i]);
+        a[i] = weights != nullptr ? __dmul_rn(__ldg(weights + i), v) : v;
+    }
     const double sum = __dadd_rn(0.0, pw_rec(a, m_q));
     scores[(r / row_len) * ld + (r % row_len)] = __ddiv_rn(sum, static_cast<double>(m_q));
 }
@@ -115,6 +119,7 @@ static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
             b.m_q = min(128, a.m_q - q0);
             b.qrecs = a.qrecs + (qs * a.m_q + q0) * static_cast<int64_t>(R);
             b.scores = nullptr;
+            b.weights = nullptr;
             b.mc = mc + qs * row_len * a.m_q;
             b.mc_stride = a.m_q;
             b.mc_q0 = q0;
@@ -127,12 +132,37 @@ static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
     if (rc == DSRT_OK && a.scores != nullptr) {
         const int64_t blocks = (rows + 127) / 128;
         finalize_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(
-            mc, rows, a.m_q, a.lut, scratch, a.scores, row_len, a.cand_mode ? a.cand_ld : a.ld);
+            mc, rows, a.m_q, a.lut, a.weights, scratch, a.scores, row_len,
+            a.cand_mode ? a.cand_ld : a.ld);
         if (cudaGetLastError() != cudaSuccess) rc = DSRT_ECUDA;
     }
     cudaFreeAsync(scratch, st);
     if (own) cudaFreeAsync(own, st);
     return rc;
+}
+
+// sigma = max with optional weights for dsrt_score_agg: the exhaustive kernel
+// when every set is scored by >= 8 query sets, else the candidate kernel.
+int score_max_fast(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                   const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                   const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, int C,
+                   const double *lut, const double *weights, double *scores, cudaStream_t st) {
+    ScoreArgs a{};
+    a.recs = records; a.set_off = set_off; a.n_sets = n_sets; a.qrecs = qrecs;
+    a.n_qsets = n_qsets; a.m_q = m_q; a.L = L; a.lut = lut; a.weights = weights;
+    a.scores = scores;
+    if (cand == nullptr && n_cand == nullptr && n_qsets >= 8 && cand_ld <= n_sets) {
+        a.cand_mode = false;
+        a.sb = 0; a.se = cand_ld; a.ld = cand_ld;
+    } else {
+        a.cand_mode = true;
+        a.cand = cand; a.n_cand = n_cand; a.cand_ld = cand_ld; a.ld = cand_ld;
+    }
+    return score_dispatch(a, C, st);
+}
+
+bool score_max_fast_supported(int L, int C) {
+    return L >= 1 && L <= 128 && C >= 1 && C <= 16 && C * plane_words(L) <= 32;
 }
 
 }  // namespace dsrt

@@ -20,6 +20,20 @@
 
 namespace dsrt {
 
+int score_max_fast(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                   const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                   const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, int C,
+                   const double *lut, const double *weights, double *scores, cudaStream_t st);
+bool score_max_fast_supported(int L, int C);
+bool score_avg_supported(int L, int C, int m_q);
+int score_avg_fast(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                   const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                   const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, int C,
+                   const double *table, const double *weights, double *scores,
+                   int64_t *ovf_items, unsigned long long *ovf_count, int64_t ovf_cap,
+                   cudaStream_t st);
+constexpr int64_t kOvfCap = 1 << 20;  // overflow items recomputed from a list
+
 constexpr int kAggWarps = 8;
 constexpr int kAggMaxC = 16;
 
@@ -91,6 +105,8 @@ struct AggArgs {
     int64_t m_cap;
     size_t warp_bytes;
     uint32_t *status;       // bit 0: target set larger than m_cap
+    const int64_t *items;   // list mode: item indices (qset * cand_ld + e); NULL = all
+    int64_t n_items;
 };
 
 template <int W>
@@ -101,18 +117,19 @@ __global__ void __launch_bounds__(kAggWarps * 32)
     const int64_t n_warps = static_cast<int64_t>(gridDim.x) * kAggWarps;
     uint8_t *cnt = a.scratch + gw * a.warp_bytes;
     double *pq = reinterpret_cast<double *>(cnt + 32 * a.m_cap);
-    const int64_t items = a.n_qsets * a.cand_ld;
+    const int64_t items = a.items ? a.n_items : a.n_qsets * a.cand_ld;
     const uint32_t tail = (a.L % 32) ? ((1u << (a.L % 32)) - 1u) : 0xffffffffu;
-    for (int64_t it = gw; it < items; it += n_warps) {
+    for (int64_t ii = gw; ii < items; ii += n_warps) {
+        const int64_t it = a.items ? a.items[ii] : ii;
         const int64_t qs = it / a.cand_ld, e = it - qs * a.cand_ld;
         double *out = a.scores + qs * a.cand_ld + e;
-        if (a.n_cand != nullptr && e >= tmin<int64_t>(a.n_cand[qs], a.cand_ld)) {
-            if (lane == 0) *out = -1.0;
+        if (a.n_cand != nullptr && e >= tmin<int64_t>(a.n_cand[qs], a.cand_ld)) continue;
+        const int64_t s = a.cand ? a.cand[qs * a.cand_ld + e] : e;
+        if (s < 0 || s >= a.n_sets) {  // invalid set index: NaN, as score_cand_kernel
+            if (lane == 0) *out = __longlong_as_double(0x7ff8000000000000ll);
             continue;
         }
-        const int64_t s = a.cand ? a.cand[qs * a.cand_ld + e] : e;
-        const bool valid = s >= 0 && s < a.n_sets;  // invalid index: empty set, as score_cand_kernel
-        const int64_t v0 = valid ? a.set_off[s] : 0, m = valid ? a.set_off[s + 1] - v0 : 0;
+        const int64_t v0 = a.set_off[s], m = a.set_off[s + 1] - v0;
         if (a.kind == 1 && m > a.m_cap) {
             if (lane == 0) {
                 atomicOr(a.status, 1u);
@@ -184,10 +201,14 @@ static size_t agg_warp_bytes(int m_q, int64_t m_cap) {
 
 using namespace dsrt;
 
+static size_t ovf_bytes(int64_t items) {
+    return static_cast<size_t>(tmin<int64_t>(items, kOvfCap)) * 8 + 256;
+}
+
 extern "C" size_t dsrt_score_agg_workspace(int64_t n_qsets, int64_t cand_ld, int m_q, int64_t m_cap) {
     if (n_qsets < 0 || cand_ld < 0 || m_q < 1 || m_cap < 0) return 0;
     const int64_t warps = (agg_warps(n_qsets * cand_ld) + kAggWarps - 1) / kAggWarps * kAggWarps;
-    return static_cast<size_t>(warps) * agg_warp_bytes(m_q, m_cap) + 256;
+    return static_cast<size_t>(warps) * agg_warp_bytes(m_q, m_cap) + 256 + ovf_bytes(n_qsets * cand_ld);
 }
 
 extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
@@ -209,6 +230,9 @@ extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, i
     DSRT_REQUIRE(W <= 4, DSRT_EUNSUPPORTED, "invalid parameter: L=%d > 128 for the aggregation kernel", L);
     const int64_t items = n_qsets * cand_ld;
     if (items == 0) return DSRT_OK;
+    if (inner_kind == 0 && score_max_fast_supported(L, C))  // weighted max: the K3 kernels
+        return score_max_fast(records, set_off, n_sets, cand, n_cand, cand_ld, qrecords, n_qsets,
+                              m_q, L, C, table, weights, scores, as_stream(stream));
     DSRT_REQUIRE(ws_bytes >= dsrt_score_agg_workspace(n_qsets, cand_ld, m_q, m_cap), DSRT_EINVAL,
                  "invalid parameter: aggregation workspace too small");
     cudaStream_t st = as_stream(stream);
@@ -233,9 +257,28 @@ extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, i
     a.warp_bytes = agg_warp_bytes(m_q, m_cap);
     uint8_t *w = static_cast<uint8_t *>(workspace);
     a.status = reinterpret_cast<uint32_t *>(w);
-    a.scratch = w + 256;
-    DSRT_CUDA(cudaMemsetAsync(a.status, 0, 4, st));
-    const unsigned blocks = static_cast<unsigned>((agg_warps(items) + kAggWarps - 1) / kAggWarps);
+    unsigned long long *ovf_count = reinterpret_cast<unsigned long long *>(w + 8);
+    int64_t *ovf_items = reinterpret_cast<int64_t *>(w + 256);
+    a.scratch = w + ovf_bytes(items) + 256;
+    DSRT_CUDA(cudaMemsetAsync(w, 0, 16, st));
+    int64_t work = items;
+    if (inner_kind == 1 && score_avg_supported(L, C, m_q)) {
+        // streaming kernel; targets with > 129 colliding vectors come back as a list
+        const int64_t cap = tmin<int64_t>(items, kOvfCap);
+        int rc = score_avg_fast(records, set_off, n_sets, cand, n_cand, cand_ld, qrecords, n_qsets,
+                                m_q, L, C, table, weights, scores, ovf_items, ovf_count, cap, st);
+        if (rc) return rc;
+        unsigned long long n_ovf = 0;
+        DSRT_CUDA(cudaMemcpyAsync(&n_ovf, ovf_count, 8, cudaMemcpyDeviceToHost, st));
+        DSRT_CUDA(cudaStreamSynchronize(st));
+        if (n_ovf == 0) return DSRT_OK;
+        if (static_cast<int64_t>(n_ovf) <= cap) {
+            a.items = ovf_items;
+            a.n_items = static_cast<int64_t>(n_ovf);
+            work = a.n_items;
+        }
+    }
+    const unsigned blocks = static_cast<unsigned>((agg_warps(work) + kAggWarps - 1) / kAggWarps);
     switch (W) {
         case 1: score_agg_kernel<1><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
         case 2: score_agg_kernel<2><<<blocks, kAggWarps * 32, 0, st>>>(a); break;

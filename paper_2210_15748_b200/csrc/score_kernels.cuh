@@ -36,26 +36,44 @@ struct SlotGeom {
 // numpy pairwise_sum_DOUBLE for one leaf (n <= 128): 8 strided accumulators,
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential remainder; n < 8 sums
 // sequentially from 0.0.  Then the reduction identity 0.0 and / n (np.mean).
-__device__ __forceinline__ double lane_score(const uint8_t *__restrict__ row, int n,
-                                             const double *__restrict__ lut_s) {
+template <bool WT>
+__device__ __forceinline__ double lane_value(const uint8_t *__restrict__ row, int i,
+                                             const double *__restrict__ lut_s,
+                                             const double *__restrict__ w_s) {
+    const double v = lut_s[row[i]];
+    return WT ? __dmul_rn(w_s[i], v) : v;  // w * per_query (index.py:216)
+}
+
+template <bool WT>
+__device__ __forceinline__ double lane_score_impl(const uint8_t *__restrict__ row, int n,
+                                                  const double *__restrict__ lut_s,
+                                                  const double *__restrict__ w_s) {
     double res;
     if (n < 8) {
         res = 0.0;
-        for (int i = 0; i < n; ++i) res = __dadd_rn(res, lut_s[row[i]]);
+        for (int i = 0; i < n; ++i) res = __dadd_rn(res, lane_value<WT>(row, i, lut_s, w_s));
     } else {
         double r[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = lut_s[row[j]];
+        for (int j = 0; j < 8; ++j) r[j] = lane_value<WT>(row, j, lut_s, w_s);
         const int n8 = n - (n & 7);
         for (int i = 8; i < n8; i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], lut_s[row[i + j]]);
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], lane_value<WT>(row, i + j, lut_s, w_s));
         }
         res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (int i = n8; i < n; ++i) res = __dadd_rn(res, lut_s[row[i]]);
+        for (int i = n8; i < n; ++i) res = __dadd_rn(res, lane_value<WT>(row, i, lut_s, w_s));
     }
     return __ddiv_rn(__dadd_rn(0.0, res), static_cast<double>(n));
+}
+
+// w_s: per-query-vector weights in shared memory, or nullptr (all ones).
+__device__ __forceinline__ double lane_score(const uint8_t *__restrict__ row, int n,
+                                             const double *__restrict__ lut_s,
+                                             const double *__restrict__ w_s) {
+    return w_s != nullptr ? lane_score_impl<true>(row, n, lut_s, w_s)
+                          : lane_score_impl<false>(row, n, lut_s, w_s);
 }
 
 // Per-warp deferred epilogue: 32 slot rows of c_q bytes.
@@ -80,6 +98,7 @@ struct Slots {
 
     // lane i < n scores slot i -> out[col0 + i]; optional uint16 max counts
     __device__ __forceinline__ void flush(int m_q, const double *__restrict__ lut_s,
+                                          const double *__restrict__ w_s,
                                           double *__restrict__ out_row, int64_t col0,
                                           uint16_t *__restrict__ mc, int64_t mc_row0,
                                           int mc_stride, int mc_q0) {
@@ -90,7 +109,7 @@ struct Slots {
             const bool ok = (valid >> lane) & 1u;
             if (out_row != nullptr)
                 out_row[col0 + lane] =
-                    ok ? lane_score(row, m_q, lut_s) : __longlong_as_double(0x7ff8000000000000ll);
+                    ok ? lane_score(row, m_q, lut_s, w_s) : __longlong_as_double(0x7ff8000000000000ll);
             if (mc != nullptr && ok) {
                 uint16_t *dst = mc + (mc_row0 + col0 + lane) * mc_stride + mc_q0;
                 for (int i = 0; i < m_q; ++i) dst[i] = row[i];
@@ -191,8 +210,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     score_all_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
                      int64_t set_begin, int64_t set_end, const uint32_t *__restrict__ qrecs,
                      int64_t n_qsets, int m_q, int L, const double *__restrict__ lut,
-                     double *__restrict__ scores, int64_t ld, uint16_t *__restrict__ maxcounts,
-                     int mc_stride, int mc_q0, int n_chunks) {
+                     const double *__restrict__ weights, double *__restrict__ scores, int64_t ld,
+                     uint16_t *__restrict__ maxcounts, int mc_stride, int mc_q0, int n_chunks) {
     constexpr int R = ((K * W) + 3) & ~3;
     constexpr int S = QS * QPL;  // register slots per lane
     extern __shared__ __align__(128) uint8_t smem[];
@@ -201,6 +220,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     uint64_t *empty = full + kStages;
     uint8_t *slot_mem = reinterpret_cast<uint8_t *>(empty + kStages);
     double *lut_s = reinterpret_cast<double *>(slot_mem + NW * QS * SlotGeom<QPL>::kBytes);
+    double *w_s = weights != nullptr ? lut_s + (L + 1) : nullptr;
     __shared__ int64_t bounds[2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -221,6 +241,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
+    if (w_s != nullptr)
+        for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = __ldg(weights + i);
     __syncthreads();
     const int64_t s_lo = bounds[0], s_hi = bounds[1];
     if (s_lo >= s_hi) return;
@@ -271,7 +293,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         for (int j = 0; j < QS; ++j) {
             const int64_t qs = qset0 + j;
             if (qs < n_qsets)
-                slots[j].flush(m_q, lut_s, scores ? scores + qs * ld : nullptr, slot_col, maxcounts,
+                slots[j].flush(m_q, lut_s, w_s, scores ? scores + qs * ld : nullptr, slot_col, maxcounts,
                                qs * ld, mc_stride, mc_q0);
             slots[j].n = 0;
             slots[j].valid = 0;
@@ -367,7 +389,8 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
                       int64_t n_sets, const int64_t *__restrict__ cand,
                       const int32_t *__restrict__ n_cand, int64_t cand_ld,
                       const uint32_t *__restrict__ qrecs, int64_t n_qsets, int m_q, int L,
-                      const double *__restrict__ lut, double *__restrict__ scores,
+                      const double *__restrict__ lut, const double *__restrict__ weights,
+                      double *__restrict__ scores,
                       uint16_t *__restrict__ maxcounts, int mc_stride, int mc_q0, int64_t run_len,
                       int64_t runs_per_q) {
     constexpr int R = ((K * W) + 3) & ~3;
@@ -379,12 +402,15 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     uint64_t *bars = reinterpret_cast<uint64_t *>(after_bufs) + warp * kBufs;
     uint8_t *slot_mem = after_bufs + kCandWarps * kBufs * sizeof(uint64_t);
     double *lut_s = reinterpret_cast<double *>(slot_mem + kCandWarps * SlotGeom<QPL>::kBytes);
+    double *w_s = weights != nullptr ? lut_s + (L + 1) : nullptr;
 
     if (lane == 0) {
         for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
+    if (w_s != nullptr)
+        for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = __ldg(weights + i);
     __syncthreads();
 
     const int64_t gw = static_cast<int64_t>(blockIdx.x) * kCandWarps + warp;
@@ -455,7 +481,7 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
 #pragma unroll
             for (int i = 0; i < QPL; ++i) rmin[i] = L;
             if (slots.n == 32) {
-                slots.flush(m_q, lut_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
+                slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
                 slot_col += 32;
             }
             ++ce;
@@ -469,7 +495,7 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         issue();  // refill the buffer just consumed
     }
     if (slots.n > 0)
-        slots.flush(m_q, lut_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
+        slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
     // drain: wait for outstanding pieces so no bulk copy outlives the CTA
     while (consumed < issued) {
         const int b = static_cast<int>(consumed % kBufs);
@@ -482,10 +508,11 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
 template <int K, int W, int QPL, int QS>
 static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, int64_t se,
                       const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
-                      double *scores, int64_t ld, uint16_t *mc, int mc_stride, int mc_q0,
-                      cudaStream_t st) {
+                      const double *weights, double *scores, int64_t ld, uint16_t *mc,
+                      int mc_stride, int mc_q0, cudaStream_t st) {
     constexpr int NW = 8;
-    const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1) * sizeof(double);
+    const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1) * sizeof(double) +
+                        (weights != nullptr ? m_q * sizeof(double) : 0);
     auto kern = score_all_kernel<K, W, QPL, NW, QS>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = (n_qsets + NW * QS - 1) / (NW * QS);
@@ -500,7 +527,7 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
     dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(chunks));
     DSRT_REQUIRE(groups < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many query sets");
     kern<<<grid, (NW + 1) * 32, smem, st>>>(recs, set_off, sb, se, qrecs, n_qsets, m_q, L, lut,
-                                           scores, ld, mc, mc_stride, mc_q0,
+                                           weights, scores, ld, mc, mc_stride, mc_q0,
                                            static_cast<int>(chunks));
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
@@ -510,8 +537,10 @@ template <int K, int W, int QPL>
 static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_sets,
                        const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
                        const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
-                       double *scores, uint16_t *mc, int mc_stride, int mc_q0, cudaStream_t st) {
-    const size_t smem = cand_smem_static<QPL>() + (L + 1) * sizeof(double);
+                       const double *weights, double *scores, uint16_t *mc, int mc_stride,
+                       int mc_q0, cudaStream_t st) {
+    const size_t smem = cand_smem_static<QPL>() + (L + 1) * sizeof(double) +
+                        (weights != nullptr ? m_q * sizeof(double) : 0);
     auto kern = score_cand_kernel<K, W, QPL>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
@@ -527,8 +556,8 @@ static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_s
     const int64_t blocks = (warps + kCandWarps - 1) / kCandWarps;
     DSRT_REQUIRE(blocks < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: grid too large");
     kern<<<static_cast<unsigned>(blocks), kCandWarps * 32, smem, st>>>(
-        recs, set_off, n_sets, cand, n_cand, cand_ld, qrecs, n_qsets, m_q, L, lut, scores, mc,
-        mc_stride, mc_q0, run_len, runs);
+        recs, set_off, n_sets, cand, n_cand, cand_ld, qrecs, n_qsets, m_q, L, lut, weights, scores,
+        mc, mc_stride, mc_q0, run_len, runs);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
@@ -546,6 +575,7 @@ struct ScoreArgs {
     int64_t n_qsets;
     int m_q, L;
     const double *lut;
+    const double *weights;  // (m_q) or nullptr = all ones
     double *scores;
     int64_t ld;
     uint16_t *mc;
@@ -557,20 +587,20 @@ template <int K, int W, int QPL>
 static int run_one(const ScoreArgs &a, cudaStream_t st) {
     if (a.cand_mode)
         return launch_cand<K, W, QPL>(a.recs, a.set_off, a.n_sets, a.cand, a.n_cand, a.cand_ld,
-                                      a.qrecs, a.n_qsets, a.m_q, a.L, a.lut, a.scores, a.mc,
+                                      a.qrecs, a.n_qsets, a.m_q, a.L, a.lut, a.weights, a.scores, a.mc,
                                       a.mc_stride, a.mc_q0, st);
     // register-block several query sets per warp when there are enough of them
     if constexpr (QPL == 1 && W <= 2 && K <= 8) {
         const int qs = a.qs_override > 0 ? a.qs_override : (a.n_qsets >= 256 ? (W == 1 ? 4 : 2) : 1);
         if (qs == 4)
             return launch_all<K, W, QPL, 4>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
-                                            a.L, a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+                                            a.L, a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
         if (qs == 2)
             return launch_all<K, W, QPL, 2>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
-                                            a.L, a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+                                            a.L, a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
     }
     return launch_all<K, W, QPL, 1>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q, a.L,
-                                    a.lut, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+                                    a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
 }
 
 template <int K, int W>
