@@ -189,6 +189,22 @@ int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scale, void *ds
 int dsrt_to_bf16_rows(const double *src, int64_t n, int d, double scale, void *dst, void *stream);
 
 /*
+ * K7 -- train_centroids (prefilter.py:47-82): spherical Lloyd iterations in
+ * float64, deterministic (no atomics), in the reference's operation order:
+ * unit rows (numpy norm), init = unit rows[init_idx] (init_idx: k indices
+ * from np.random.default_rng(seed).choice(n, k, replace=False), computed by
+ * the caller), per iteration exact argmax assignment (K6 screen for d = 128,
+ * SIMT scan otherwise), sequential per-centroid sums in sample order
+ * (np.add.at), pairwise norms, dead clusters reseeded from the stable argsort
+ * of the best similarities.  centroids_out: (k, d) float64.  d <= 1024.
+ * Errors in the reference's order: zero vector, k < 1, n < k, iters < 1.
+ */
+size_t dsrt_train_centroids_workspace(int64_t n, int d, int64_t k);
+int dsrt_train_centroids(const double *samples, int64_t n, int d, int64_t k, int iters,
+                         const int64_t *init_idx, double *centroids_out, void *workspace,
+                         size_t ws_bytes, void *stream);
+
+/*
  * K6 -- centroid assignment for build_centroid_index (prefilter.py:85-108):
  * assign[i] = argmax_c <X[i], centroids[c]> (lowest c on ties, as np.argmax),
  * exact: tensor-core screen + float64 re-rank + exact fallback.  X of

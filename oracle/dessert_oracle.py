@@ -323,6 +323,40 @@ def _unit_rows(X, name: str) -> np.ndarray:  # prefilter.py:37-44
     return X / norms
 
 
+def train_centroids(samples, k: int, iters: int, seed: int) -> np.ndarray:
+    """Spherical Lloyd iterations, prefilter.py:47-82, restated step by step.
+
+    Also spells out the operation order K7 reproduces: dot products as
+    X @ C.T (BLAS), sums by in-order np.add.at, row norms by np.linalg.norm,
+    dead clusters (empty or norm < 1e-12) reseeded in ascending id from the
+    stable argsort of each point's best similarity.
+    """
+    X = _unit_rows(samples, "samples")
+    n = X.shape[0]
+    if k < 1:
+        raise ValueError(f"invalid parameter: k must be >= 1, got {k}")
+    if n < k:
+        raise ValueError(f"too few samples: need at least k={k}, got {n}")
+    if iters < 1:
+        raise ValueError(f"invalid parameter: iters must be >= 1, got {iters}")
+    C = X[np.random.default_rng(seed).choice(n, size=k, replace=False)].copy()
+    for _ in range(iters):
+        sims = X @ C.T
+        assign = np.argmax(sims, axis=1)
+        sums = np.zeros_like(C)
+        np.add.at(sums, assign, X)
+        counts = np.bincount(assign, minlength=k)
+        norms = np.linalg.norm(sums, axis=1)
+        dead = np.flatnonzero((counts == 0) | (norms < 1e-12))
+        if dead.size:
+            best = sims[np.arange(n), assign]
+            far = np.argsort(best, kind="stable")[:dead.size]
+            sums[dead] = X[far]
+            norms[dead] = 1.0
+        C = sums / norms[:, None]
+    return C
+
+
 def build_centroid_index(docs, centroid_vectors) -> list[np.ndarray]:
     """Posting c = ascending doc indices with a vector whose argmax centroid is c.
 

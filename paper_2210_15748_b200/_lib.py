@@ -47,6 +47,8 @@ SIGNATURES = {
     "dsrt_score_agg_workspace": (_sz, [_i64, _i64, _i32, _i64]),
     "dsrt_score_agg": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _i32, _i32,
                               _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "dsrt_train_centroids_workspace": (_sz, [_i64, _i32, _i64]),
+    "dsrt_train_centroids": (_i32, [_vp, _i64, _i32, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "dsrt_topk": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_topk_max_k": (_i32, []),
     "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp,

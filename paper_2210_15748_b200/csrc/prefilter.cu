@@ -707,7 +707,7 @@ template <typename TQ>
 __global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int32_t *__restrict__ list_n,
                                  const TQ *__restrict__ Q, const double *__restrict__ cents,
                                  int64_t n_rows, int d, int P, int32_t *__restrict__ probed,
-                                 int32_t *__restrict__ fallback) {
+                                 int32_t *__restrict__ fallback, double *__restrict__ best = nullptr) {
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n_rows) return;
@@ -732,6 +732,7 @@ __global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int
     int ei = 0x7fffffff;
     warp_topP_merge(es, ei, ex, eid, P);
     if (lane < P) probed[row * P + lane] = ei;
+    if (best != nullptr && lane == 0) best[row] = es;  // P == 1: the exact top similarity
 }
 
 // exact float64 scan for flagged rows (one CTA per row; rare)
@@ -739,7 +740,7 @@ template <typename TQ>
 __global__ void __launch_bounds__(256)
     pf_fallback_kernel(const int32_t *__restrict__ fallback, const TQ *__restrict__ Q,
                        const double *__restrict__ cents, int64_t n_rows, int64_t k_c, int d, int P,
-                       int32_t *__restrict__ probed) {
+                       int32_t *__restrict__ probed, double *__restrict__ best = nullptr) {
     const int64_t row = blockIdx.x;
     if (row >= n_rows || fallback[row] == 0) return;
     __shared__ double q[512];
@@ -771,6 +772,7 @@ __global__ void __launch_bounds__(256)
         for (int w = 0; w < 8; ++w) warp_topP_merge(fs, fi, lane < P ? cs[w][lane] : -INFINITY,
                                                     lane < P ? ci[w][lane] : 0x7fffffff, P);
         if (lane < P) probed[row * P + lane] = fi;
+        if (best != nullptr && lane == 0) best[row] = fs;
     }
 }
 
@@ -979,7 +981,7 @@ static size_t assign_ws_layout(int64_t n, size_t *parts) {
 template <typename TQ>
 static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const void *cents_lp,
                        int64_t k_c, bool raw, bool bf16, int32_t *assign_out, void *ws,
-                       cudaStream_t st) {
+                       cudaStream_t st, double *best = nullptr) {
     size_t part[6];
     assign_ws_layout(n, part);
     uint8_t *w = static_cast<uint8_t *>(ws);
@@ -1030,14 +1032,22 @@ static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const
         rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, nullptr, theta, lists, listn, idesc);
         if (rc) return rc;
         pf_rerank_kernel<TQ><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
-            lists, listn, X + r0 * d, cents, rows, d, 1, assign_out + r0, fallback);
+            lists, listn, X + r0 * d, cents, rows, d, 1, assign_out + r0, fallback,
+            best ? best + r0 : nullptr);
         pf_fallback_kernel<TQ><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, X + r0 * d, cents, rows,
-                                                                             k_c, d, 1, assign_out + r0);
+                                                                             k_c, d, 1, assign_out + r0,
+                                                                             best ? best + r0 : nullptr);
         if (vtmp) cudaFreeAsync(vtmp, st);
         DSRT_LAUNCH_CHECK();
     }
     return DSRT_OK;
 }
+// k-means assignment step: float64 unit rows, exact argmax and its similarity.
+int assign_unit_rows_f64(const double *X, int64_t n, const double *cents, const void *cents_f16,
+                         int64_t k_c, int32_t *assign_out, double *best, void *ws, cudaStream_t st) {
+    return assign_impl<double>(X, n, 128, cents, cents_f16, k_c, false, false, assign_out, ws, st, best);
+}
+
 }  // namespace dsrt
 
 extern "C" size_t dsrt_assign_centroids_workspace(int64_t n, int64_t k_c) {

@@ -198,6 +198,21 @@ def score_agg(records, set_off, qrecords, m_q: int, L: int, C: int, table, inner
     return scores
 
 
+def train_centroids(samples: torch.Tensor, k: int, iters: int, init_idx):
+    """K7: spherical k-means on float64 samples (n, d) -> centroids (k, d) float64."""
+    _need(samples, torch.float64, "samples")
+    n, d = samples.shape
+    init = None
+    if init_idx is not None:
+        init = torch.as_tensor(np.asarray(init_idx, dtype=np.int64)).to(samples.device)
+    out = torch.empty((max(k, 1), d), dtype=torch.float64, device=samples.device)
+    ws_bytes = _lib.lib().dsrt_train_centroids_workspace(n, d, k)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=samples.device)
+    _lib.call("dsrt_train_centroids", _ptr(samples), n, d, k, iters, _ptr(init), _ptr(out),
+              _ptr(ws), ws_bytes, _stream())
+    return out
+
+
 # ------------------------------------------------------------------- K4
 def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None):
     """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D)."""

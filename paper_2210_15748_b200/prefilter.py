@@ -94,37 +94,21 @@ def _as_dev(X, device="cuda") -> torch.Tensor:
 
 
 def train_centroids(samples, k: int, iters: int, seed: int, device="cuda") -> Centroids:
-    """Spherical Lloyd iterations (prefilter.py:47-82) on the device in float64."""
-    X = _unit_rows_dev(_as_dev(samples, device), "samples")
+    """Spherical Lloyd iterations (prefilter.py:47-82) -- K7, native and deterministic.
+
+    The init indices come from the reference's own rng call
+    (np.random.default_rng(seed).choice(n, k, replace=False)); everything
+    else runs in dsrt_train_centroids in float64, in numpy's operation order.
+    """
+    X = _as_dev(samples, device)
+    if X.dim() != 2 or X.shape[0] == 0:
+        raise ValueError(f"samples must be a non-empty (n, d) matrix, got shape {tuple(X.shape)}")
+    X = X.to(torch.float64).contiguous()
     n = X.shape[0]
-    if k < 1:
-        raise ValueError(f"invalid parameter: k must be >= 1, got {k}")
-    if n < k:
-        raise ValueError(f"too few samples: need at least k={k}, got {n}")
-    if iters < 1:
-        raise ValueError(f"invalid parameter: iters must be >= 1, got {iters}")
-    rng = np.random.default_rng(seed)
-    init = torch.from_numpy(rng.choice(n, size=k, replace=False)).to(X.device)
-    cents = X[init].clone()
-    for _ in range(iters):
-        assign = torch.empty(n, dtype=torch.int64, device=X.device)
-        best = torch.empty(n, dtype=torch.float64, device=X.device)
-        for lo in range(0, n, 1 << 16):
-            sims = X[lo:lo + (1 << 16)] @ cents.T
-            b, a = sims.max(dim=1)  # first max on ties, like np.argmax
-            assign[lo:lo + (1 << 16)] = a
-            best[lo:lo + (1 << 16)] = b
-        sums = torch.zeros_like(cents).index_add_(0, assign, X)
-        counts = torch.bincount(assign, minlength=k)
-        norms = torch.linalg.norm(sums, dim=1)
-        dead = (counts == 0) | (norms < 1e-12)
-        if bool(dead.any()):
-            order = torch.argsort(best, stable=True)
-            slots = torch.nonzero(dead).flatten()
-            pts = order[: slots.numel()]
-            sums[slots] = X[pts]
-            norms[slots] = 1.0
-        cents = sums / norms[:, None]
+    init = None
+    if 1 <= k <= n and iters >= 1:
+        init = np.random.default_rng(seed).choice(n, size=k, replace=False)
+    cents = engine.train_centroids(X, k, iters, init)
     return Centroids(k=k, seed=seed, vectors=cents.cpu().numpy())
 
 

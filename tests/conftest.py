@@ -8,6 +8,8 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
 GOLDEN = os.path.join(REPO, "tests", "golden")
+if GOLDEN not in sys.path:
+    sys.path.insert(0, GOLDEN)  # kmeans_inputs (seeded golden inputs)
 
 
 def pytest_configure(config):
@@ -46,6 +48,11 @@ def golden_prefilter():
 @pytest.fixture(scope="session")
 def golden_e2e():
     return load_golden("end_to_end.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_kmeans():
+    return load_golden("kmeans.npz")
 
 
 @pytest.fixture(scope="session")

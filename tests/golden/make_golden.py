@@ -277,10 +277,36 @@ def make_agg():
     np.savez_compressed(os.path.join(HERE, "agg.npz"), **out)
 
 
+def make_kmeans():
+    """train_centroids (prefilter.py:47-82) and a filter-enabled build_index +
+    query end to end (index.py:147-157) -- row f4.  Inputs: kmeans_inputs.py."""
+    sys.path.insert(0, HERE)
+    import kmeans_inputs as KI
+    out = {}
+    for c, (n, d, k, iters, seed, _) in enumerate(KI.SPECS):
+        out[f"k{c}_C"] = ref_prefilter.train_centroids(KI.samples(c), k=k, iters=iters,
+                                                       seed=seed).vectors
+    sizes, X, ids, Q = KI.e2e_docs()
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    docs = [(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+    cfg = dessert.IndexConfig(d=128, C=6, L=32, seed=11,
+                              filter=dessert.FilterConfig(enabled=True, iters=4, probe=3,
+                                                          k_filter=40))
+    index = dessert.build_index(docs, cfg)
+    centroids, cindex = index.filter
+    out["e_centroids"] = centroids.vectors
+    out["e_post_off"] = np.concatenate([[0], np.cumsum([len(p) for p in cindex.postings])])
+    out["e_post_docs"] = np.concatenate(cindex.postings).astype(np.int64)
+    res = [dessert.query(index, q, top_k=10) for q in Q]
+    out["e_top_ids"] = np.array([[d_ for d_, _ in r_] for r_ in res])
+    out["e_top_scores"] = np.array([[s_ for _, s_ in r_] for r_ in res])
+    np.savez_compressed(os.path.join(HERE, "kmeans.npz"), **out)
+
+
 if __name__ == "__main__":
     assert "reference" in dessert.__file__, dessert.__file__
     makers = {"lsh": make_lsh, "agg": make_agg, "small": make_small, "end_to_end": make_end_to_end,
-              "prefilter": make_prefilter, "cfg0": make_cfg0}
+              "prefilter": make_prefilter, "cfg0": make_cfg0, "kmeans": make_kmeans}
     for name in (sys.argv[1:] or list(makers)):  # e.g. `make_golden.py agg` for one fixture
         makers[name]()
     print("golden vectors written to", HERE)

@@ -380,6 +380,57 @@ def test_agg_random_long_sets_vs_oracle():
         np.testing.assert_array_equal(got.cpu().numpy()[0], want)
 
 
+# ------------------------------------------------------ k-means (K7, f4)
+def test_train_centroids_golden(golden_kmeans):
+    """Native train_centroids vs the reference's, bit for bit (TC path at d=128,
+    SIMT path otherwise, dead-cluster reseeding in the 'dups' cases)."""
+    import kmeans_inputs as KI
+    g = golden_kmeans
+    for c, (n, dd, k, iters, seed, _) in enumerate(KI.SPECS):
+        S = KI.samples(c)
+        got = d.train_centroids(S, k, iters, seed).vectors
+        want = g[f"k{c}_C"]
+        np.testing.assert_array_equal(got, want, err_msg=f"case {c}: max |diff| "
+                                      f"{np.abs(got - want).max():.3e}")
+        # deterministic: a second run (and a device-resident input) gives the same bytes
+        got2 = d.train_centroids(torch.from_numpy(S).to(DEV), k, iters, seed).vectors
+        np.testing.assert_array_equal(got2, got)
+
+
+def test_train_centroids_errors():
+    with pytest.raises(ValueError, match="zero vector"):
+        d.train_centroids(np.zeros((3, 4)), 0, 1, 0)
+    with pytest.raises(ValueError, match="k must be"):
+        d.train_centroids(np.ones((3, 4)), 0, 1, 0)
+    with pytest.raises(ValueError, match="too few samples"):
+        d.train_centroids(np.ones((3, 4)), 4, 1, 0)
+    with pytest.raises(ValueError, match="iters"):
+        d.train_centroids(np.ones((3, 4)), 2, 0, 0)
+    with pytest.raises(ValueError, match="non-empty"):
+        d.train_centroids(np.ones((0, 4)), 1, 1, 0)
+
+
+def test_filter_enabled_build_query_golden(golden_kmeans):
+    """build_index with the prefilter on (trained centroids, postings) -> query,
+    against the reference end to end."""
+    import kmeans_inputs as KI
+    g = golden_kmeans
+    sizes, X, ids, Q = KI.e2e_docs()
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    docs = [(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+    cfg = d.IndexConfig(d=128, C=6, L=32, seed=11,
+                        filter=d.FilterConfig(enabled=True, iters=4, probe=3, k_filter=40))
+    idx = d.build_index(docs, cfg)
+    centroids, cindex = idx.filter
+    np.testing.assert_array_equal(centroids.vectors, g["e_centroids"])
+    np.testing.assert_array_equal(cindex.post_off.cpu().numpy(), g["e_post_off"])
+    np.testing.assert_array_equal(cindex.post_docs.cpu().numpy(), g["e_post_docs"])
+    for q in range(Q.shape[0]):
+        r = d.query(idx, Q[q], top_k=10)
+        assert [x for x, _ in r] == list(g["e_top_ids"][q])
+        assert [v for _, v in r] == list(g["e_top_scores"][q])
+
+
 def test_reference_index_semantics():  # pkg/tests/test_index.py restated
     nf = d.FilterConfig(enabled=False)
     rng = np.random.default_rng(0)

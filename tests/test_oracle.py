@@ -159,6 +159,26 @@ def agg_scorer_for(name, weights):
     return agg_scorer(name, weights)
 
 
+def test_kmeans_golden_oracle(golden_kmeans):
+    """Row f4: the oracle's train_centroids restatement equals the reference's output."""
+    import kmeans_inputs as KI
+    g = golden_kmeans
+    for c, (n, d, k, iters, seed, _) in enumerate(KI.SPECS):
+        got = O.train_centroids(KI.samples(c), k, iters, seed)
+        np.testing.assert_array_equal(got, g[f"k{c}_C"], err_msg=f"case {c}")
+
+
+def test_kmeans_oracle_errors():
+    with pytest.raises(ValueError, match="zero vector"):
+        O.train_centroids(np.zeros((3, 4)), 0, 1, 0)
+    with pytest.raises(ValueError, match="k must be"):
+        O.train_centroids(np.ones((3, 4)), 0, 1, 0)
+    with pytest.raises(ValueError, match="too few samples"):
+        O.train_centroids(np.ones((3, 4)), 4, 1, 0)
+    with pytest.raises(ValueError, match="iters"):
+        O.train_centroids(np.ones((3, 4)), 2, 0, 0)
+
+
 def test_reduceat_restatement():
     rng = np.random.default_rng(11)
     for _ in range(500):
