@@ -205,6 +205,40 @@ int dsrt_train_centroids(const double *samples, int64_t n, int d, int64_t k, int
                          size_t ws_bytes, void *stream);
 
 /*
+ * .dsri index files (storage.py:130-260, sketch.py:192-239) from / to the
+ * device layout.
+ * dsrt_dsri_write_sets: the sets section -- per set s at byte rec_off[s] of
+ *   out: doc id u64, TinyTable header (m, L, r, flags u32, 0 u64), offsets
+ *   (L, r+1) and ids (L, m), u8/u16 LE by m -- built from the plane records
+ *   with a stable per-(set, table) counting sort.  C <= 12.
+ * dsrt_postings_to_varints: prefilter postings CSR -> the varint stream
+ *   (count, then doc-id deltas, per centroid); out NULL = length only.
+ * dsrt_dsri_scan_sets (HOST memory, no GPU): walk the set headers of buf
+ *   from pos; per set doc id, m and TinyTable position; stops at the first
+ *   header failure (err_kind 1..6, see storage.cu).  Returns sets parsed.
+ * dsrt_dsri_decode_sets: validate (offsets span 0..m, monotone, ids a
+ *   permutation) and decode codes (n_vec, L) for the parsed sets;
+ *   *first_bad = -1 or (set << 2 | kind) of the first failing set.
+ * dsrt_varints_to_postings: varint stream -> postings CSR (ERANGE: truncated).
+ */
+int dsrt_dsri_write_sets(const uint32_t *records, const int64_t *set_off, const uint64_t *doc_ids,
+                         int64_t n_sets, int L, int C, const int64_t *rec_off, uint8_t *out,
+                         void *stream);
+size_t dsrt_varint_workspace(int64_t n_vals);
+int dsrt_postings_to_varints(const int64_t *post_off, const int64_t *post_docs, int64_t k,
+                             int64_t total, uint8_t *out, int64_t *n_bytes, void *workspace,
+                             size_t ws_bytes, void *stream);
+int64_t dsrt_dsri_scan_sets(const uint8_t *buf, size_t len, size_t pos, int64_t n_sets, int L,
+                            int C, uint64_t *doc_ids, int64_t *sizes, int64_t *tt_off,
+                            uint32_t *hdr_out, int *err_kind, size_t *end_pos);
+int dsrt_dsri_decode_sets(const uint8_t *buf, const int64_t *tt_off, const int64_t *set_off,
+                          int64_t n_sets, int L, int C, int64_t m_max, void *codes,
+                          int code_bytes, int64_t *first_bad, void *stream);
+int dsrt_varints_to_postings(const uint8_t *bytes, int64_t n_bytes, int64_t k, int64_t *post_off,
+                             int64_t *post_docs, int64_t *total_out, void *workspace,
+                             size_t ws_bytes, void *stream);
+
+/*
  * K6 -- centroid assignment for build_centroid_index (prefilter.py:85-108):
  * assign[i] = argmax_c <X[i], centroids[c]> (lowest c on ties, as np.argmax),
  * exact: tensor-core screen + float64 re-rank + exact fallback.  X of

@@ -49,6 +49,12 @@ SIGNATURES = {
                               _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "dsrt_train_centroids_workspace": (_sz, [_i64, _i32, _i64]),
     "dsrt_train_centroids": (_i32, [_vp, _i64, _i32, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "dsrt_dsri_write_sets": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "dsrt_varint_workspace": (_sz, [_i64]),
+    "dsrt_postings_to_varints": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "dsrt_dsri_scan_sets": (_i64, [_vp, _sz, _sz, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dsrt_dsri_decode_sets": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i64, _vp, _i32, _vp, _vp]),
+    "dsrt_varints_to_postings": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dsrt_topk": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_topk_max_k": (_i32, []),
     "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp,

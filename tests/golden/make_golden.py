@@ -303,10 +303,35 @@ def make_kmeans():
     np.savez_compressed(os.path.join(HERE, "kmeans.npz"), **out)
 
 
+def make_storage():
+    """.dsri files written by the reference's save_index (storage.py:130-173) and
+    query results of the same indexes -- row f2.  Inputs: storage_inputs.py."""
+    import tempfile
+    sys.path.insert(0, HERE)
+    import storage_inputs as SI
+    from dessert import storage as ref_storage
+    out = {}
+    for name, (d, C, L, seed, inner, phi, fkw, _) in SI.CASES.items():
+        filt = dessert.FilterConfig(enabled=fkw is not None, **(fkw or {}))
+        cfg = dessert.IndexConfig(d=d, C=C, L=L, seed=seed, inner_kind=inner, phi=phi, filter=filt)
+        index = dessert.build_index(SI.docs(name), cfg)
+        with tempfile.TemporaryDirectory() as tmp:
+            path = os.path.join(tmp, "x.dsri")
+            ref_storage.save_index(path, index)
+            raw = open(path, "rb").read()
+        out[f"{name}_file"] = np.frombuffer(raw, dtype=np.uint8)
+        for q, Q in enumerate(SI.queries(name)):
+            res = dessert.query(index, Q, top_k=5)
+            out[f"{name}_q{q}_ids"] = np.array([x for x, _ in res], dtype=np.int64)
+            out[f"{name}_q{q}_scores"] = np.array([v for _, v in res], dtype=np.float64)
+    np.savez_compressed(os.path.join(HERE, "storage.npz"), **out)
+
+
 if __name__ == "__main__":
     assert "reference" in dessert.__file__, dessert.__file__
     makers = {"lsh": make_lsh, "agg": make_agg, "small": make_small, "end_to_end": make_end_to_end,
-              "prefilter": make_prefilter, "cfg0": make_cfg0, "kmeans": make_kmeans}
+              "prefilter": make_prefilter, "cfg0": make_cfg0, "kmeans": make_kmeans,
+              "storage": make_storage}
     for name in (sys.argv[1:] or list(makers)):  # e.g. `make_golden.py agg` for one fixture
         makers[name]()
     print("golden vectors written to", HERE)
