@@ -69,7 +69,7 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _sets_section(index: DessertIndex) -> bytes:
+def _sets_section(index: DessertIndex) -> np.ndarray:
     cfg = index.config
     r = 1 << cfg.C
     sizes = index.sizes.astype(np.int64)
@@ -83,7 +83,7 @@ def _sets_section(index: DessertIndex) -> bytes:
     _lib.call("dsrt_dsri_write_sets", _ptr(index.records), _ptr(index.set_off),
               _ptr(index.doc_ids_dev), index.n_docs, cfg.L, cfg.C, _ptr(off_dev), _ptr(out),
               _stream())
-    return out.cpu().numpy().tobytes()
+    return out.cpu().numpy()
 
 
 def _postings_varints(cindex: CentroidIndex) -> bytes:
@@ -119,7 +119,9 @@ def save_index(path, index: DessertIndex) -> None:
         parts.append(struct.pack("<IIQ", centroids.k, cfg.d, cindex.n_docs))
         parts.append(np.ascontiguousarray(centroids.vectors, dtype="<f8").tobytes())
         parts.append(_postings_varints(cindex))
-    Path(path).write_bytes(b"".join(parts))
+    with open(path, "wb") as f:  # buffers written as they are (no joined copy)
+        for part in parts:
+            f.write(memoryview(part))
 
 
 class _Reader:
