@@ -36,44 +36,29 @@ struct SlotGeom {
 // numpy pairwise_sum_DOUBLE for one leaf (n <= 128): 8 strided accumulators,
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), sequential remainder; n < 8 sums
 // sequentially from 0.0.  Then the reduction identity 0.0 and / n (np.mean).
-template <bool WT>
-__device__ __forceinline__ double lane_value(const uint8_t *__restrict__ row, int i,
-                                             const double *__restrict__ lut_s,
-                                             const double *__restrict__ w_s) {
-    const double v = lut_s[row[i]];
-    return WT ? __dmul_rn(w_s[i], v) : v;  // w * per_query (index.py:216)
-}
-
-template <bool WT>
-__device__ __forceinline__ double lane_score_impl(const uint8_t *__restrict__ row, int n,
-                                                  const double *__restrict__ lut_s,
-                                                  const double *__restrict__ w_s) {
-    double res;
-    if (n < 8) {
-        res = 0.0;
-        for (int i = 0; i < n; ++i) res = __dadd_rn(res, lane_value<WT>(row, i, lut_s, w_s));
-    } else {
-        double r[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = lane_value<WT>(row, j, lut_s, w_s);
-        const int n8 = n - (n & 7);
-        for (int i = 8; i < n8; i += 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], lane_value<WT>(row, i + j, lut_s, w_s));
-        }
-        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (int i = n8; i < n; ++i) res = __dadd_rn(res, lane_value<WT>(row, i, lut_s, w_s));
-    }
-    return __ddiv_rn(__dadd_rn(0.0, res), static_cast<double>(n));
-}
-
-// w_s: per-query-vector weights in shared memory, or nullptr (all ones).
+// w_s: per-query-vector weights in shared memory (all 1.0 for the default
+// scorer: 1.0 * v == v exactly, so one code path serves both, index.py:216).
 __device__ __forceinline__ double lane_score(const uint8_t *__restrict__ row, int n,
                                              const double *__restrict__ lut_s,
                                              const double *__restrict__ w_s) {
-    return w_s != nullptr ? lane_score_impl<true>(row, n, lut_s, w_s)
-                          : lane_score_impl<false>(row, n, lut_s, w_s);
+    double res;
+    if (n < 8) {
+        res = 0.0;
+        for (int i = 0; i < n; ++i) res = __dadd_rn(res, __dmul_rn(w_s[i], lut_s[row[i]]));
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dmul_rn(w_s[j], lut_s[row[j]]);
+        const int n8 = n - (n & 7);
+        for (int i = 8; i < n8; i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], __dmul_rn(w_s[i + j], lut_s[row[i + j]]));
+        }
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (int i = n8; i < n; ++i) res = __dadd_rn(res, __dmul_rn(w_s[i], lut_s[row[i]]));
+    }
+    return __ddiv_rn(__dadd_rn(0.0, res), static_cast<double>(n));
 }
 
 // Per-warp deferred epilogue: 32 slot rows of c_q bytes.
@@ -220,7 +205,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     uint64_t *empty = full + kStages;
     uint8_t *slot_mem = reinterpret_cast<uint8_t *>(empty + kStages);
     double *lut_s = reinterpret_cast<double *>(slot_mem + NW * QS * SlotGeom<QPL>::kBytes);
-    double *w_s = weights != nullptr ? lut_s + (L + 1) : nullptr;
+    double *w_s = lut_s + (L + 1);  // m_q weights (1.0 when none); used only when m_q <= 128
     __shared__ int64_t bounds[2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,8 +226,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
-    if (w_s != nullptr)
-        for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = __ldg(weights + i);
+    for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = weights ? __ldg(weights + i) : 1.0;
     __syncthreads();
     const int64_t s_lo = bounds[0], s_hi = bounds[1];
     if (s_lo >= s_hi) return;
@@ -402,15 +386,14 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     uint64_t *bars = reinterpret_cast<uint64_t *>(after_bufs) + warp * kBufs;
     uint8_t *slot_mem = after_bufs + kCandWarps * kBufs * sizeof(uint64_t);
     double *lut_s = reinterpret_cast<double *>(slot_mem + kCandWarps * SlotGeom<QPL>::kBytes);
-    double *w_s = weights != nullptr ? lut_s + (L + 1) : nullptr;
+    double *w_s = lut_s + (L + 1);  // m_q weights (1.0 when none)
 
     if (lane == 0) {
         for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
-    if (w_s != nullptr)
-        for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = __ldg(weights + i);
+    for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = weights ? __ldg(weights + i) : 1.0;
     __syncthreads();
 
     const int64_t gw = static_cast<int64_t>(blockIdx.x) * kCandWarps + warp;
@@ -511,8 +494,7 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
                       const double *weights, double *scores, int64_t ld, uint16_t *mc,
                       int mc_stride, int mc_q0, cudaStream_t st) {
     constexpr int NW = 8;
-    const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1) * sizeof(double) +
-                        (weights != nullptr ? m_q * sizeof(double) : 0);
+    const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1 + m_q) * sizeof(double);
     auto kern = score_all_kernel<K, W, QPL, NW, QS>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t groups = (n_qsets + NW * QS - 1) / (NW * QS);
@@ -539,8 +521,7 @@ static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_s
                        const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
                        const double *weights, double *scores, uint16_t *mc, int mc_stride,
                        int mc_q0, cudaStream_t st) {
-    const size_t smem = cand_smem_static<QPL>() + (L + 1) * sizeof(double) +
-                        (weights != nullptr ? m_q * sizeof(double) : 0);
+    const size_t smem = cand_smem_static<QPL>() + (L + 1 + m_q) * sizeof(double);
     auto kern = score_cand_kernel<K, W, QPL>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
