@@ -136,14 +136,34 @@ __device__ __forceinline__ int mismatches(const uint32_t (&q)[K * W], const uint
     return mm;
 }
 
-// Process vectors [0, nv) of a shared-memory record array.
+// Process vectors [0, nv) of a shared-memory record array.  For W = 1 two
+// vectors share one 3-input min (VIMNMX3): 8 LOP3 + 0.5 min per (query,
+// vector) at C = 8 instead of 8 + 1; for W = 2 ptxas already fuses the
+// two-word add with the min (VIADDMNMX).
 template <int K, int W, int QPL>
 __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], int (&rmin)[QPL],
                                              const uint32_t *xs, int nv) {
     constexpr int R = ((K * W) + 3) & ~3;
     const uint4 *x4 = reinterpret_cast<const uint4 *>(xs);
+    int i = 0;
+    if constexpr (W == 1) {
+#pragma unroll 2
+        for (; i + 2 <= nv; i += 2) {
+            uint4 xa[R / 4], xb[R / 4];
+#pragma unroll
+            for (int u = 0; u < R / 4; ++u) {
+                xa[u] = x4[i * (R / 4) + u];
+                xb[u] = x4[(i + 1) * (R / 4) + u];
+            }
+            const uint32_t *a = reinterpret_cast<const uint32_t *>(xa);
+            const uint32_t *b = reinterpret_cast<const uint32_t *>(xb);
+#pragma unroll
+            for (int s = 0; s < QPL; ++s)
+                rmin[s] = __vimin3_s32(rmin[s], mismatches<K, W>(q[s], a), mismatches<K, W>(q[s], b));
+        }
+    }
 #pragma unroll 4
-    for (int i = 0; i < nv; ++i) {
+    for (; i < nv; ++i) {
         uint4 xv[R / 4];
 #pragma unroll
         for (int u = 0; u < R / 4; ++u) xv[u] = x4[i * (R / 4) + u];
