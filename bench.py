@@ -529,8 +529,9 @@ def run_cfg3(args):
                    "probe": probe, "k_filter": k_filter, "batch": 256, "top_k": top_k,
                    "setup_s": t_gen, "centroid_index_build_s": t_ci,
                    "postings": int(cindex.post_docs.shape[0])},
-        "batch1_latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
-                              "n": int(lat.size)},
+        "batch1_latency_ms": None if lat.size == 0 else {
+            "p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+            "n": int(lat.size)},
         "kernel_ms": {"prefilter": pf_ms, "score_candidates": sc_ms},
         "clocks": clk, "int_microbench": mb,
     }

@@ -11,8 +11,10 @@
 // chains into the same accumulator).  fp16/bf16 X is exact (the reference
 // hashes the same values cast to float64).
 //
-// Decomposition: the L tables split into column groups of <= 32 tables
-// (one plane word each, N_g = tables*C <= 256 MMA columns).  CTA c handles
+// Decomposition: the L tables split into column groups of 32 tables (one
+// plane word each, N_g = 32*C <= 256 MMA columns, plane-major: column
+// b*32 + t = bit b of table t, so one 32-column TMEM load is one plane word;
+// the planes are permuted into that order per call).  CTA c handles
 // group c % G for the 128-row tiles c/G, c/G + n_cta/G, ...  -- consecutive
 // CTAs share each X tile through L2.  Warp roles (192 threads):
 //   warp 0: TMA producer (3-stage ring of X tiles, planes loaded once),
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             for (int part = 0; part < PARTS; ++part)
                 for (int kb = 0; kb < 2; ++kb)
                     tma_load_2d(sb + (part * 2 + kb) * NP * 128, &map_w, kb * 64,
-                                part * (p.L * C) + prow, &bar_b);
+                                part * (p.groups * 32 * C) + prow, &bar_b);
             int it = 0;
             for (int64_t tile = cta_in_group; tile < n_tiles; tile += ctas_per_group, ++it) {
                 const int st = it % kHStages;
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const int L = p.L;
         const int t0 = group * 32;
         const int nt = min(32, L - t0);
-        const int ncols = nt * C;
+        const uint32_t tmask = nt == 32 ? 0xffffffffu : ((1u << nt) - 1u);
         const int W = (L + 31) >> 5, R = ((C * W) + 3) & ~3;
         int it = 0;
         for (int64_t tile = cta_in_group; tile < n_tiles; tile += ctas_per_group, ++it) {
@@ -134,25 +136,37 @@ __global__ void __launch_bounds__(kHThreads, 1)
 #pragma unroll
             for (int b = 0; b < C; ++b) plane[b] = 0;
             uint32_t codes_w[8];  // 32 tables x 8-bit codes
-#pragma unroll
-            for (int i = 0; i < 8; ++i) codes_w[i] = 0;
             uint32_t any_nonzero = 0;
             const uint32_t base = tmem + acc * 256 + (static_cast<uint32_t>(quarter * 32) << 16);
-            // 32 tables x C bits = C chunks of 32 columns; all indices static
+            // chunk b = plane word b (32 tables); sign bits gathered by funnel
+            // shifts of -D (MSB set iff D > 0 as an int, i.e. float D > +0)
+            bool want_zero = group == 0 && p.zero_rows != nullptr;
 #pragma unroll
-            for (int ch = 0; ch < C; ++ch) {
+            for (int b = 0; b < C; ++b) {
                 uint32_t r[32];
-                tmem_ld32(base + ch * 32, r);
+                tmem_ld32(base + b * 32, r);
                 tmem_wait_ld();
+                uint32_t pw = 0;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                                const int col = ch * 32 + j;
-                    const int t = col / C, b = col % C;
-                    const bool in = col < ncols;
-                    any_nonzero |= in ? (r[j] & 0x7fffffffu) : 0u;
-                    const uint32_t bit = (in && static_cast<int>(r[j]) > 0) ? 1u : 0u;  // +-0.0 -> 0
-                    codes_w[t >> 2] |= bit << (8 * (t & 3) + b);
-                    plane[b] |= bit << t;
+                for (int j = 31; j >= 0; --j) pw = __funnelshift_l(0u - r[j], pw, 1);
+                plane[b] = pw & tmask;
+                if (want_zero) {  // rows whose first word is all +-0 check every column (rare)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) any_nonzero |= r[j];
+                    if (b == 0) want_zero = __any_sync(0xffffffffu, (any_nonzero & 0x7fffffffu) == 0u);
+                }
+            }
+            any_nonzero &= 0x7fffffffu;
+            if (p.codes_out) {  // u8 codes: spread 4 plane bits into 4 bytes per step
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int b = 0; b < C; ++b) {
+                        const uint32_t y = (plane[b] >> (4 * k)) & 0xfu;
+                        w |= ((y * 0x00204081u) & 0x01010101u) << b;
+                    }
+                    codes_w[k] = w;
                 }
             }
             tc_fence_before();
@@ -191,6 +205,23 @@ template <int PARTS, int C, int STAGES>
 static int launch_hash_tc(const CUtensorMap &mx, const CUtensorMap &mw, const HashTcParams &hp,
                           uint32_t idesc, size_t smem, int ctas, cudaStream_t st);
 
+// reference plane order (row t*C + b per part) -> plane-major groups (row
+// g*32*C + b*32 + t), zero planes for tables >= L.  16-bit elements.
+__global__ void permute_planes_kernel(const uint16_t *__restrict__ src, int parts, int L, int C,
+                                      int groups, uint16_t *__restrict__ dst) {
+    const int64_t rows = static_cast<int64_t>(parts) * groups * 32 * C;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= rows * 128) return;
+    const int64_t row = i >> 7;
+    const int k = static_cast<int>(i & 127);
+    const int per_part = groups * 32 * C;
+    const int part = static_cast<int>(row / per_part);
+    const int rem = static_cast<int>(row % per_part);
+    const int g = rem / (32 * C), b = (rem % (32 * C)) / 32, t = rem % 32;
+    const int tg = g * 32 + t;
+    dst[i] = tg < L ? src[(static_cast<int64_t>(part) * L * C + tg * C + b) * 128 + k] : uint16_t(0);
+}
+
 static int launch_hash_tc_c(int C, int parts, int stages, const CUtensorMap &mx,
                             const CUtensorMap &mw, const HashTcParams &hp, uint32_t idesc,
                             size_t smem, int ctas, cudaStream_t st) {
@@ -221,16 +252,24 @@ int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, in
     DSRT_REQUIRE(C <= 8, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core hash needs C <= 8, got %d", C);
     DSRT_REQUIRE(n < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many rows for one call");
     const int groups = (L + 31) / 32;
-    int n_pad = ((tmin(32, L) * C) + 15) & ~15;
-    n_pad = tmax(n_pad, 16);
+    const int n_pad = 32 * C;  // plane-major group: 32 tables per plane word
     DSRT_REQUIRE(n_pad <= 256, DSRT_EUNSUPPORTED, "invalid parameter: MMA N too large");
     const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    const int64_t prow = static_cast<int64_t>(parts) * groups * 32 * C;
+    uint16_t *pp = nullptr;
+    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&pp), prow * 128 * sizeof(uint16_t), st));
+    permute_planes_kernel<<<static_cast<unsigned>((prow * 128 + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint16_t *>(planes), parts, L, C, groups, pp);
+    DSRT_LAUNCH_CHECK();
     CUtensorMap mx, mw;
     int rc = make_tmap_2d(&mx, X, dt, 128, static_cast<uint64_t>(n), 256, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc) return rc;
-    rc = make_tmap_2d(&mw, planes, dt, 128, static_cast<uint64_t>(parts) * L * C, 256, 64, n_pad,
-                      CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc) return rc;
+    if (rc == DSRT_OK)
+        rc = make_tmap_2d(&mw, pp, dt, 128, static_cast<uint64_t>(prow), 256, 64, n_pad,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) {
+        cudaFreeAsync(pp, st);
+        return rc;
+    }
     HashTcParams hp{n, L, C, groups, n_pad, parts, codes_out, records_out, zero_rows};
     const size_t b_bytes = static_cast<size_t>(parts) * 2 * n_pad * 128;
     const int stages = (1024 + 3 * 2 * 128 * 128 + b_bytes <= 227 * 1024) ? 3 : 2;
@@ -241,7 +280,9 @@ int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, in
     ctas = static_cast<int>(tmin<int64_t>(ctas, n_tiles * groups));
     ctas = tmax(ctas, groups);
     const uint32_t idesc = idesc_f16(128, n_pad, bf16, bf16);
-    return launch_hash_tc_c(C, parts, stages, mx, mw, hp, idesc, smem, ctas, st);
+    rc = launch_hash_tc_c(C, parts, stages, mx, mw, hp, idesc, smem, ctas, st);
+    cudaFreeAsync(pp, st);  // stream-ordered: freed after the kernel
+    return rc;
 }
 
 template <int PARTS, int C, int STAGES>
