@@ -34,6 +34,21 @@ METRIC = "set-pair scores/sec (cfg1: 100k sets x 1000 query sets, L=64 C=7, exha
 UNIT = "set-pairs/s"
 
 
+
+def _ncu_traffic(config: str, scale: float = 1.0):
+    """Per-launch DRAM bytes (read + write) of the dominant kernel from the committed
+    `ncu --set full` capture (profiles/r01_ncu_traffic.json), scaled to this launch."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)[config]
+    except (OSError, KeyError, ValueError):
+        return None, None
+    return rec["traffic_bytes"] * scale, {"source": "profiles/r01_ncu_traffic.json (" + rec["source"] + ")",
+                                          "captured_launch": rec["launch"],
+                                          "dram_read_bytes": rec["dram_read_bytes"] * scale,
+                                          "dram_write_bytes": rec["dram_write_bytes"] * scale}
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -297,10 +312,14 @@ def run_gpu(args):
     achieved = compares / (kern_ms * 1e-3)
     p_int = mb["lop3_ops_per_s"] * 4.0                            # 4 byte-compares / lane-op
     rec_bytes = total_vec * engine.record_words(L, C) * 4
+    traffic, traffic_src = _ncu_traffic("cfg1", n_sets / 100_000 * n_q / 1000)
+    alg_bytes = rec_bytes + n_q * n_sets * 8 + n_q * m_q * engine.record_words(L, C) * 4
     roofline = {
         "bound": "int", "unit": "Gcompare/s", "achieved": achieved / 1e9, "peak": p_int / 1e9,
-        "frac": achieved / p_int, "traffic": None,
-        "kernel": "score_all_kernel<7,2,1,8>", "kernel_ms": kern_ms,
+        "frac": achieved / p_int, "traffic": traffic,
+        "traffic_detail": dict(traffic_src or {}, algorithmic_bytes=alg_bytes,
+                               ratio=None if traffic is None else traffic / alg_bytes),
+        "kernel": "score_all_kernel<7,2,1,8,2>", "kernel_ms": kern_ms,
         "per_launch": {"compares": compares, "code_bytes": rec_bytes,
                        "hbm_floor_ms": rec_bytes / 6456.2e9 * 1e3},
         "peak_source": "measured on this GPU in-run: LOP3 lane-ops/s x 4 (dsrt_microbench_int)",
@@ -426,6 +445,9 @@ def run_cfg4(args):
     achieved = compares / (k_ms * 1e-3)
     value = n_q * n_sets / (ms * 1e-3)
     rec_bytes = total_vec * engine.record_words(L, C) * 4
+    per_launch_sets = min(n_sets, chunk)
+    traffic4, traffic4_src = _ncu_traffic("cfg4", per_launch_sets / 1_000_000 * n_q / 1024)
+    alg4 = rec_bytes * per_launch_sets / n_sets + n_q * per_launch_sets * 8
     line = {
         "metric": "set-pair scores/sec (cfg4: 8M sets x 1024 query sets, L=32 C=8, exhaustive, top-1000)",
         "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -435,8 +457,11 @@ def run_cfg4(args):
                    "top_k": top_k, "vectors": total_vec, "score_chunk_sets": chunk,
                    "l2": "inputs larger than L2 (17.9 GB records)", "generation_s": t_gen},
         "roofline": {"bound": "int", "unit": "Gcompare/s", "achieved": achieved / 1e9,
-                     "peak": p_int / 1e9, "frac": achieved / p_int, "traffic": None,
-                     "kernel": "score_all_kernel<8,1,1,8>", "kernel_ms_per_step": k_ms,
+                     "peak": p_int / 1e9, "frac": achieved / p_int, "traffic": traffic4,
+                     "traffic_detail": dict(traffic4_src or {}, per="one 1M-set launch",
+                                            algorithmic_bytes=alg4,
+                                            ratio=None if traffic4 is None else traffic4 / alg4),
+                     "kernel": "score_all_kernel<8,1,1,8,4>", "kernel_ms_per_step": k_ms,
                      "launches_per_step": launches_per_step,
                      "per_step": {"compares": compares, "code_bytes_per_pass": rec_bytes},
                      "achieved_hbm_gbs_code_stream": rec_bytes / (k_ms * 1e-3) / 1e9,
@@ -601,6 +626,7 @@ def run_cfg2(args):
     alg_flops = 2.0 * 128 * L * C * n_vec
     mma_flops = 2 * alg_flops  # hi/lo planes: two MMA chains
     hbm_bytes = n_vec * (128 * 2 + L + engine.record_words(L, C) * 4)
+    traffic2, traffic2_src = _ncu_traffic("cfg2", n_vec / 4_000_000)
     line = {
         "metric": "index-build vectors/sec (cfg2: 10M bf16 vectors, L=64 C=7, hash + CSR layout)",
         "value": n_vec / (ms * 1e-3), "unit": "vectors/s", "n_gpus": 1, "steps": args.steps,
@@ -617,7 +643,10 @@ def run_cfg2(args):
                      "mma_frac": mma_flops / (k_ms * 1e-3) / 1e12 / peaks["bf16_tflops"],
                      "hbm_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9,
                      "hbm_frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                     "traffic": None,
+                     "traffic": traffic2,
+                     "traffic_detail": dict(traffic2_src or {}, algorithmic_bytes=hbm_bytes,
+                                            ratio=None if traffic2 is None else traffic2 / hbm_bytes,
+                                            note="X tiles are read by both 32-table groups' CTAs"),
                      "algorithmic": "2*d*L*C flops per vector; bytes 2d in + L codes + 4R records out",
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst), hbm_gbs"},
         "hash_bit_flips": {"sample_vectors": int(len(samp)), "bits": int(flips.size),
