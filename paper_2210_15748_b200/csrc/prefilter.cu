@@ -447,16 +447,22 @@ static PrefilterWs ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, 
 
 // ====================================================================
 // Tensor-core screen (exact results): sims ~ fp16(q/|q|) . fp16(c*s) on
-// tcgen05.  Pass 0 finds each row's P-th best approx value A_P; every
-// centroid with approx >= A_P - 2 eps (pass 1, a second cheap GEMM sweep) is
-// re-ranked in float64 -- that set provably contains the exact top-P, ties
-// included; rows with more than kCandMax such centroids fall back to the
-// exact float64 scan.  eps bounds |approx - exact| for unit-bounded rows:
+// tcgen05.  Pass 0 finds a lower bound A'_P <= A_P of each row's P-th best
+// approx value: the P-th best of the 32-column chunk maxima (P real values of
+// the row; one insertion per chunk instead of per value).  Every centroid with
+// approx >= A'_P - 2 eps (pass 1, a second cheap GEMM sweep) is re-ranked in
+// float64 -- that set provably contains the exact top-P, ties included; rows
+// with more than kCandMax such centroids fall back to the exact float64 scan.  eps bounds |approx - exact| for unit-bounded rows:
 // fp16 operand rounding 2u(1+u) with u = 2^-11 plus fp32 accumulation.
 // ====================================================================
 constexpr int kSN = 128;         // centroids per N-tile
-constexpr int kSStages = 4;
-constexpr int kSThreads = 192;
+#ifndef DSRT_SSTAGES
+#define DSRT_SSTAGES 4
+#endif
+constexpr int kSStages = DSRT_SSTAGES;
+constexpr int kSEpi = 8;                     // epilogue warps: 2 per TMEM lane quarter
+constexpr int kSThreads = 64 + 32 * kSEpi;   // + TMA producer warp + MMA warp
+constexpr int kSHalves = kSEpi / 4;          // column halves of a tile per lane quarter
 constexpr double kScreenEps = 1.2e-3;
 
 struct ScreenCand {
@@ -535,7 +541,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], kSEpi);
         }
         mbar_init(&bar_a, 1);
         fence_mbar_init();
@@ -580,7 +586,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
             }
         }
     } else {
-        const int quarter = warp & 3;
+        const int quarter = warp & 3;                // TMEM lanes 32*quarter .. +31
+        const int half = (warp - 2) / 4;             // which column slice of each tile
         const int64_t row = m0 + quarter * 32 + lane;
         const bool row_ok = row < n_rows;
         float tv[PT];
@@ -597,7 +604,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
             const int64_t id0 = t * kSN;
             const bool full_tile = id0 + kSN <= k_c;
 #pragma unroll 1
-            for (int c0 = 0; c0 < kSN; c0 += 32) {
+            for (int c0 = half * (kSN / kSHalves); c0 < (half + 1) * (kSN / kSHalves); c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(base + c0, r);
                 tmem_wait_ld();
@@ -617,22 +624,22 @@ __global__ void __launch_bounds__(kSThreads, 1)
                     for (int j = 0; j < w; ++j) m16[j] = fmaxf(m16[j], m16[j + w]);
                 const float cmax = m16[0];
                 if (PASS == 0) {
+                    // top-P of the chunk maxima: P real values of the row, so their
+                    // P-th best A'_P <= A_P and theta' = A'_P - 2 eps keeps pass 1 a
+                    // superset of the exact top-P (one insertion per chunk, not 32)
                     if (__any_sync(0xffffffffu, cmax > worst)) {
+                        float x = cmax;
+                        if (x > worst) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            float x = __uint_as_float(r[j]);
-                            if (x > worst) {  // branch-free insertion into the sorted list
-#pragma unroll
-                                for (int q = 0; q < PT; ++q) {
-                                    const float hi = fmaxf(tv[q], x);
-                                    x = fminf(tv[q], x);
-                                    tv[q] = hi;
-                                }
-                                worst = tv[0];
-#pragma unroll
-                                for (int q = 1; q < PT; ++q)
-                                    if (q < P) worst = tv[q];
+                            for (int q = 0; q < PT; ++q) {
+                                const float hi = fmaxf(tv[q], x);
+                                x = fminf(tv[q], x);
+                                tv[q] = hi;
                             }
+                            worst = tv[0];
+#pragma unroll
+                            for (int q = 1; q < PT; ++q)
+                                if (q < P) worst = tv[q];
                         }
                     }
                 } else {
@@ -654,7 +661,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         if (PASS == 0 && row_ok) {
-            float *o = out_vals + (row * gridDim.y + blockIdx.y) * kMaxPtc;
+            // one partial list per (split, column half): n_split * kSHalves lists per row
+            float *o = out_vals + ((row * gridDim.y + blockIdx.y) * kSHalves + half) * kMaxPtc;
 #pragma unroll
             for (int j = 0; j < kMaxPtc; ++j) o[j] = j < PT ? tv[j < PT ? j : 0] : -INFINITY;
         }
@@ -867,7 +875,7 @@ static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int 
     w.n_split = (n_tiles + w.tiles_per_split - 1) / w.tiles_per_split;
     w.row_words = row_words_for(n_docs, m_q * P);
     w.q16 = align256(static_cast<size_t>(m_tiles * 128) * 128 * 2);
-    w.screen = align256(static_cast<size_t>(rows) * w.n_split * kMaxPtc * sizeof(float));
+    w.screen = align256(static_cast<size_t>(rows) * w.n_split * kSHalves * kMaxPtc * sizeof(float));
     w.theta = align256(static_cast<size_t>(rows) * sizeof(float));
     w.lists = align256(static_cast<size_t>(rows) * kCandMax * sizeof(ScreenCand));
     w.listn = align256(static_cast<size_t>(rows) * sizeof(int32_t));
@@ -936,7 +944,7 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     if (rc) return rc;
     // eps in normalised units (|q^| = 1, |c*s| <= 1)
     pf_theta_kernel<double><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
-        vals, static_cast<int>(w.n_split), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn,
+        vals, static_cast<int>(w.n_split * kSHalves), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn,
         nullptr, d);
     rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
                              listn, idesc);
@@ -968,7 +976,7 @@ static size_t assign_ws_layout(int64_t n, size_t *parts) {
     const int64_t ch = tmin<int64_t>(n, kAssignChunk);
     const int64_t tiles = (ch + 127) / 128;
     parts[0] = align256(static_cast<size_t>(tiles * 128) * 128 * 2);        // q16 staging
-    parts[1] = align256(static_cast<size_t>(ch) * kMaxPtc * sizeof(float));  // pass-0 values (1 split)
+    parts[1] = align256(static_cast<size_t>(ch) * kSHalves * kMaxPtc * sizeof(float));  // pass-0 values (1 split)
     parts[2] = align256(static_cast<size_t>(ch) * sizeof(float));            // theta
     parts[3] = align256(static_cast<size_t>(ch) * kCandMax * sizeof(ScreenCand));
     parts[4] = align256(static_cast<size_t>(ch) * sizeof(int32_t));          // list counts
@@ -1021,13 +1029,13 @@ static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const
         float *v = vals;
         float *vtmp = nullptr;
         if (n_split > 1) {
-            DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&vtmp), rows * n_split * kMaxPtc * sizeof(float), st));
+            DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&vtmp), rows * n_split * kSHalves * kMaxPtc * sizeof(float), st));
             v = vtmp;
         }
         rc = launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, v, nullptr, nullptr, nullptr, idesc);
         if (rc) return rc;
         pf_theta_kernel<TQ><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
-            v, static_cast<int>(n_split), rows, 1, static_cast<float>(2.0 * eps), theta, listn,
+            v, static_cast<int>(n_split * kSHalves), rows, 1, static_cast<float>(2.0 * eps), theta, listn,
             raw ? X + r0 * d : nullptr, d);
         rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, nullptr, theta, lists, listn, idesc);
         if (rc) return rc;
