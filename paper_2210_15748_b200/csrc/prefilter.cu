@@ -251,22 +251,50 @@ __global__ void __launch_bounds__(kSelThreads)
     };
     const int64_t per_step = static_cast<int64_t>(blockDim.x) * G;
     uint32_t *myh = whist + warp * kSelBins;
+    // counts 1..3 (the bulk of the touched docs) are counted with SIMD byte /
+    // half-word compares in registers; only counts >= 4 use shared atomics
+    constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
+    uint32_t h1 = 0, h2 = 0, h3 = 0;
     for (int64_t base = 0; base < n_groups; base += per_step) {
         const int64_t g0 = base + static_cast<int64_t>(tid) * G;
         uint32_t w[4 * G];
         load_groups(g0, w);  // rows are zero-padded past n_docs: no bounds checks
 #pragma unroll
         for (int q = 0; q < 4 * G; ++q) {
-            if (w[q] == 0u) continue;  // most words hold no touched doc
+            const uint32_t x = w[q];
+            if (x == 0u) continue;  // most words hold no touched doc
+            if (CB == 8) {
+                h1 += __popc(__vcmpeq4(x, ONE) & ONE);
+                h2 += __popc(__vcmpeq4(x, 2 * ONE) & ONE);
+                h3 += __popc(__vcmpeq4(x, 3 * ONE) & ONE);
+                if (__vcmpgeu4(x, 4 * ONE) == 0u) continue;
+            } else {
+                h1 += __popc(__vcmpeq2(x, ONE) & ONE);
+                h2 += __popc(__vcmpeq2(x, 2 * ONE) & ONE);
+                h3 += __popc(__vcmpeq2(x, 3 * ONE) & ONE);
+                if (__vcmpgeu2(x, 4 * ONE) == 0u) continue;
+            }
 #pragma unroll
             for (int k = 0; k < DPW; ++k) {
-                const uint32_t c = (w[q] >> (CB * k)) & MASK;
-                if (c != 0) {
+                const uint32_t c = (x >> (CB * k)) & MASK;
+                if (c >= 4) {
                     if (small_bins) atomicAdd(&myh[c], 1u);
                     else atomicAdd(&hist[tmin<uint32_t>(c, static_cast<uint32_t>(max_count))], 1u);
                 }
             }
         }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+        h3 += __shfl_xor_sync(0xffffffffu, h3, o);
+    }
+    if (lane == 0) {
+        uint32_t *dst = small_bins ? myh : hist;
+        if (max_count >= 1) atomicAdd(&dst[1], h1);
+        if (max_count >= 2) atomicAdd(&dst[2], h2);
+        if (max_count >= 3) atomicAdd(&dst[3], h3);
     }
     __syncthreads();
     if (small_bins)
