@@ -241,15 +241,24 @@ int dsrt_varints_to_postings(const uint8_t *bytes, int64_t n_bytes, int64_t k, i
 /*
  * K6 -- centroid assignment for build_centroid_index (prefilter.py:85-108):
  * assign[i] = argmax_c <X[i], centroids[c]> (lowest c on ties, as np.argmax),
- * exact: tensor-core screen + float64 re-rank + exact fallback.  X of
- * x_dtype (fp16/bf16 rows are read in place; f32/f64 are normalised into an
- * fp16 staging buffer); cents_lp = fp16 (bf16 for bf16 X) copy of
- * centroids / max_c |c|.  d = 128.
+ * exact.  d = 128: tensor-core screen + float64 re-rank + exact fallback (X
+ * of x_dtype: fp16/bf16 rows are read in place; f32/f64 are normalised into
+ * an fp16 staging buffer; cents_lp = fp16 (bf16 for bf16 X) copy of
+ * centroids / max_c |c|).  Other d (<= 1024): float64 unit rows in numpy's
+ * order and a sequential-FMA SIMT scan (cents_lp unused); zero rows -> EINVAL.
  */
 int dsrt_assign_centroids(const void *X, int x_dtype, int64_t n, int d, const double *centroids,
                           const void *cents_lp, int64_t k_c, int32_t *assign_out, void *workspace,
                           size_t workspace_bytes, void *stream);
-size_t dsrt_assign_centroids_workspace(int64_t n, int64_t k_c);
+size_t dsrt_assign_centroids_workspace(int64_t n, int d, int64_t k_c);
+/*
+ * Append postings of new documents (ids all >= those of the old postings) to
+ * an existing CSR: posting c = old posting c followed by added posting c.
+ * new_off (k_c + 1), new_docs (old_total + add_total).
+ */
+int dsrt_merge_postings(const int64_t *old_off, const int64_t *old_docs, const int64_t *add_off,
+                        const int64_t *add_docs, int64_t k_c, int64_t *new_off, int64_t *new_docs,
+                        void *stream);
 /*
  * Postings from assignments: vectors grouped by document (set_off, N+1);
  * post_off (k_c + 1), post_docs (capacity n_vec), *n_post (device int64):

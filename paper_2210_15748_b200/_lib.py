@@ -66,7 +66,8 @@ SIGNATURES = {
     "dsrt_to_f16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),
     "dsrt_to_bf16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),
     "dsrt_assign_centroids": (_i32, [_vp, _i32, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
-    "dsrt_assign_centroids_workspace": (_sz, [_i64, _i64]),
+    "dsrt_assign_centroids_workspace": (_sz, [_i64, _i32, _i64]),
+    "dsrt_merge_postings": (_i32, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "dsrt_postings_from_assign": (_i32, [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dsrt_postings_workspace": (_sz, [_i64, _i64]),
     "dsrt_tinytable": (_i32, [_vp, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),

@@ -16,6 +16,9 @@
 // Members of a centroid are found with the stable counting sort of K2, so
 // the per-centroid sums run sequentially in sample order (no atomics: the
 // result is deterministic, unlike a scatter-add).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cmath>
 
 #include "common.cuh"
@@ -24,7 +27,7 @@ extern "C" int dsrt_counting_sort(const int64_t *set_of_vec, int64_t n, int64_t 
                                   int64_t *set_off_out, int64_t *perm_out, void *workspace,
                                   size_t ws_bytes, void *stream);
 extern "C" size_t dsrt_counting_sort_workspace(int64_t n, int64_t n_sets);
-extern "C" size_t dsrt_assign_centroids_workspace(int64_t n, int64_t k_c);
+extern "C" size_t dsrt_assign_centroids_workspace(int64_t n, int d, int64_t k_c);
 extern "C" int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scale, void *dst,
                                 void *stream);
 
@@ -73,16 +76,23 @@ __device__ __forceinline__ double row_norm(const double *a, int n) {
     return __dsqrt_rn(__dadd_rn(0.0, pw_sq(a, n, 1)));
 }
 
-// _unit_rows (prefilter.py:37-44): X / norm, zero rows flagged
-__global__ void km_unit_rows_kernel(const double *__restrict__ X, int64_t n, int d,
+__device__ __forceinline__ double km_f64(double v) { return v; }
+__device__ __forceinline__ double km_f64(float v) { return static_cast<double>(v); }
+__device__ __forceinline__ double km_f64(__half v) { return static_cast<double>(__half2float(v)); }
+__device__ __forceinline__ double km_f64(__nv_bfloat16 v) { return static_cast<double>(__bfloat162float(v)); }
+
+// _unit_rows (prefilter.py:37-44): rows as float64 (exact for every input
+// dtype), X / norm in numpy's order; zero rows flagged
+template <typename TQ>
+__global__ void km_unit_rows_kernel(const TQ *__restrict__ X, int64_t n, int d,
                                     double *__restrict__ out, uint32_t *__restrict__ zero) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
-    const double *x = X + i * d;
-    const double nrm = row_norm(x, d);
-    if (nrm == 0.0) atomicOr(zero, 1u);
     double *o = out + i * d;
-    for (int k = 0; k < d; ++k) o[k] = __ddiv_rn(x[k], nrm);
+    for (int k = 0; k < d; ++k) o[k] = km_f64(X[i * d + k]);
+    const double nrm = row_norm(o, d);
+    if (nrm == 0.0) atomicOr(zero, 1u);
+    for (int k = 0; k < d; ++k) o[k] = __ddiv_rn(o[k], nrm);
 }
 
 __global__ void km_gather_rows_kernel(const double *__restrict__ X, const int64_t *__restrict__ idx,
@@ -180,6 +190,49 @@ __global__ void km_divide_kernel(const double *__restrict__ sums, const double *
     cents[i] = __ddiv_rn(sums[i], norms[i / d]);
 }
 
+// Exact assignment for any d <= kKmMaxD (K6 for d != 128): unit rows in
+// numpy's order, sequential FMA dots, np.argmax's first-index rule.  Rows go
+// in chunks of kKmChunk through a float64 staging buffer (ws: kKmChunk*d*8
+// bytes + 64).  Zero rows are reported through *zero_rows (host).
+constexpr int64_t kKmChunk = 1 << 18;
+size_t assign_simt_ws(int64_t n, int d) {
+    return static_cast<size_t>(tmin<int64_t>(tmax<int64_t>(n, 1), kKmChunk)) * d * 8 + 256;
+}
+int assign_simt(const void *X, int dtype, int64_t n, int d, const double *cents, int64_t k,
+                int32_t *assign, void *ws, cudaStream_t st) {
+    DSRT_REQUIRE(d >= 1 && d <= kKmMaxD, DSRT_EUNSUPPORTED, "invalid parameter: d=%d > %d", d, kKmMaxD);
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    uint32_t *zero = reinterpret_cast<uint32_t *>(w);
+    double *xu = reinterpret_cast<double *>(w + 256);
+    double *best = nullptr;
+    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&best), tmin<int64_t>(n, kKmChunk) * 8, st));
+    DSRT_CUDA(cudaMemsetAsync(zero, 0, 4, st));
+    const size_t smem = 4 * static_cast<size_t>(d) * 8;
+    for (int64_t r0 = 0; r0 < n; r0 += kKmChunk) {
+        const int64_t rows = tmin<int64_t>(kKmChunk, n - r0);
+        const unsigned nb = static_cast<unsigned>((rows + 127) / 128);
+        switch (dtype) {
+            case DSRT_F64: km_unit_rows_kernel<double><<<nb, 128, 0, st>>>(static_cast<const double *>(X) + r0 * d, rows, d, xu, zero); break;
+            case DSRT_F32: km_unit_rows_kernel<float><<<nb, 128, 0, st>>>(static_cast<const float *>(X) + r0 * d, rows, d, xu, zero); break;
+            case DSRT_F16: km_unit_rows_kernel<__half><<<nb, 128, 0, st>>>(static_cast<const __half *>(X) + r0 * d, rows, d, xu, zero); break;
+            case DSRT_BF16: km_unit_rows_kernel<__nv_bfloat16><<<nb, 128, 0, st>>>(static_cast<const __nv_bfloat16 *>(X) + r0 * d, rows, d, xu, zero); break;
+            default:
+                cudaFreeAsync(best, st);
+                set_error("invalid parameter: x dtype %d", dtype);
+                return DSRT_EINVAL;
+        }
+        km_assign_simt_kernel<<<static_cast<unsigned>((rows + 3) / 4), 128, smem, st>>>(
+            xu, rows, d, cents, k, assign + r0, best);
+        DSRT_LAUNCH_CHECK();
+    }
+    cudaFreeAsync(best, st);
+    uint32_t hz = 0;
+    DSRT_CUDA(cudaMemcpyAsync(&hz, zero, 4, cudaMemcpyDeviceToHost, st));
+    DSRT_CUDA(cudaStreamSynchronize(st));
+    DSRT_REQUIRE(hz == 0, DSRT_EINVAL, "zero vector in documents: cannot assign to a centroid");
+    return DSRT_OK;
+}
+
 struct KmLayout {
     size_t xu, assign, best, keys, off, perm, sums, norms, dead, rank, c16, misc, sort, aws, rws, sws;
     size_t total;
@@ -206,7 +259,7 @@ static KmLayout km_layout(int64_t n, int d, int64_t k) {
     L.c16 = take(static_cast<size_t>(k) * d * 2);
     L.misc = take(64);
     L.sort = take(dsrt_counting_sort_workspace(n, k));
-    L.aws = take(d == 128 ? dsrt_assign_centroids_workspace(n, k) : 0);
+    L.aws = take(d == 128 ? dsrt_assign_centroids_workspace(n, d, k) : 0);
     L.rws = take(radix_sort_ws(n));
     L.sws = take(scan_ws_bytes(k + 1));
     L.total = o;
@@ -250,7 +303,7 @@ extern "C" int dsrt_train_centroids(const double *samples, int64_t n, int d, int
 
     DSRT_CUDA(cudaMemsetAsync(w + L.misc, 0, 64, st));
     const unsigned nb = static_cast<unsigned>((n + 127) / 128);
-    km_unit_rows_kernel<<<nb, 128, 0, st>>>(samples, n, d, xu, zero);
+    km_unit_rows_kernel<double><<<nb, 128, 0, st>>>(samples, n, d, xu, zero);
     DSRT_LAUNCH_CHECK();
     uint32_t hz = 0;
     DSRT_CUDA(cudaMemcpyAsync(&hz, zero, 4, cudaMemcpyDeviceToHost, st));

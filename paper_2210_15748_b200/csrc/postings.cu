@@ -63,9 +63,35 @@ __global__ void compact_kernel(const int64_t *__restrict__ perm, const int64_t *
 
 static size_t al(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
+// block per centroid: old posting, then the added one (add ids > old ids)
+__global__ void merge_postings_kernel(const int64_t *__restrict__ old_off, const int64_t *__restrict__ old_docs,
+                                      const int64_t *__restrict__ add_off, const int64_t *__restrict__ add_docs,
+                                      int64_t k_c, int64_t *__restrict__ new_off, int64_t *__restrict__ new_docs) {
+    const int64_t c = blockIdx.x;
+    if (c >= k_c) return;
+    const int64_t o0 = old_off[c], o1 = old_off[c + 1], a0 = add_off[c], a1 = add_off[c + 1];
+    const int64_t dst = o0 + a0;  // (old start) + (added start) = merged start
+    if (threadIdx.x == 0) {
+        new_off[c] = dst;
+        if (c == k_c - 1) new_off[k_c] = o1 + a1;
+    }
+    for (int64_t i = threadIdx.x; i < o1 - o0; i += blockDim.x) new_docs[dst + i] = old_docs[o0 + i];
+    for (int64_t i = threadIdx.x; i < a1 - a0; i += blockDim.x) new_docs[dst + (o1 - o0) + i] = add_docs[a0 + i];
+}
+
 }  // namespace dsrt
 
 using namespace dsrt;
+
+extern "C" int dsrt_merge_postings(const int64_t *old_off, const int64_t *old_docs, const int64_t *add_off,
+                                   const int64_t *add_docs, int64_t k_c, int64_t *new_off, int64_t *new_docs,
+                                   void *stream) {
+    DSRT_REQUIRE(k_c >= 1 && k_c < (1LL << 31), DSRT_EINVAL, "invalid parameter: k=%lld", (long long)k_c);
+    merge_postings_kernel<<<static_cast<unsigned>(k_c), 128, 0, as_stream(stream)>>>(
+        old_off, old_docs, add_off, add_docs, k_c, new_off, new_docs);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
 
 extern "C" size_t dsrt_postings_workspace(int64_t n_vec, int64_t k_c) {
     const size_t n8 = al(static_cast<size_t>(n_vec + 1) * 8);

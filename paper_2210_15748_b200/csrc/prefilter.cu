@@ -1078,6 +1078,10 @@ static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const
     }
     return DSRT_OK;
 }
+size_t assign_simt_ws(int64_t n, int d);
+int assign_simt(const void *X, int dtype, int64_t n, int d, const double *cents, int64_t k,
+                int32_t *assign, void *ws, cudaStream_t st);
+
 // k-means assignment step: float64 unit rows, exact argmax and its similarity.
 int assign_unit_rows_f64(const double *X, int64_t n, const double *cents, const void *cents_f16,
                          int64_t k_c, int32_t *assign_out, double *best, void *ws, cudaStream_t st) {
@@ -1086,21 +1090,22 @@ int assign_unit_rows_f64(const double *X, int64_t n, const double *cents, const 
 
 }  // namespace dsrt
 
-extern "C" size_t dsrt_assign_centroids_workspace(int64_t n, int64_t k_c) {
+extern "C" size_t dsrt_assign_centroids_workspace(int64_t n, int d, int64_t k_c) {
     size_t parts[6];
     (void)k_c;
+    if (d != 128) return assign_simt_ws(n, d);
     return assign_ws_layout(tmax<int64_t>(n, 1), parts);
 }
 
 extern "C" int dsrt_assign_centroids(const void *X, int x_dtype, int64_t n, int d, const double *cents,
                                      const void *cents_lp, int64_t k_c, int32_t *assign_out,
                                      void *workspace, size_t ws_bytes, void *stream) {
-    DSRT_REQUIRE(d == 128, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core assignment needs d=128");
     DSRT_REQUIRE(k_c >= 1 && k_c < (1LL << 31), DSRT_EINVAL, "invalid parameter: k=%lld", (long long)k_c);
-    DSRT_REQUIRE(ws_bytes >= dsrt_assign_centroids_workspace(n, k_c), DSRT_EINVAL,
+    DSRT_REQUIRE(ws_bytes >= dsrt_assign_centroids_workspace(n, d, k_c), DSRT_EINVAL,
                  "invalid parameter: assignment workspace too small");
     if (n == 0) return DSRT_OK;
     cudaStream_t st = as_stream(stream);
+    if (d != 128) return assign_simt(X, x_dtype, n, d, cents, k_c, assign_out, workspace, st);
     switch (x_dtype) {
         case DSRT_F16: return assign_impl<__half>(static_cast<const __half *>(X), n, d, cents, cents_lp, k_c, true, false, assign_out, workspace, st);
         case DSRT_BF16: return assign_impl<__nv_bfloat16>(static_cast<const __nv_bfloat16 *>(X), n, d, cents, cents_lp, k_c, true, true, assign_out, workspace, st);

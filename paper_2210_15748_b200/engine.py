@@ -299,15 +299,15 @@ def to_bf16_rows(src: torch.Tensor, scale: float) -> torch.Tensor:
     return dst
 
 
-def assign_centroids(X: torch.Tensor, centroids: torch.Tensor, cents_lp: torch.Tensor):
-    """Exact argmax centroid per row of X (n, 128) -> int32 (n,)."""
+def assign_centroids(X: torch.Tensor, centroids: torch.Tensor, cents_lp: torch.Tensor | None):
+    """Exact argmax centroid per row of X (n, d) -> int32 (n,); cents_lp only for d = 128."""
     if X.dtype not in _DT:
         raise ValueError(f"invalid parameter: unsupported vector dtype {X.dtype}")
     X = X.contiguous()
     _need(centroids, torch.float64, "centroids")
     n, d = X.shape
     out = torch.empty(n, dtype=torch.int32, device=X.device)
-    ws_bytes = _lib.lib().dsrt_assign_centroids_workspace(n, centroids.shape[0])
+    ws_bytes = _lib.lib().dsrt_assign_centroids_workspace(n, d, centroids.shape[0])
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=X.device)
     _lib.call("dsrt_assign_centroids", _ptr(X), _DT[X.dtype], n, d, _ptr(centroids),
               _ptr(cents_lp), centroids.shape[0], _ptr(out), _ptr(ws), ws_bytes, _stream())
@@ -329,6 +329,21 @@ def postings_from_assign(assign: torch.Tensor, set_off: torch.Tensor, n_docs: in
     return post_off, post_docs[: int(n_post.item())].clone()
 
 
+def merge_postings(old_off: torch.Tensor, old_docs: torch.Tensor, add_off: torch.Tensor,
+                   add_docs: torch.Tensor):
+    """Posting c = old posting c + added posting c (added doc ids all newer)."""
+    for t, name in ((old_off, "old_off"), (old_docs, "old_docs"), (add_off, "add_off"),
+                    (add_docs, "add_docs")):
+        _need(t, torch.int64, name)
+    k = old_off.shape[0] - 1
+    new_off = torch.empty(k + 1, dtype=torch.int64, device=old_off.device)
+    new_docs = torch.empty(old_docs.shape[0] + add_docs.shape[0], dtype=torch.int64,
+                           device=old_off.device)
+    _lib.call("dsrt_merge_postings", _ptr(old_off), _ptr(old_docs), _ptr(add_off), _ptr(add_docs),
+              k, _ptr(new_off), _ptr(new_docs), _stream())
+    return new_off, new_docs
+
+
 def microbench_int() -> dict:
     out = (ctypes.c_double * 4)()
     _lib.call("dsrt_microbench_int", out, _stream())
@@ -336,5 +351,3 @@ def microbench_int() -> dict:
             "mix_compares_per_s": out[3]}
 
 
-def as_numpy(t: torch.Tensor) -> np.ndarray:
-    return t.detach().cpu().numpy()

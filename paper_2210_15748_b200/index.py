@@ -292,12 +292,6 @@ def add_sets(index: DessertIndex, docs) -> DessertIndex:
 
 
 # --------------------------------------------------------------------- query
-def _query_records(index: DessertIndex, Q) -> tuple[torch.Tensor, int]:
-    t = to_device_matrix(Q, index.config.d, index.device)
-    _, recs = hash_device(index.family, t, want_codes=False)
-    return recs, t.shape[0]
-
-
 def _rank(scores: torch.Tensor, top_k: int, ids: torch.Tensor, n_valid=None):
     """Row-wise (score desc, doc_id asc) top-k on the device."""
     rows, n = scores.shape

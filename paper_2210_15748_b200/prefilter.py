@@ -77,16 +77,6 @@ class CentroidIndex:
         return [docs[off[c]:off[c + 1]] for c in range(len(off) - 1)]
 
 
-def _unit_rows_dev(X: torch.Tensor, name: str) -> torch.Tensor:
-    X = X.to(torch.float64)
-    if X.dim() != 2 or X.shape[0] == 0:
-        raise ValueError(f"{name} must be a non-empty (n, d) matrix, got shape {tuple(X.shape)}")
-    norms = torch.linalg.norm(X, dim=1, keepdim=True)
-    if bool((norms == 0).any()):
-        raise ValueError(f"zero vector in {name}: cannot assign to a centroid")
-    return X / norms
-
-
 def _as_dev(X, device="cuda") -> torch.Tensor:
     if isinstance(X, torch.Tensor):
         return X.to(device)
@@ -110,26 +100,6 @@ def train_centroids(samples, k: int, iters: int, seed: int, device="cuda") -> Ce
         init = np.random.default_rng(seed).choice(n, size=k, replace=False)
     cents = engine.train_centroids(X, k, iters, init)
     return Centroids(k=k, seed=seed, vectors=cents.cpu().numpy())
-
-
-def _postings_from_assign(doc_of: torch.Tensor, assign: torch.Tensor, k: int, n_docs: int):
-    key = assign * n_docs + doc_of           # (centroid, doc) pairs, deduplicated
-    key = torch.unique(key)                  # sorted: by centroid, then doc ascending
-    cent = key // n_docs
-    docs = key % n_docs
-    counts = torch.bincount(cent, minlength=k)
-    off = torch.zeros(k + 1, dtype=torch.int64, device=key.device)
-    off[1:] = torch.cumsum(counts, 0)
-    return off, docs.contiguous()
-
-
-def _assign(X: torch.Tensor, cvec: torch.Tensor) -> torch.Tensor:
-    n = X.shape[0]
-    out = torch.empty(n, dtype=torch.int64, device=X.device)
-    step = max(1, (1 << 28) // max(1, cvec.shape[0]))
-    for lo in range(0, n, step):
-        out[lo:lo + step] = torch.argmax(X[lo:lo + step] @ cvec.T, dim=1)
-    return out
 
 
 def _check_nonzero_rows(X: torch.Tensor, off: torch.Tensor, chunk: int = 1 << 22) -> None:
@@ -170,68 +140,36 @@ def build_centroid_index(docs, centroids: Centroids, set_off: torch.Tensor | Non
         off = torch.from_numpy(np.concatenate([[0], np.cumsum(sizes)])).to(X.device)
         N = len(mats)
     _check_nonzero_rows(X, off)
-    if X.shape[1] == 128:
-        return build_centroid_index_native(X, centroids, off, N)
-    Xu = _unit_rows_dev(X, "documents")
-    cvec = centroids.device_vectors(X.device)
-    assign = _assign(Xu, cvec)
-    sizes_dev = off[1:] - off[:-1]
-    doc_of = torch.repeat_interleave(torch.arange(N, device=X.device), sizes_dev)
-    post_off, post_docs = _postings_from_assign(doc_of, assign, centroids.k, N)
-    return CentroidIndex(n_docs=N, post_off=post_off, post_docs=post_docs)
+    return build_centroid_index_native(X, centroids, off, N)
 
 
 def build_centroid_index_native(X: torch.Tensor, centroids: Centroids, set_off: torch.Tensor,
                                 n_docs: int) -> CentroidIndex:
-    """K6 on the device (d = 128): exact argmax assignment (tcgen05 screen + float64
-    re-rank, np.argmax tie rule) and postings by stable radix counting sort."""
+    """K6 on the device: exact argmax assignment (d = 128: tcgen05 screen + float64
+    re-rank; other d: float64 SIMT scan; np.argmax tie rule) and postings by stable
+    radix counting sort."""
     if X.dtype not in (torch.float16, torch.bfloat16, torch.float32, torch.float64):
         X = X.to(torch.float64)
     cvec = centroids.device_vectors(X.device)
-    lowp = centroids.device_lowp(X.device, bf16=X.dtype == torch.bfloat16)
+    lowp = (centroids.device_lowp(X.device, bf16=X.dtype == torch.bfloat16)
+            if X.shape[1] == 128 else None)
     assign = engine.assign_centroids(X, cvec, lowp)
     post_off, post_docs = engine.postings_from_assign(assign, set_off.contiguous(), n_docs,
                                                       centroids.k)
     return CentroidIndex(n_docs=n_docs, post_off=post_off, post_docs=post_docs)
 
 
-def build_centroid_index_fast(X: torch.Tensor, centroids: Centroids, set_off: torch.Tensor,
-                              n_docs: int, chunk: int = 1 << 14) -> CentroidIndex:
-    """Benchmark-setup variant of build_centroid_index for tens of millions of
-    vectors: argmax over a TF32 tensor-core GEMM instead of float64 (near-tie
-    assignments may differ from a float64 argmax; the resulting postings are
-    the index both the device path and the oracle are then given)."""
-    cvec = centroids.device_vectors(X.device).float()
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        n = X.shape[0]
-        assign = torch.empty(n, dtype=torch.int64, device=X.device)
-        for lo in range(0, n, chunk):
-            assign[lo:lo + chunk] = torch.argmax(X[lo:lo + chunk].float() @ cvec.T, dim=1)
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-    sizes_dev = set_off[1:] - set_off[:-1]
-    doc_of = torch.repeat_interleave(torch.arange(n_docs, device=X.device), sizes_dev)
-    post_off, post_docs = _postings_from_assign(doc_of, assign, centroids.k, n_docs)
-    return CentroidIndex(n_docs=n_docs, post_off=post_off, post_docs=post_docs)
-
-
 def extend_centroid_index(cindex: CentroidIndex, X: torch.Tensor, centroids: Centroids,
                           sizes: np.ndarray) -> CentroidIndex:
-    """Add postings for new docs (appended after the existing n_docs)."""
-    Xu = _unit_rows_dev(X, "documents")
-    assign = _assign(Xu, centroids.device_vectors(X.device))
-    sizes_dev = torch.from_numpy(np.asarray(sizes, np.int64)).to(X.device)
-    doc_of = cindex.n_docs + torch.repeat_interleave(
-        torch.arange(len(sizes), device=X.device), sizes_dev)
-    old_off = cindex.post_off
-    old_cent = torch.repeat_interleave(torch.arange(centroids.k, device=X.device),
-                                       old_off[1:] - old_off[:-1])
-    N = cindex.n_docs + len(sizes)
-    key = torch.cat([old_cent * N + cindex.post_docs, assign * N + doc_of])
-    post_off, post_docs = _postings_from_assign(key % N, key // N, centroids.k, N)
-    return CentroidIndex(n_docs=N, post_off=post_off, post_docs=post_docs)
+    """Add postings for new docs (appended after the existing n_docs): K6 on the
+    new vectors, then each posting = old posting + new docs (ids all larger)."""
+    sizes = np.asarray(sizes, np.int64)
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum(sizes)])).to(X.device)
+    add = build_centroid_index_native(X, centroids, off, len(sizes))
+    add_docs = add.post_docs + cindex.n_docs
+    post_off, post_docs = engine.merge_postings(cindex.post_off, cindex.post_docs, add.post_off,
+                                                add_docs)
+    return CentroidIndex(n_docs=cindex.n_docs + len(sizes), post_off=post_off, post_docs=post_docs)
 
 
 def filter_candidates_device(cindex: CentroidIndex, centroids: Centroids, Q: torch.Tensor,

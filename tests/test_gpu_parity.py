@@ -480,6 +480,46 @@ def test_add_sets_equals_full_build():
         d.add_sets(part, docs[:1])
 
 
+@pytest.mark.parametrize("dd", [16, 48, 200])
+def test_centroid_index_any_d_matches_oracle(dd):
+    """K6 for d != 128 (float64 SIMT path) vs the oracle's build_centroid_index,
+    float64 and float32 documents, with duplicated centroids (exact ties)."""
+    rng = np.random.default_rng(dd)
+    k = 37
+    C = rng.standard_normal((k, dd))
+    C[5] = C[4]
+    C = C / np.linalg.norm(C, axis=1, keepdims=True)
+    docs = [rng.standard_normal((int(rng.integers(1, 12)), dd)) for _ in range(150)]
+    docs[3][0] = C[4] * 2.0  # exact tie between centroids 4 and 5
+    cents = d.Centroids(k=k, seed=0, vectors=C)
+    want = O.build_centroid_index(docs, C)
+    for dt in (np.float64, np.float32):
+        cindex = d.build_centroid_index([x.astype(dt) for x in docs], cents)
+        got = cindex.postings
+        for c in range(k):
+            np.testing.assert_array_equal(got[c], want[c], err_msg=f"centroid {c}")
+
+
+def test_add_sets_with_prefilter_equals_full_build():
+    """add_sets extends the postings natively (new docs appended per centroid)."""
+    rng = np.random.default_rng(8)
+    docs = [(i, rng.standard_normal((int(rng.integers(1, 20)), 128))) for i in range(300)]
+    cfg = d.IndexConfig(d=128, C=6, L=32, seed=3,
+                        filter=d.FilterConfig(enabled=True, centroids=20, iters=3, probe=3,
+                                              k_filter=60))
+    full = d.build_index(docs, cfg)
+    part = d.build_index(docs[:180], cfg)
+    part.filter = (full.filter[0], d.build_centroid_index([x for _, x in docs[:180]],
+                                                          full.filter[0]))
+    d.add_sets(part, docs[180:])
+    np.testing.assert_array_equal(part.filter[1].post_off.cpu().numpy(),
+                                  full.filter[1].post_off.cpu().numpy())
+    np.testing.assert_array_equal(part.filter[1].post_docs.cpu().numpy(),
+                                  full.filter[1].post_docs.cpu().numpy())
+    Q = rng.standard_normal((3, 16, 128))
+    assert d.query_batch(full, Q, 10) == d.query_batch(part, Q, 10)
+
+
 def test_filtered_query_matches_reference_pipeline():
     """build_index with the prefilter on: candidates from K5, then K3/K4 over them,
     equals the oracle pipeline given the same centroids and postings."""

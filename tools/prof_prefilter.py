@@ -24,9 +24,10 @@ C = C / C.norm(dim=1, keepdim=True)
 cents = pf.Centroids(k=a.kc, seed=0, vectors=C.cpu().numpy())
 # synthetic postings: each doc in ~4 random postings
 n_post = a.docs * 4
-cent_of = torch.randint(0, a.kc, (n_post,), generator=g, device=dev)
-doc_of = torch.arange(a.docs, device=dev).repeat_interleave(4)
-off, docs = pf._postings_from_assign(doc_of, cent_of, a.kc, a.docs)
+cent_of = torch.randint(0, a.kc, (n_post,), generator=g, device=dev).to(torch.int32)
+set_off = torch.arange(0, n_post + 1, 4, device=dev, dtype=torch.int64)
+from paper_2210_15748_b200 import engine  # noqa: E402
+off, docs = engine.postings_from_assign(cent_of, set_off, a.docs, a.kc)
 cindex = pf.CentroidIndex(n_docs=a.docs, post_off=off, post_docs=docs)
 Q = torch.randn(a.qsets * 32, 128, generator=g, device=dev, dtype=torch.float64)
 torch.cuda.synchronize()
