@@ -354,6 +354,43 @@ def test_agg_end_to_end_query(golden_agg):
         np.testing.assert_array_equal(out_s.cpu().numpy(), g[f"e{n}_top_scores"])
 
 
+@pytest.mark.parametrize("m_q", [1, 7, 33, 129, 300])
+def test_agg_weighted_and_avgphi_any_mq(m_q):
+    """Weighted max across the K3 variants (m_q <= 128 single pass, > 128 slices +
+    finalize) and avg-phi across K3a (m_q <= 32) / K3g (larger m_q), vs the dense
+    oracle, bit-exact; exhaustive (>= 8 query sets) and candidate lists."""
+    from oracle import dessert_oracle as O
+    from paper_2210_15748_b200 import scoring
+    rng = np.random.default_rng(m_q)
+    L, C = 32, 5
+    sizes = rng.integers(1, 60, size=40)
+    hot = rng.integers(0, 32, size=L)
+    codes = rng.integers(0, 32, size=(int(sizes.sum()), L))
+    mask = rng.random(codes.shape) < 0.5
+    codes[mask] = np.broadcast_to(hot, codes.shape)[mask]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    n_q = 9
+    qc = rng.integers(0, 32, size=(n_q, m_q, L))
+    qm = rng.random(qc.shape) < 0.5
+    qc[qm] = np.broadcast_to(hot, qc.shape)[qm]
+    cfg = d.IndexConfig(d=4, C=C, L=L, filter=d.FilterConfig(enabled=False))
+    idx = d.build_from_codes(torch.from_numpy(codes.astype(np.int32)).to(DEV), sizes,
+                             np.arange(len(sizes)), cfg)
+    w = rng.uniform(0, 1, size=m_q)
+    sets = np.stack([rng.permutation(len(sizes))[:25] for _ in range(n_q)])
+    for sc in (d.Scorer(d.max_aggregation(), w), d.Scorer(d.avg_phi_aggregation("exp-minus-one"), w),
+               d.Scorer(d.avg_phi_aggregation("identity"))):
+        table = scoring.table_for(idx.lookup.table, sc)
+        kind = sc.inner.kind
+        want = np.stack([O.score_sets_dense_agg(qc[r], codes, off, table, kind, sc.weights)
+                         for r in range(n_q)])
+        got, _ = d.score_matrix(idx, qc, scorer=sc)
+        np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"{kind} all")
+        got2, _ = d.score_matrix(idx, qc, sets=sets, scorer=sc)
+        np.testing.assert_array_equal(got2.cpu().numpy(), np.take_along_axis(want, sets, axis=1),
+                                      err_msg=f"{kind} cand")
+
+
 def test_agg_random_long_sets_vs_oracle():
     """Sets with up to 600 vectors (several recursive pairwise levels), m_q = 70,
     avg-phi with weights, against the dense restatement."""
