@@ -551,7 +551,7 @@ def run_cfg3(args):
         d.query_batch(idx, Qb.to(dev, non_blocking=True), top_k, return_tensors=True)
     torch.cuda.synchronize()
     te = time.perf_counter()
-    n_e2e = max(3, min(args.steps, 10))
+    n_e2e = max(5, min(args.steps, 20))
     for _ in range(n_e2e):
         s_, i_ = d.query_batch(idx, Qb.to(dev, non_blocking=True), top_k, return_tensors=True)
         hs, hi = s_.cpu(), i_.cpu()

@@ -197,6 +197,104 @@ __global__ void count_kernel(const int32_t *__restrict__ probed, int64_t n_q, in
     }
 }
 
+// ---- chunked counting: CTA per (query set, doc chunk), counters in shared memory
+constexpr int kChunkBytes = 64 * 1024;  // counters per CTA (3 CTAs per SM)
+constexpr int kCntThreads = 512;
+static int64_t chunk_docs(int cb) { return static_cast<int64_t>(kChunkBytes) * 8 / cb; }
+
+// bnd[c * (nch + 1) + j] = index in post_docs of the first doc >= j * D of posting c
+// (postings are doc-ascending); j = nch -> end of the posting
+__global__ void chunk_bounds_kernel(const int64_t *__restrict__ post_off, const int64_t *__restrict__ post_docs,
+                                    int64_t k_c, int nch, int64_t D, int64_t *__restrict__ bnd) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= k_c * (nch + 1)) return;
+    const int64_t c = i / (nch + 1);
+    const int j = static_cast<int>(i - c * (nch + 1));
+    const int64_t lo = post_off[c], hi = post_off[c + 1];
+    bnd[i] = j == nch ? hi : lo + lower_bound_i64(post_docs + lo, hi - lo, j * D);
+}
+
+// counts of one doc chunk for one query set in shared memory, then its count
+// histogram (hist_bins = max_count + 1) and the counter words of the row
+template <int CB>
+__global__ void __launch_bounds__(kCntThreads)
+    count_chunk_kernel(const int32_t *__restrict__ probed, int MP, const int64_t *__restrict__ bnd,
+                       int nch, const int64_t *__restrict__ post_docs, int64_t row_words,
+                       int max_count, uint32_t *__restrict__ counts, uint32_t *__restrict__ chist) {
+    constexpr int DPW = 32 / CB;
+    constexpr uint32_t MASK = (1u << CB) - 1u;
+    constexpr int W_CH = kChunkBytes / 4;          // counter words per chunk
+    constexpr int64_t D = static_cast<int64_t>(W_CH) * DPW;  // docs per chunk
+    extern __shared__ __align__(16) uint32_t sc[];  // W_CH counter words, then max_count+1 bins
+    uint32_t *hist = sc + W_CH;
+    const int ch = blockIdx.x;
+    const int64_t qs = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < W_CH / 4; i += kCntThreads) reinterpret_cast<uint4 *>(sc)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i <= max_count; i += kCntThreads) hist[i] = 0;
+    __syncthreads();
+    const int64_t doc0 = ch * D;
+    for (int r = warp; r < MP; r += kCntThreads / 32) {
+        const int c = probed[qs * MP + r];
+        if (c < 0 || c == 0x7fffffff) continue;
+        const int64_t a = bnd[static_cast<int64_t>(c) * (nch + 1) + ch];
+        const int64_t b = bnd[static_cast<int64_t>(c) * (nch + 1) + ch + 1];
+        for (int64_t i = a + lane; i < b; i += 4 * 32) {  // 4 loads in flight per lane
+            int64_t dd[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dd[u] = i + u * 32 < b ? post_docs[i + u * 32] - doc0 : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (dd[u] >= 0)
+                    atomicAdd(&sc[dd[u] / DPW], 1u << (CB * static_cast<int>(dd[u] % DPW)));
+        }
+    }
+    __syncthreads();
+    // histogram of this chunk's counts: 1..3 by SIMD compares, >= 4 by shared atomics
+    constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
+    uint32_t h1 = 0, h2 = 0, h3 = 0;
+    for (int i = tid; i < W_CH; i += kCntThreads) {
+        const uint32_t x = sc[i];
+        if (x == 0u) continue;
+        if (CB == 8) {
+            h1 += __popc(__vcmpeq4(x, ONE) & ONE);
+            h2 += __popc(__vcmpeq4(x, 2 * ONE) & ONE);
+            h3 += __popc(__vcmpeq4(x, 3 * ONE) & ONE);
+            if (__vcmpgeu4(x, 4 * ONE) == 0u) continue;
+        } else {
+            h1 += __popc(__vcmpeq2(x, ONE) & ONE);
+            h2 += __popc(__vcmpeq2(x, 2 * ONE) & ONE);
+            h3 += __popc(__vcmpeq2(x, 3 * ONE) & ONE);
+            if (__vcmpgeu2(x, 4 * ONE) == 0u) continue;
+        }
+#pragma unroll
+        for (int k = 0; k < DPW; ++k) {
+            const uint32_t v = (x >> (CB * k)) & MASK;
+            if (v >= 4) atomicAdd(&hist[tmin<uint32_t>(v, static_cast<uint32_t>(max_count))], 1u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+        h3 += __shfl_xor_sync(0xffffffffu, h3, o);
+    }
+    if (lane == 0) {
+        if (max_count >= 1) atomicAdd(&hist[1], h1);
+        if (max_count >= 2) atomicAdd(&hist[2], h2);
+        if (max_count >= 3) atomicAdd(&hist[3], h3);
+    }
+    __syncthreads();
+    uint32_t *gh = chist + (qs * nch + ch) * static_cast<int64_t>(max_count + 1);
+    for (int i = tid; i <= max_count; i += kCntThreads) gh[i] = hist[i];
+    // counter words of the row (chunks tile the whole padded row)
+    const int64_t w0 = static_cast<int64_t>(ch) * W_CH;
+    const int64_t nw = tmin<int64_t>(W_CH, row_words - w0);
+    uint32_t *row = counts + qs * row_words + w0;
+    for (int64_t i = tid; i < nw / 4; i += kCntThreads)
+        reinterpret_cast<uint4 *>(row)[i] = reinterpret_cast<const uint4 *>(sc)[i];
+}
+
 __device__ __forceinline__ uint32_t count_of(const uint32_t *row, int64_t doc) {
     return (row[doc >> 1] >> (16 * (doc & 1))) & 0xffffu;
 }
@@ -216,7 +314,7 @@ template <int CB>  // counter bits: 8 or 16
 __global__ void __launch_bounds__(kSelThreads)
     select_kernel(const uint32_t *__restrict__ counts, int64_t row_words, int64_t n_docs,
                   int max_count, int k_filter, int64_t *__restrict__ cand,
-                  int32_t *__restrict__ n_cand) {
+                  int32_t *__restrict__ n_cand, const uint32_t *__restrict__ chist, int nch) {
     constexpr int DPG = 128 / CB;            // docs per uint4 group
     constexpr int DPW = 32 / CB;             // docs per word
     constexpr uint32_t MASK = (1u << CB) - 1u;
@@ -251,6 +349,15 @@ __global__ void __launch_bounds__(kSelThreads)
     };
     const int64_t per_step = static_cast<int64_t>(blockDim.x) * G;
     uint32_t *myh = whist + warp * kSelBins;
+    if (chist != nullptr) {  // histogram from the chunked counting pass
+        const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(max_count + 1);
+        for (int b = tid; b <= max_count; b += blockDim.x) {
+            uint32_t t = 0;
+            for (int c = 0; c < nch; ++c) t += gh[c * static_cast<int64_t>(max_count + 1) + b];
+            hist[b] = t;
+        }
+        __syncthreads();
+    } else {
     // counts 1..3 (the bulk of the touched docs) are counted with SIMD byte /
     // half-word compares in registers; only counts >= 4 use shared atomics
     constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
@@ -304,6 +411,7 @@ __global__ void __launch_bounds__(kSelThreads)
             hist[b] = t;
         }
     __syncthreads();
+    }
     if (tid == 0) {
         int64_t cum = 0;
         bool found = false;
@@ -425,31 +533,48 @@ static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255);
 static int counter_bits(int max_count) { return max_count <= 255 ? 8 : 16; }
 static int64_t row_words_for(int64_t n_docs, int max_count) {
     const int64_t dpg = 128 / counter_bits(max_count);
-    return ((n_docs + dpg - 1) / dpg) * 4;
+    return ((n_docs + dpg - 1) / dpg) * 4;  // 16-byte groups; the last chunk may be partial
 }
-static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int P, const int64_t *post_off,
-                               const int64_t *post_docs, int64_t n_docs, int64_t row_words,
-                               uint32_t *counts, int k_filter, int64_t *cand, int32_t *n_cand,
-                               cudaStream_t st);
 
+// chunked counting workspace: posting chunk boundaries + per-chunk histograms
+static int n_chunks_for(int64_t n_docs, int max_count) {
+    return static_cast<int>((n_docs + chunk_docs(counter_bits(max_count)) - 1) / chunk_docs(counter_bits(max_count)));
+}
+static size_t count_ws_bytes(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n_docs) {
+    const int mc = m_q * P, nch = n_chunks_for(n_docs, mc);
+    return align256(static_cast<size_t>(k_c) * (nch + 1) * sizeof(int64_t)) +
+           align256(static_cast<size_t>(n_q) * nch * (mc + 1) * sizeof(uint32_t));
+}
+
+// counts (written whole by the chunked pass; no memset) -> candidates.  cws:
+// count_ws_bytes workspace.
 static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int P, const int64_t *post_off,
-                               const int64_t *post_docs, int64_t n_docs, int64_t row_words,
+                               const int64_t *post_docs, int64_t n_docs, int64_t k_c, int64_t row_words,
                                uint32_t *counts, int k_filter, int64_t *cand, int32_t *n_cand,
-                               cudaStream_t st) {
+                               uint8_t *cws, cudaStream_t st) {
     const int max_count = m_q * P;
     const int cb = counter_bits(max_count);
-    const int64_t warps = n_q * m_q * P;
-    count_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(
-        probed, n_q, m_q, P, post_off, post_docs, row_words, counts, cb);
+    const int nch = n_chunks_for(n_docs, max_count);
+    DSRT_REQUIRE(nch < 65536 && n_q < 65536, DSRT_EUNSUPPORTED, "invalid parameter: count grid too large");
+    int64_t *bnd = reinterpret_cast<int64_t *>(cws);
+    uint32_t *chist = reinterpret_cast<uint32_t *>(cws + align256(static_cast<size_t>(k_c) * (nch + 1) * sizeof(int64_t)));
+    const int64_t nb = k_c * (nch + 1);
+    chunk_bounds_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(post_off, post_docs, k_c, nch,
+                                                                              chunk_docs(cb), bnd);
+    const size_t csmem = kChunkBytes + (max_count + 1) * sizeof(uint32_t);
+    auto ck = cb == 8 ? count_chunk_kernel<8> : count_chunk_kernel<16>;
+    DSRT_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+    ck<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kCntThreads, csmem, st>>>(
+        probed, m_q * P, bnd, nch, post_docs, row_words, max_count, counts, chist);
     const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1 + kSelWarps * kSelBins) * sizeof(uint32_t);
     if (cb == 8) {
         DSRT_CUDA(cudaFuncSetAttribute(select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         select_kernel<8><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
-            counts, row_words, n_docs, max_count, k_filter, cand, n_cand);
+            counts, row_words, n_docs, max_count, k_filter, cand, n_cand, chist, nch);
     } else {
         DSRT_CUDA(cudaFuncSetAttribute(select_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         select_kernel<16><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
-            counts, row_words, n_docs, max_count, k_filter, cand, n_cand);
+            counts, row_words, n_docs, max_count, k_filter, cand, n_cand, chist, nch);
     }
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
@@ -468,7 +593,7 @@ static PrefilterWs ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, 
     w.cand_bytes = align256(static_cast<size_t>(rows) * w.n_chunks * P * sizeof(Cand));
     w.probed_bytes = align256(static_cast<size_t>(rows) * P * sizeof(int32_t));
     w.counts_bytes = align256(static_cast<size_t>(n_q) * w.row_words * sizeof(uint32_t));
-    w.total = w.cand_bytes + w.probed_bytes + w.counts_bytes;
+    w.total = w.cand_bytes + w.probed_bytes + w.counts_bytes + count_ws_bytes(n_q, m_q, P, k_c, n_docs);
     return w;
 }
 
@@ -854,9 +979,9 @@ extern "C" int dsrt_prefilter(const double *Q, int64_t n_q, int m_q, int d, cons
     probe_kernel<<<g1, kPTile, psmem, st>>>(Q, rows, d, cents, k_c, P, cands);
     merge_kernel<<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
         cands, rows, static_cast<int>(w.n_chunks), P, probed);
-    DSRT_CUDA(cudaMemsetAsync(counts, 0, w.counts_bytes, st));
-    int rc2 = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, w.row_words, counts,
-                                  k_filter, cand, n_cand, st);
+    int rc2 = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, k_c, w.row_words, counts,
+                                  k_filter, cand, n_cand, ws + w.cand_bytes + w.probed_bytes + w.counts_bytes,
+                                  st);
     if (rc2) return rc2;
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
@@ -887,7 +1012,7 @@ extern "C" int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scal
 
 namespace dsrt {
 struct TcWs {
-    size_t q16, screen, theta, lists, listn, probed, fallback, counts, total;
+    size_t q16, screen, theta, lists, listn, probed, fallback, counts, cnt_ws, total;
     int64_t n_split, row_words, tiles_per_split;
 };
 static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int P) {
@@ -910,7 +1035,8 @@ static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int 
     w.probed = align256(static_cast<size_t>(rows) * P * sizeof(int32_t));
     w.fallback = align256(static_cast<size_t>(rows) * sizeof(int32_t));
     w.counts = align256(static_cast<size_t>(n_q) * w.row_words * sizeof(uint32_t));
-    w.total = w.q16 + w.screen + w.theta + w.lists + w.listn + w.probed + w.fallback + w.counts;
+    w.cnt_ws = count_ws_bytes(n_q, m_q, P, k_c, n_docs);
+    w.total = w.q16 + w.screen + w.theta + w.lists + w.listn + w.probed + w.fallback + w.counts + w.cnt_ws;
     return w;
 }
 }  // namespace dsrt
@@ -951,7 +1077,8 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     int32_t *listn = reinterpret_cast<int32_t *>(ws + o); o += w.listn;
     int32_t *probed = reinterpret_cast<int32_t *>(ws + o); o += w.probed;
     int32_t *fallback = reinterpret_cast<int32_t *>(ws + o); o += w.fallback;
-    uint32_t *counts = reinterpret_cast<uint32_t *>(ws + o);
+    uint32_t *counts = reinterpret_cast<uint32_t *>(ws + o); o += w.counts;
+    uint8_t *cnt_ws = ws + o;
     const int64_t rows = n_q * m_q;
     const int64_t m_tiles = (rows + 127) / 128;
     DSRT_CUDA(cudaMemsetAsync(q16, 0, w.q16, st));
@@ -981,9 +1108,8 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
         lists, listn, Q, cents, rows, d, P, probed, fallback);
     pf_fallback_kernel<double><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d,
                                                                            P, probed);
-    DSRT_CUDA(cudaMemsetAsync(counts, 0, w.counts, st));
-    rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, w.row_words, counts,
-                             k_filter, cand, n_cand, st);
+    rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, k_c, w.row_words, counts,
+                             k_filter, cand, n_cand, cnt_ws, st);
     if (rc) return rc;
     DSRT_LAUNCH_CHECK();
     (void)cent_max_norm;
