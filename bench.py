@@ -534,9 +534,21 @@ def run_cfg3(args):
         last["cand"], last["n_cand"] = cand, n_cand
         return engine.topk(scores, top_k, ids=idx.doc_ids_dev[cand.clamp(min=0)], n_valid=n_cand)
 
-    ms, clk = _clocks_and_time(step, args.steps, max(3, args.warmup), local, stream)
+    # per-stage kernel times from eager steps with events between the stages
+    for _ in range(3):
+        step(False)
+    for _ in range(10):
+        step(True)
+    torch.cuda.synchronize()
     pf_ms = float(np.mean([a.elapsed_time(b) for a, b in kev["prefilter"]]))
     sc_ms = float(np.mean([a.elapsed_time(b) for a, b in kev["score"]]))
+    # the batch step is a fixed sequence of ~11 kernels: capture it once in a CUDA
+    # graph and time replays (no host launch gaps between the kernels)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step(False)
+    ms, clk = _clocks_and_time(lambda timed: graph.replay(), args.steps, max(3, args.warmup),
+                               local, stream)
     # batch-1 latency through the public API (host query in, host results out)
     lat = []
     Qh = Qall[256:].cpu()
