@@ -14,6 +14,23 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 
+// Stream-ordered scratch allocations.  The device's default memory pool keeps
+// its memory across synchronisations (release threshold = max), otherwise
+// every synchronising call would unmap and re-map its scratch (~0.4 ms).
+cudaError_t malloc_async(void **p, size_t bytes, cudaStream_t st) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    return cudaMallocAsync(p, bytes, st);
+}
+
 int sm_count() {
     static int cached = 0;
     static std::once_flag once;

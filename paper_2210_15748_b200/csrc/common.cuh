@@ -38,6 +38,7 @@ void set_error(const char *fmt, ...);
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+cudaError_t malloc_async(void **p, size_t bytes, cudaStream_t st);  // default pool, memory kept
 
 template <typename T>
 __host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }

@@ -127,10 +127,79 @@ __global__ void __launch_bounds__(kHRows)
     }
 }
 
+// Small batches (too few 64-row blocks to fill the GPU): the 32-plane chunk
+// becomes a grid dimension; each CTA writes one sign word per row (same
+// per-(row, plane) sequential FMA as above, so bits are identical) and a
+// per-row pass packs the words into codes and records.
+template <typename TX, typename A>
+__global__ void __launch_bounds__(kHRows)
+    hash_simt_chunk_kernel(const TX *__restrict__ X, int64_t n, int d, const A *__restrict__ planes, int P,
+                           uint32_t *__restrict__ bits, int bw, uint32_t *zero_rows) {
+    __shared__ A xs[kHDim][kHRows + 1];
+    __shared__ __align__(16) A ps[kHDim][kHPlanes];
+    const int tid = threadIdx.x;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kHRows;
+    const int64_t row = row0 + tid;
+    const int p0 = blockIdx.y * kHPlanes;
+    bool nonzero = false;
+    A acc[kHPlanes];
+#pragma unroll
+    for (int j = 0; j < kHPlanes; ++j) acc[j] = A(0);
+    for (int k0 = 0; k0 < d; k0 += kHDim) {
+        __syncthreads();
+        for (int i = tid; i < kHRows * kHDim; i += kHRows) {
+            const int r = i / kHDim, kk = i % kHDim;
+            const int64_t gr = row0 + r;
+            A v = A(0);
+            if (gr < n && k0 + kk < d) v = to_acc<TX, A>(X[gr * d + k0 + kk]);
+            xs[kk][r] = v;
+        }
+        for (int i = tid; i < kHPlanes * kHDim; i += kHRows) {
+            const int pp = i / kHDim, kk = i % kHDim;
+            A v = A(0);
+            if (p0 + pp < P && k0 + kk < d) v = planes[static_cast<int64_t>(p0 + pp) * d + k0 + kk];
+            ps[kk][pp] = v;
+        }
+        __syncthreads();
+        const int kmax = min(kHDim, d - k0);
+        for (int kk = 0; kk < kmax; ++kk) {
+            const A xv = xs[kk][tid];
+            nonzero |= (xv != A(0));
+#pragma unroll
+            for (int j = 0; j < kHPlanes; ++j) acc[j] = fma(xv, ps[kk][j], acc[j]);
+        }
+    }
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < kHPlanes; ++j) word |= (acc[j] > A(0) ? 1u : 0u) << j;
+    if (row < n) {
+        bits[row * bw + blockIdx.y] = word;
+        if (blockIdx.y == 0 && !nonzero && zero_rows) atomicAdd(zero_rows, 1u);
+    }
+}
+
+__global__ void hash_pack_kernel(const uint32_t *__restrict__ bits, int bw, int64_t n, int L, int C,
+                                 void *codes_out, uint32_t *recs_out) {
+    const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (row < n) pack_row(bits + row * bw, L, C, row, codes_out, recs_out);
+}
+
 template <typename TX, typename A>
 static int launch_hash(const void *X, int64_t n, int d, const void *planes, int L, int C,
                        void *codes, uint32_t *recs, uint32_t *zero_rows, cudaStream_t st) {
     const int64_t blocks = (n + kHRows - 1) / kHRows;
+    if (blocks < sm_count()) {  // small batch: split the planes across CTAs
+        const int bw = (L * C + 31) / 32;
+        uint32_t *bits = nullptr;
+        DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&bits), static_cast<size_t>(n) * bw * 4, st));
+        hash_simt_chunk_kernel<TX, A><<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(bw)), kHRows, 0, st>>>(
+            static_cast<const TX *>(X), n, d, static_cast<const A *>(planes), L * C, bits, bw, zero_rows);
+        hash_pack_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(bits, bw, n, L, C, codes,
+                                                                               recs);
+        cudaFreeAsync(bits, st);
+        DSRT_LAUNCH_CHECK();
+        return DSRT_OK;
+    }
     const size_t smem = static_cast<size_t>(kHRows) * ((L * C + 31) / 32 + 1) * sizeof(uint32_t);
     DSRT_CUDA(cudaFuncSetAttribute(hash_simt_kernel<TX, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));

@@ -257,7 +257,7 @@ int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, in
     const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     const int64_t prow = static_cast<int64_t>(parts) * groups * 32 * C;
     uint16_t *pp = nullptr;
-    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&pp), prow * 128 * sizeof(uint16_t), st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&pp), prow * 128 * sizeof(uint16_t), st));
     permute_planes_kernel<<<static_cast<unsigned>((prow * 128 + 255) / 256), 256, 0, st>>>(
         static_cast<const uint16_t *>(planes), parts, L, C, groups, pp);
     DSRT_LAUNCH_CHECK();

@@ -205,7 +205,7 @@ int assign_simt(const void *X, int dtype, int64_t n, int d, const double *cents,
     uint32_t *zero = reinterpret_cast<uint32_t *>(w);
     double *xu = reinterpret_cast<double *>(w + 256);
     double *best = nullptr;
-    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&best), tmin<int64_t>(n, kKmChunk) * 8, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&best), tmin<int64_t>(n, kKmChunk) * 8, st));
     DSRT_CUDA(cudaMemsetAsync(zero, 0, 4, st));
     const size_t smem = 4 * static_cast<size_t>(d) * 8;
     for (int64_t r0 = 0; r0 < n; r0 += kKmChunk) {

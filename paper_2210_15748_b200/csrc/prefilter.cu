@@ -1183,7 +1183,7 @@ static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const
         float *v = vals;
         float *vtmp = nullptr;
         if (n_split > 1) {
-            DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&vtmp), rows * n_split * kSHalves * kMaxPtc * sizeof(float), st));
+            DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&vtmp), rows * n_split * kSHalves * kMaxPtc * sizeof(float), st));
             v = vtmp;
         }
         rc = launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, v, nullptr, nullptr, nullptr, idesc);

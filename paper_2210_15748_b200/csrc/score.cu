@@ -106,11 +106,11 @@ static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
     uint16_t *mc = a.mc;
     uint16_t *own = nullptr;
     if (mc == nullptr) {
-        DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&own), rows * a.m_q * sizeof(uint16_t), st));
+        DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&own), rows * a.m_q * sizeof(uint16_t), st));
         mc = own;
     }
     double *scratch = nullptr;
-    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&scratch), rows * a.m_q * sizeof(double), st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&scratch), rows * a.m_q * sizeof(double), st));
     int rc = DSRT_OK;
     for (int64_t qs = 0; qs < a.n_qsets && rc == DSRT_OK; ++qs) {
         for (int q0 = 0; q0 < a.m_q && rc == DSRT_OK; q0 += 128) {

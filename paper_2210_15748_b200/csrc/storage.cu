@@ -424,7 +424,7 @@ extern "C" int dsrt_dsri_decode_sets(const uint8_t *buf, const int64_t *tt_off, 
     if (n_sets == 0) return DSRT_OK;
     cudaStream_t st = as_stream(stream);
     unsigned long long *fb = nullptr;
-    DSRT_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&fb), 8, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&fb), 8, st));
     DSRT_CUDA(cudaMemsetAsync(fb, 0xff, 8, st));
     const int wpw = static_cast<int>((m_max + 31) / 32);
     const size_t smem = static_cast<size_t>(kStWarps) * wpw * 4;
