@@ -165,8 +165,8 @@ int dsrt_topk_max_k(void);
  */
 int dsrt_prefilter(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
                    int64_t k_c, const int64_t *post_off, const int64_t *post_docs, int64_t n_docs,
-                   int probe, int k_filter, int64_t *cand, int32_t *n_cand, void *workspace,
-                   size_t workspace_bytes, void *stream);
+                   const int64_t *chunk_bounds, int probe, int k_filter, int64_t *cand,
+                   int32_t *n_cand, void *workspace, size_t workspace_bytes, void *stream);
 size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
 /*
  * K5, tensor-core screen (same results as dsrt_prefilter): tcgen05 fp16 GEMM of
@@ -179,9 +179,19 @@ size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n
  */
 int dsrt_prefilter_tc(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
                       const void *centroids_f16, double cent_max_norm, int64_t k_c,
-                      const int64_t *post_off, const int64_t *post_docs, int64_t n_docs, int probe,
-                      int k_filter, int64_t *cand, int32_t *n_cand, void *workspace,
-                      size_t workspace_bytes, void *stream);
+                      const int64_t *post_off, const int64_t *post_docs, int64_t n_docs,
+                      const int64_t *chunk_bounds, int probe, int k_filter, int64_t *cand,
+                      int32_t *n_cand, void *workspace, size_t workspace_bytes, void *stream);
+/*
+ * Posting chunk boundaries for the counting pass (postings are doc-ascending):
+ * out[c * (nch + 1) + j] = index in post_docs of the first doc >= j * D in
+ * posting c, D = the counting chunk (64 KB of counters), nch = chunks of n_docs.
+ * Depend only on the postings and the counter width (m_q * probe), so callers
+ * compute them once per index and pass them as chunk_bounds (NULL: per call).
+ */
+int64_t dsrt_posting_chunk_bounds_size(int64_t k_c, int64_t n_docs, int m_q, int probe);
+int dsrt_posting_chunk_bounds(const int64_t *post_off, const int64_t *post_docs, int64_t k_c,
+                              int64_t n_docs, int m_q, int probe, int64_t *out, void *stream);
 size_t dsrt_prefilter_tc_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n_docs, int probe);
 /* rows of float64 -> fp16 (scale > 0: multiply by scale; scale <= 0: normalise each row) */
 int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scale, void *dst, void *stream);

@@ -57,11 +57,13 @@ SIGNATURES = {
     "dsrt_varints_to_postings": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dsrt_topk": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_topk_max_k": (_i32, []),
-    "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _vp,
-                              _vp, _vp, _sz, _vp]),
+    "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _i32, _i32,
+                              _vp, _vp, _vp, _sz, _vp]),
     "dsrt_prefilter_workspace": (_sz, [_i64, _i32, _i64, _i64, _i32]),
     "dsrt_prefilter_tc": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, ctypes.c_double, _i64, _vp, _vp,
-                                 _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+                                 _i64, _vp, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "dsrt_posting_chunk_bounds_size": (_i64, [_i64, _i64, _i32, _i32]),
+    "dsrt_posting_chunk_bounds": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp]),
     "dsrt_prefilter_tc_workspace": (_sz, [_i64, _i32, _i64, _i64, _i32]),
     "dsrt_to_f16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),
     "dsrt_to_bf16_rows": (_i32, [_vp, _i64, _i32, ctypes.c_double, _vp, _vp]),

@@ -551,7 +551,7 @@ static size_t count_ws_bytes(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n
 static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int P, const int64_t *post_off,
                                const int64_t *post_docs, int64_t n_docs, int64_t k_c, int64_t row_words,
                                uint32_t *counts, int k_filter, int64_t *cand, int32_t *n_cand,
-                               uint8_t *cws, cudaStream_t st) {
+                               uint8_t *cws, const int64_t *bounds_in, cudaStream_t st) {
     const int max_count = m_q * P;
     const int cb = counter_bits(max_count);
     const int nch = n_chunks_for(n_docs, max_count);
@@ -559,8 +559,12 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
     int64_t *bnd = reinterpret_cast<int64_t *>(cws);
     uint32_t *chist = reinterpret_cast<uint32_t *>(cws + align256(static_cast<size_t>(k_c) * (nch + 1) * sizeof(int64_t)));
     const int64_t nb = k_c * (nch + 1);
-    chunk_bounds_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(post_off, post_docs, k_c, nch,
-                                                                              chunk_docs(cb), bnd);
+    if (bounds_in != nullptr) {  // cached by the caller (dsrt_posting_chunk_bounds)
+        bnd = const_cast<int64_t *>(bounds_in);
+    } else {
+        chunk_bounds_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(post_off, post_docs, k_c,
+                                                                                  nch, chunk_docs(cb), bnd);
+    }
     const size_t csmem = kChunkBytes + (max_count + 1) * sizeof(uint32_t);
     auto ck = cb == 8 ? count_chunk_kernel<8> : count_chunk_kernel<16>;
     DSRT_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
@@ -825,26 +829,29 @@ __global__ void __launch_bounds__(kSThreads, 1)
     if (warp == 1) tmem_dealloc(tmem, 256);
 }
 
-// thread per row: theta = (P-th best approx over all splits) - 2 eps
+// theta = (P-th best approx over all splits) - 2 eps
 // (theta scaled by |x| when the screen ran on raw, unnormalised rows Xraw)
 template <typename TQ>
 __global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int64_t n_rows, int P,
                                 float eps2, float *__restrict__ theta, int32_t *__restrict__ list_n,
                                 const TQ *__restrict__ Xraw, int d) {
-    const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    // warp per row: lanes merge disjoint partial lists, then P rounds of a warp max
+    const int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (row >= n_rows) return;
-    if (Xraw != nullptr) {
+    if (Xraw != nullptr) {  // eps bound scales with |x| (the 1.0001 margin covers rounding)
         double ss = 0.0;
-        for (int k = 0; k < d; ++k) {
+        for (int k = lane; k < d; k += 32) {
             const double v = as_f64(Xraw[row * d + k]);
             ss = fma(v, v, ss);
         }
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
         eps2 = static_cast<float>(eps2 * sqrt(ss) * 1.0001);
     }
     float tv[kMaxPtc];
 #pragma unroll
     for (int j = 0; j < kMaxPtc; ++j) tv[j] = -INFINITY;
-    for (int s = 0; s < n_split; ++s)
+    for (int s = lane; s < n_split; s += 32)
         for (int j = 0; j < P; ++j) {
             float x = vals[(row * n_split + s) * kMaxPtc + j];
 #pragma unroll
@@ -854,12 +861,23 @@ __global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int
                 tv[q] = hi;
             }
         }
-    float aP = tv[0];
+    float aP = -INFINITY;
+    for (int q = 0; q < P; ++q) {  // pop the warp-wide maximum P times
+        float wm = tv[0];
 #pragma unroll
-    for (int q = 1; q < kMaxPtc; ++q)
-        if (q < P) aP = tv[q];
-    theta[row] = aP - eps2;
-    list_n[row] = 0;
+        for (int o = 16; o > 0; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        const int owner = __ffs(__ballot_sync(0xffffffffu, tv[0] == wm)) - 1;
+        if (lane == owner) {
+#pragma unroll
+            for (int k = 0; k + 1 < kMaxPtc; ++k) tv[k] = tv[k + 1];
+            tv[kMaxPtc - 1] = -INFINITY;
+        }
+        aP = wm;
+    }
+    if (lane == 0) {
+        theta[row] = aP - eps2;
+        list_n[row] = 0;
+    }
 }
 
 // warp per row: exact float64 re-rank of the collected candidates -> probed ids;
@@ -941,6 +959,23 @@ __global__ void __launch_bounds__(256)
 
 using namespace dsrt;
 
+extern "C" int64_t dsrt_posting_chunk_bounds_size(int64_t k_c, int64_t n_docs, int m_q, int probe) {
+    return k_c * (n_chunks_for(n_docs, m_q * tmax(probe, 1)) + 1);
+}
+
+extern "C" int dsrt_posting_chunk_bounds(const int64_t *post_off, const int64_t *post_docs, int64_t k_c,
+                                         int64_t n_docs, int m_q, int probe, int64_t *out, void *stream) {
+    DSRT_REQUIRE(k_c >= 1 && n_docs >= 1 && m_q >= 1 && probe >= 1, DSRT_EINVAL, "invalid parameter: empty");
+    const int P = static_cast<int>(tmin<int64_t>(probe, k_c));
+    const int cb = counter_bits(m_q * P);
+    const int nch = n_chunks_for(n_docs, m_q * P);
+    const int64_t nb = k_c * (nch + 1);
+    chunk_bounds_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, as_stream(stream)>>>(
+        post_off, post_docs, k_c, nch, chunk_docs(cb), out);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
 extern "C" size_t dsrt_prefilter_workspace(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs,
                                            int probe) {
     const int P = static_cast<int>(tmin<int64_t>(tmax(probe, 1), k_c));
@@ -949,8 +984,9 @@ extern "C" size_t dsrt_prefilter_workspace(int64_t n_q, int m_q, int64_t k_c, in
 
 extern "C" int dsrt_prefilter(const double *Q, int64_t n_q, int m_q, int d, const double *cents,
                               int64_t k_c, const int64_t *post_off, const int64_t *post_docs,
-                              int64_t n_docs, int probe, int k_filter, int64_t *cand,
-                              int32_t *n_cand, void *workspace, size_t ws_bytes, void *stream) {
+                              int64_t n_docs, const int64_t *chunk_bounds, int probe, int k_filter,
+                              int64_t *cand, int32_t *n_cand, void *workspace, size_t ws_bytes,
+                              void *stream) {
     DSRT_REQUIRE(probe >= 1, DSRT_EINVAL, "invalid parameter: probe must be >= 1, got %d", probe);
     DSRT_REQUIRE(k_filter >= 1, DSRT_EINVAL, "invalid parameter: k_filter must be >= 1, got %d", k_filter);
     DSRT_REQUIRE(m_q >= 1 && n_q >= 0, DSRT_EINVAL, "Q must be a non-empty (m_q, d) matrix");
@@ -981,7 +1017,7 @@ extern "C" int dsrt_prefilter(const double *Q, int64_t n_q, int m_q, int d, cons
         cands, rows, static_cast<int>(w.n_chunks), P, probed);
     int rc2 = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, k_c, w.row_words, counts,
                                   k_filter, cand, n_cand, ws + w.cand_bytes + w.probed_bytes + w.counts_bytes,
-                                  st);
+                                  chunk_bounds, st);
     if (rc2) return rc2;
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
@@ -1050,6 +1086,7 @@ extern "C" size_t dsrt_prefilter_tc_workspace(int64_t n_q, int m_q, int64_t k_c,
 extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, const double *cents,
                                  const void *cents_f16, double cent_max_norm, int64_t k_c,
                                  const int64_t *post_off, const int64_t *post_docs, int64_t n_docs,
+                                 const int64_t *chunk_bounds,
                                  int probe, int k_filter, int64_t *cand, int32_t *n_cand,
                                  void *workspace, size_t ws_bytes, void *stream) {
     DSRT_REQUIRE(probe >= 1, DSRT_EINVAL, "invalid parameter: probe must be >= 1, got %d", probe);
@@ -1098,7 +1135,7 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
                 : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc);
     if (rc) return rc;
     // eps in normalised units (|q^| = 1, |c*s| <= 1)
-    pf_theta_kernel<double><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+    pf_theta_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
         vals, static_cast<int>(w.n_split * kSHalves), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn,
         nullptr, d);
     rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
@@ -1109,7 +1146,7 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     pf_fallback_kernel<double><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d,
                                                                            P, probed);
     rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, k_c, w.row_words, counts,
-                             k_filter, cand, n_cand, cnt_ws, st);
+                             k_filter, cand, n_cand, cnt_ws, chunk_bounds, st);
     if (rc) return rc;
     DSRT_LAUNCH_CHECK();
     (void)cent_max_norm;
@@ -1188,7 +1225,7 @@ static int assign_impl(const TQ *X, int64_t n, int d, const double *cents, const
         }
         rc = launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, v, nullptr, nullptr, nullptr, idesc);
         if (rc) return rc;
-        pf_theta_kernel<TQ><<<static_cast<unsigned>((rows + 127) / 128), 128, 0, st>>>(
+        pf_theta_kernel<TQ><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
             v, static_cast<int>(n_split * kSHalves), rows, 1, static_cast<float>(2.0 * eps), theta, listn,
             raw ? X + r0 * d : nullptr, d);
         rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, tps, 1, nullptr, theta, lists, listn, idesc);

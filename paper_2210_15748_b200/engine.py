@@ -240,8 +240,18 @@ def topk_max_k() -> int:
 
 
 # ------------------------------------------------------------------- K5
+def posting_chunk_bounds(post_off, post_docs, n_docs: int, m_q: int, probe: int):
+    """Chunk boundaries of every posting for the counting pass (cache per index)."""
+    k_c = post_off.shape[0] - 1
+    n = _lib.lib().dsrt_posting_chunk_bounds_size(k_c, n_docs, m_q, probe)
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=post_off.device)
+    _lib.call("dsrt_posting_chunk_bounds", _ptr(post_off), _ptr(post_docs), k_c, n_docs, m_q, probe,
+              _ptr(out), _stream())
+    return out
+
+
 def prefilter(Q, m_q: int, centroids, post_off, post_docs, n_docs: int, probe: int,
-              k_filter: int):
+              k_filter: int, chunk_bounds=None):
     """Q (n_qsets*m_q, d) float64 -> (cand (n_qsets, k_filter) int64, n_cand (n_qsets) int32)."""
     _need(Q, torch.float64, "Q")
     _need(centroids, torch.float64, "centroids")
@@ -252,8 +262,8 @@ def prefilter(Q, m_q: int, centroids, post_off, post_docs, n_docs: int, probe: i
     ws_bytes = _lib.lib().dsrt_prefilter_workspace(n_q, m_q, k_c, n_docs, probe)
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=Q.device)
     _lib.call("dsrt_prefilter", _ptr(Q), n_q, m_q, d, _ptr(centroids), k_c, _ptr(post_off),
-              _ptr(post_docs), n_docs, probe, k_filter, _ptr(cand), _ptr(n_cand), _ptr(ws),
-              ws_bytes, _stream())
+              _ptr(post_docs), n_docs, _ptr(chunk_bounds), probe, k_filter, _ptr(cand),
+              _ptr(n_cand), _ptr(ws), ws_bytes, _stream())
     return cand, n_cand
 
 
@@ -275,7 +285,7 @@ def to_f16_rows(src: torch.Tensor, scale: float) -> torch.Tensor:
 
 
 def prefilter_tc(Q, m_q: int, centroids, cents_f16, cent_max_norm: float, post_off, post_docs,
-                 n_docs: int, probe: int, k_filter: int):
+                 n_docs: int, probe: int, k_filter: int, chunk_bounds=None):
     """Tensor-core screened prefilter (exact results); Q (n_qsets*m_q, 128) float64."""
     _need(Q, torch.float64, "Q")
     _need(centroids, torch.float64, "centroids")
@@ -286,8 +296,9 @@ def prefilter_tc(Q, m_q: int, centroids, cents_f16, cent_max_norm: float, post_o
     ws_bytes = _lib.lib().dsrt_prefilter_tc_workspace(n_q, m_q, k_c, n_docs, probe)
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device=Q.device)
     _lib.call("dsrt_prefilter_tc", _ptr(Q), n_q, m_q, d, _ptr(centroids), _ptr(cents_f16),
-              float(cent_max_norm), k_c, _ptr(post_off), _ptr(post_docs), n_docs, probe, k_filter,
-              _ptr(cand), _ptr(n_cand), _ptr(ws), ws_bytes, _stream())
+              float(cent_max_norm), k_c, _ptr(post_off), _ptr(post_docs), n_docs,
+              _ptr(chunk_bounds), probe, k_filter, _ptr(cand), _ptr(n_cand), _ptr(ws), ws_bytes,
+              _stream())
     return cand, n_cand
 
 

@@ -69,6 +69,18 @@ class CentroidIndex:
     n_docs: int
     post_off: torch.Tensor
     post_docs: torch.Tensor
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def chunk_bounds(self, m_q: int, probe: int) -> torch.Tensor:
+        """Posting chunk boundaries for the counting pass, computed once per counter
+        width (the index is immutable)."""
+        k_c = self.post_off.shape[0] - 1
+        key = 8 if m_q * min(probe, k_c) <= 255 else 16
+        t = self._cache.get(key)
+        if t is None:
+            t = engine.posting_chunk_bounds(self.post_off, self.post_docs, self.n_docs, m_q, probe)
+            self._cache[key] = t
+        return t
 
     @property
     def postings(self) -> list[np.ndarray]:
@@ -188,9 +200,10 @@ def filter_candidates_device(cindex: CentroidIndex, centroids: Centroids, Q: tor
         c16, mx = centroids.device_f16(Qd.device)
         return engine.prefilter_tc(Qd, m_q, centroids.device_vectors(Qd.device), c16, mx,
                                    cindex.post_off, cindex.post_docs, cindex.n_docs, probe,
-                                   k_filter)
+                                   k_filter, chunk_bounds=cindex.chunk_bounds(m_q, probe))
     return engine.prefilter(Qd, m_q, centroids.device_vectors(Qd.device), cindex.post_off,
-                            cindex.post_docs, cindex.n_docs, probe, k_filter)
+                            cindex.post_docs, cindex.n_docs, probe, k_filter,
+                            chunk_bounds=cindex.chunk_bounds(m_q, probe))
 
 
 def filter_candidates(index: CentroidIndex, centroids: Centroids, Q, probe: int,

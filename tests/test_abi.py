@@ -43,6 +43,7 @@ def test_errors_map_to_reference_exceptions():
         _lib.check(rc)
     rc = lib.dsrt_hash(None, 0, 1, 0, None, 0, 1, 1, None, None, None, None)
     assert rc == _lib.EINVAL and "d must be >= 1" in _lib.last_error()
-    rc = lib.dsrt_prefilter(None, 1, 1, 4, None, 4, None, None, 1, 0, 5, None, None, None, 0, None)
+    rc = lib.dsrt_prefilter(None, 1, 1, 4, None, 4, None, None, 1, None, 0, 5, None, None, None, 0,
+                            None)
     assert rc == _lib.EINVAL and _lib.last_error().startswith("invalid parameter: probe")
     assert ctypes.sizeof(ctypes.c_void_p) == 8
