@@ -528,6 +528,191 @@ __global__ void __launch_bounds__(kSelThreads)
     if (tid == 0) n_cand[qs] = outn;
 }
 
+// ---- small batches: chunk-parallel selection (the single-CTA ordered scan of
+// select_kernel would scan a whole counter row alone):
+//  plan:  per query set, c*/need from the summed chunk histograms and the
+//         number of ties (count == c*) in earlier chunks;
+//  scan:  CTA per (query set, chunk), 32-word strips per thread in doc order;
+//         ties ranked by a block scan go straight to their final slot (they
+//         follow all hits, ascending doc), hits (count > c*) are appended;
+//  final: per query set, bitonic sort of the hits by (count desc, index asc).
+struct SelPlan {
+    int32_t cstar, need, pad0, pad1;
+};
+
+__global__ void sel_plan_kernel(const uint32_t *__restrict__ chist, int nch, int max_count, int k_filter,
+                                SelPlan *__restrict__ plan, int32_t *__restrict__ tie_base,
+                                int32_t *__restrict__ hits_n) {
+    extern __shared__ uint32_t ph[];  // max_count + 1
+    const int64_t qs = blockIdx.x;
+    const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(max_count + 1);
+    for (int b = threadIdx.x; b <= max_count; b += blockDim.x) {
+        uint32_t t = 0;
+        for (int c = 0; c < nch; ++c) t += gh[c * static_cast<int64_t>(max_count + 1) + b];
+        ph[b] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t cum = 0;
+        int cstar = 1, need = static_cast<int>(ph[1]);
+        for (int c = max_count; c >= 1; --c) {
+            if (cum + ph[c] >= static_cast<uint32_t>(k_filter)) {
+                cstar = c;
+                need = static_cast<int>(k_filter - cum);
+                break;
+            }
+            cum += ph[c];
+        }
+        plan[qs] = SelPlan{cstar, need, 0, 0};
+        hits_n[qs] = 0;
+        int32_t run = 0;
+        for (int c = 0; c < nch; ++c) {
+            tie_base[qs * nch + c] = run;
+            run += static_cast<int32_t>(gh[c * static_cast<int64_t>(max_count + 1) + cstar]);
+        }
+    }
+}
+
+constexpr int kScanThreads = 512;
+
+template <int CB>
+__global__ void __launch_bounds__(kScanThreads)
+    sel_scan_kernel(const uint32_t *__restrict__ counts, int64_t row_words, int nch, int k_filter,
+                    const SelPlan *__restrict__ plan, const int32_t *__restrict__ tie_base,
+                    int32_t *__restrict__ hits_n, uint64_t *__restrict__ hits,
+                    int64_t *__restrict__ ties) {
+    constexpr int DPW = 32 / CB;
+    constexpr uint32_t MASK = (1u << CB) - 1u;
+    constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
+    constexpr int W_CH = kChunkBytes / 4;
+    constexpr int SW = W_CH / kScanThreads;  // words per thread strip
+    __shared__ int warp_tot[kScanThreads / 32];
+    const int ch = blockIdx.x;
+    const int64_t qs = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const SelPlan pl = plan[qs];
+    const uint32_t cstar = static_cast<uint32_t>(pl.cstar);
+    const int64_t w0 = static_cast<int64_t>(ch) * W_CH + static_cast<int64_t>(tid) * SW;
+    const uint32_t *row = counts + qs * row_words;
+    const uint32_t ceq = cstar * ONE, cgt = (cstar + 1) * ONE;
+    uint32_t w[SW];
+#pragma unroll
+    for (int q = 0; q < SW; q += 4) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (w0 + q + 4 <= row_words) v = *reinterpret_cast<const uint4 *>(row + w0 + q);
+        w[q] = v.x; w[q + 1] = v.y; w[q + 2] = v.z; w[q + 3] = v.w;
+    }
+    int eqn = 0;
+    uint32_t hitmask = 0;
+#pragma unroll
+    for (int q = 0; q < SW; ++q) {
+        const uint32_t x = w[q];
+        if (x == 0u) continue;
+        if (CB == 8) {
+            eqn += __popc(__vcmpeq4(x, ceq) & ONE);
+            if (cstar < MASK && __vcmpgeu4(x, cgt) != 0u) hitmask |= 1u << q;
+        } else {
+            eqn += __popc(__vcmpeq2(x, ceq) & ONE);
+            if (cstar < MASK && __vcmpgeu2(x, cgt) != 0u) hitmask |= 1u << q;
+        }
+    }
+    int x = eqn;  // block exclusive scan of the tie counts (doc order = thread order)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const int t = lane < kScanThreads / 32 ? warp_tot[lane] : 0;
+        int sx = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, sx, o);
+            if (lane >= o) sx += y;
+        }
+        if (lane < kScanThreads / 32) warp_tot[lane] = sx - t;
+    }
+    __syncthreads();
+    int rank = tie_base[qs * nch + ch] + warp_tot[warp] + (x - eqn);
+    const int need = pl.need;
+    int64_t *tout = ties + qs * k_filter;
+    const int64_t doc_w0 = w0 * DPW;
+    if (eqn > 0 && rank < need) {  // rare: rolled loops over the words (re-read via L1)
+#pragma unroll 1
+        for (int q = 0; q < SW && rank < need; ++q) {
+            const uint32_t xw = row[w0 + q];
+            if (xw == 0u) continue;
+#pragma unroll 1
+            for (int k = 0; k < DPW; ++k)
+                if (((xw >> (CB * k)) & MASK) == cstar) {
+                    if (rank < need) tout[rank] = doc_w0 + q * DPW + k;
+                    ++rank;
+                }
+        }
+    }
+    if (hitmask != 0u) {
+#pragma unroll 1
+        for (int q = 0; q < SW; ++q) {
+            if (!((hitmask >> q) & 1u)) continue;
+            const uint32_t xw = row[w0 + q];
+#pragma unroll 1
+            for (int k = 0; k < DPW; ++k) {
+                const uint32_t c = (xw >> (CB * k)) & MASK;
+                if (c > cstar) {
+                    const int slot = atomicAdd(hits_n + qs, 1);
+                    if (slot < k_filter)
+                        hits[qs * k_filter + slot] = (static_cast<uint64_t>(c) << 40) |
+                                                     (0xffffffffffull - static_cast<uint64_t>(doc_w0 + q * DPW + k));
+                }
+            }
+        }
+    }
+}
+
+constexpr int kFinThreads = 1024;
+
+// hits sorted by (count desc, index asc), then the ties (ascending doc)
+__global__ void __launch_bounds__(kFinThreads)
+    sel_final_kernel(const SelPlan *__restrict__ plan, const int32_t *__restrict__ hits_n,
+                     const uint64_t *__restrict__ hits, const int64_t *__restrict__ ties, int k_filter,
+                     int64_t *__restrict__ cand, int32_t *__restrict__ n_cand) {
+    extern __shared__ uint64_t hb[];  // pow2 >= k_filter keys
+    const int64_t qs = blockIdx.x;
+    const int tid = threadIdx.x;
+    const SelPlan pl = plan[qs];
+    const int nh = tmin(hits_n[qs], k_filter);
+    int p2 = 1;
+    while (p2 < nh) p2 <<= 1;
+    for (int i = tid; i < p2; i += blockDim.x) hb[i] = i < nh ? hits[qs * k_filter + i] : 0ull;
+    __syncthreads();
+    for (int size = 2; size <= p2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < p2; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool desc = (i & size) == 0;
+                    if ((hb[i] < hb[j]) == desc) {
+                        const uint64_t t = hb[i];
+                        hb[i] = hb[j];
+                        hb[j] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    const int nt = tmin(pl.need, k_filter - nh);
+    const int outn = nh + nt;
+    for (int i = tid; i < k_filter; i += blockDim.x) {
+        int64_t v = -1;
+        if (i < nh) v = static_cast<int64_t>(0xffffffffffull - (hb[i] & 0xffffffffffull));
+        else if (i < outn) v = ties[qs * k_filter + (i - nh)];
+        cand[qs * k_filter + i] = v;
+    }
+    if (tid == 0) n_cand[qs] = outn;
+}
+
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 // counters: uint8 when m_q*probe <= 255, else uint16; rows padded to 16 bytes
 static int counter_bits(int max_count) { return max_count <= 255 ? 8 : 16; }
@@ -540,10 +725,23 @@ static int64_t row_words_for(int64_t n_docs, int max_count) {
 static int n_chunks_for(int64_t n_docs, int max_count) {
     return static_cast<int>((n_docs + chunk_docs(counter_bits(max_count)) - 1) / chunk_docs(counter_bits(max_count)));
 }
-static size_t count_ws_bytes(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n_docs) {
+static size_t count_ws_chunks(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n_docs) {
     const int mc = m_q * P, nch = n_chunks_for(n_docs, mc);
     return align256(static_cast<size_t>(k_c) * (nch + 1) * sizeof(int64_t)) +
            align256(static_cast<size_t>(n_q) * nch * (mc + 1) * sizeof(uint32_t));
+}
+static bool small_batch(int64_t n_q) { return n_q * 8 <= sm_count(); }
+// + the small-batch selection buffers (plans, tie bases, hit counts, hits, ties)
+static size_t count_ws_bytes(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n_docs) {
+    size_t b = count_ws_chunks(n_q, m_q, P, k_c, n_docs);
+    if (small_batch(n_q)) {
+        const int nch = n_chunks_for(n_docs, m_q * P);
+        b += align256(static_cast<size_t>(n_q) * sizeof(SelPlan)) +
+             align256(static_cast<size_t>(n_q) * nch * sizeof(int32_t)) +
+             align256(static_cast<size_t>(n_q) * sizeof(int32_t)) +
+             align256(static_cast<size_t>(n_q) * kSelMax * 16);
+    }
+    return b;
 }
 
 // counts (written whole by the chunked pass; no memset) -> candidates.  cws:
@@ -570,6 +768,30 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
     DSRT_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
     ck<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kCntThreads, csmem, st>>>(
         probed, m_q * P, bnd, nch, post_docs, row_words, max_count, counts, chist);
+    if (small_batch(n_q)) {  // chunk-parallel selection: plan -> chunk scans -> final sort
+        uint8_t *sws = cws + count_ws_chunks(n_q, m_q, P, k_c, n_docs);
+        SelPlan *plan = reinterpret_cast<SelPlan *>(sws);
+        sws += align256(static_cast<size_t>(n_q) * sizeof(SelPlan));
+        int32_t *tie_base = reinterpret_cast<int32_t *>(sws);
+        sws += align256(static_cast<size_t>(n_q) * nch * sizeof(int32_t));
+        int32_t *hits_n = reinterpret_cast<int32_t *>(sws);
+        sws += align256(static_cast<size_t>(n_q) * sizeof(int32_t));
+        uint64_t *hits = reinterpret_cast<uint64_t *>(sws);
+        int64_t *ties = reinterpret_cast<int64_t *>(hits + static_cast<size_t>(n_q) * k_filter);
+        sel_plan_kernel<<<static_cast<unsigned>(n_q), 128, (max_count + 1) * sizeof(uint32_t), st>>>(
+            chist, nch, max_count, k_filter, plan, tie_base, hits_n);
+        auto sk = cb == 8 ? sel_scan_kernel<8> : sel_scan_kernel<16>;
+        sk<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kScanThreads, 0, st>>>(
+            counts, row_words, nch, k_filter, plan, tie_base, hits_n, hits, ties);
+        int p2 = 1;
+        while (p2 < k_filter) p2 <<= 1;
+        const size_t fsmem = static_cast<size_t>(p2) * sizeof(uint64_t);
+        DSRT_CUDA(cudaFuncSetAttribute(sel_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+        sel_final_kernel<<<static_cast<unsigned>(n_q), kFinThreads, fsmem, st>>>(plan, hits_n, hits, ties,
+                                                                                  k_filter, cand, n_cand);
+        DSRT_LAUNCH_CHECK();
+        return DSRT_OK;
+    }
     const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1 + kSelWarps * kSelBins) * sizeof(uint32_t);
     if (cb == 8) {
         DSRT_CUDA(cudaFuncSetAttribute(select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -557,6 +557,32 @@ def test_add_sets_with_prefilter_equals_full_build():
     assert d.query_batch(full, Q, 10) == d.query_batch(part, Q, 10)
 
 
+def test_prefilter_small_and_large_batch_paths_agree():
+    """The chunk-parallel selection (small batches) and the single-CTA ordered scan
+    (large batches) give the oracle's candidates; many ties at c* (low k_filter)."""
+    from paper_2210_15748_b200 import prefilter as pf
+    rng = np.random.default_rng(12)
+    dd, k = 128, 300
+    C = rng.standard_normal((k, dd))
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    docs = [rng.standard_normal((int(rng.integers(1, 10)), dd)) for _ in range(200_000 // 50)]
+    cents = d.Centroids(k=k, seed=0, vectors=C)
+    cindex = d.build_centroid_index(docs, cents)
+    post = cindex.postings
+    n_q, m_q = 40, 16
+    Q = rng.standard_normal((n_q * m_q, dd))
+    for probe, k_filter in ((2, 7), (4, 300), (3, 4096)):
+        big, nb = pf.filter_candidates_device(cindex, cents, torch.from_numpy(Q).to(DEV), m_q, probe,
+                                              k_filter)
+        for q in range(n_q):
+            want = O.filter_candidates(post, len(docs), C, Q[q * m_q:(q + 1) * m_q], probe, k_filter)
+            np.testing.assert_array_equal(big[q, : int(nb[q])].cpu().numpy(), want)
+            one, n1 = pf.filter_candidates_device(cindex, cents,
+                                                  torch.from_numpy(Q[q * m_q:(q + 1) * m_q]).to(DEV),
+                                                  m_q, probe, k_filter)
+            np.testing.assert_array_equal(one[0, : int(n1[0])].cpu().numpy(), want)
+
+
 def test_filtered_query_matches_reference_pipeline():
     """build_index with the prefilter on: candidates from K5, then K3/K4 over them,
     equals the oracle pipeline given the same centroids and postings."""
