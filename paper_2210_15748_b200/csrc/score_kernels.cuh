@@ -27,6 +27,7 @@ namespace dsrt {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+
 template <int QPL>
 struct SlotGeom {
     static constexpr int kRow = 32 * QPL + 4;  // bytes per slot row (+4: bank skew)
@@ -140,14 +141,17 @@ __device__ __forceinline__ int mismatches(const uint32_t (&q)[K * W], const uint
 // vectors share one 3-input min (VIMNMX3): 8 LOP3 + 0.5 min per (query,
 // vector) at C = 8 instead of 8 + 1; for W = 2 ptxas already fuses the
 // two-word add with the min (VIADDMNMX).
-template <int K, int W, int QPL>
+// PU: unroll of the W = 1 pair loop (4 in candidate mode: one query set per
+// warp needs more vectors in flight; 2 in exhaustive mode, where register
+// blocking of several query sets already provides them)
+template <int K, int W, int QPL, int PU = 2>
 __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], int (&rmin)[QPL],
                                              const uint32_t *xs, int nv) {
     constexpr int R = ((K * W) + 3) & ~3;
     const uint4 *x4 = reinterpret_cast<const uint4 *>(xs);
     int i = 0;
     if constexpr (W == 1) {
-#pragma unroll 2
+#pragma unroll PU
         for (; i + 2 <= nv; i += 2) {
             uint4 xa[R / 4], xb[R / 4];
 #pragma unroll
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         const int b = static_cast<int>(consumed % kBufs);
         mbar_wait(&bars[b], static_cast<uint32_t>(consumed / kBufs) & 1);
         const int64_t nvec = tmin<int64_t>(PV, cvend - cv);
-        if (nvec > 0) scan_vectors<K, W, QPL>(q, rmin, bufs + b * (PV * R), static_cast<int>(nvec));
+        if (nvec > 0) scan_vectors<K, W, QPL, 4>(q, rmin, bufs + b * (PV * R), static_cast<int>(nvec));
         ++consumed;
         cv += nvec;
         if (cv >= cvend) {  // candidate complete
