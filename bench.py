@@ -448,6 +448,12 @@ def run_cfg4(args):
     per_launch_sets = min(n_sets, chunk)
     traffic4, traffic4_src = _ncu_traffic("cfg4", per_launch_sets / 1_000_000 * n_q / 1024)
     alg4 = rec_bytes * per_launch_sets / n_sets + n_q * per_launch_sets * 8
+    # e2e: one query_batch call (public API) with pinned host query vectors and host results
+    Qh = Qv.cpu().pin_memory()
+    te = time.perf_counter()
+    s_e, i_e = d.query_batch(idx, Qh.to(dev, non_blocking=True), top_k, return_tensors=True)
+    hs, hi = s_e.cpu(), i_e.cpu()
+    e2e_s = time.perf_counter() - te
     line = {
         "metric": "set-pair scores/sec (cfg4: 8M sets x 1024 query sets, L=32 C=8, exhaustive, top-1000)",
         "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -466,6 +472,10 @@ def run_cfg4(args):
                      "per_step": {"compares": compares, "code_bytes_per_pass": rec_bytes},
                      "achieved_hbm_gbs_code_stream": rec_bytes / (k_ms * 1e-3) / 1e9,
                      "peak_source": "measured in-run: LOP3 lane-ops/s x 4", "int_microbench": mb},
+        "e2e": {"value": n_q * n_sets / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": Qh.numel() * Qh.element_size(),
+                "d2h_bytes_per_step": hs.numel() * 8 + hi.numel() * 8, "ms_per_step": e2e_s * 1e3,
+                "path": "query_batch (hash -> chunked exhaustive scoring -> top-k merge)"},
         "clocks": clk, "gpu_launches": (2 + 2 * launches_per_step) * args.steps,
     }
     del so
@@ -671,6 +681,23 @@ def run_cfg2(args):
     mma_flops = 2 * alg_flops  # hi/lo planes: two MMA chains
     hbm_bytes = n_vec * (128 * 2 + L + engine.record_words(L, C) * 4)
     traffic2, traffic2_src = _ncu_traffic("cfg2", n_vec / 4_000_000)
+    # e2e: the public build path from pinned host vectors (H2D inside the timed region),
+    # reading back the last set offset
+    import paper_2210_15748_b200 as dd
+    Xh = X.cpu().pin_memory()
+    cfg_e = dd.IndexConfig(d=128, C=C, L=L, seed=0, filter=dd.FilterConfig(enabled=False))
+    ids_e = np.arange(len(sizes))
+    dd.build_from_vectors(Xh.to(dev, non_blocking=True), sizes, ids_e, cfg_e, keep_codes=True,
+                          hash_mode=mode)
+    torch.cuda.synchronize()
+    n_e2e = 5
+    te = time.perf_counter()
+    for _ in range(n_e2e):
+        ie = dd.build_from_vectors(Xh.to(dev, non_blocking=True), sizes, ids_e, cfg_e,
+                                   keep_codes=True, hash_mode=mode)
+        tail = int(ie.set_off[-1].item())
+    e2e_s = (time.perf_counter() - te) / n_e2e
+    del ie, tail
     line = {
         "metric": "index-build vectors/sec (cfg2: 10M bf16 vectors, L=64 C=7, hash + CSR layout)",
         "value": n_vec / (ms * 1e-3), "unit": "vectors/s", "n_gpus": 1, "steps": args.steps,
@@ -696,6 +723,10 @@ def run_cfg2(args):
         "hash_bit_flips": {"sample_vectors": int(len(samp)), "bits": int(flips.size),
                            "flips": int(flips.sum()), "outside_band": int((flips & ~band).sum()),
                            "band_fraction": float(band.mean())},
+        "e2e": {"value": n_vec / e2e_s, "unit": "vectors/s",
+                "h2d_bytes_per_step": Xh.numel() * Xh.element_size(), "d2h_bytes_per_step": 8,
+                "ms_per_step": e2e_s * 1e3,
+                "path": "build_from_vectors (pinned host bf16 -> device, hash, layout)"},
         "clocks": clk, "gpu_launches": 4 * args.steps,
     }
     print(json.dumps(line))

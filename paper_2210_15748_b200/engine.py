@@ -215,10 +215,17 @@ def train_centroids(samples: torch.Tensor, k: int, iters: int, init_idx):
 
 # ------------------------------------------------------------------- K4
 def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None):
-    """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D)."""
-    _need(scores, torch.float64, "scores")
-    rows, ld = scores.shape
-    n = ld if n is None else n
+    """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D).
+
+    ``scores`` may be a row-strided view (unit column stride), e.g. the first
+    columns of a wider score buffer; the kernel reads rows at stride ld."""
+    if not scores.is_cuda or scores.dtype != torch.float64:
+        raise ValueError("invalid parameter: scores must be a float64 CUDA tensor")
+    if scores.dim() != 2 or (scores.shape[1] > 1 and scores.stride(1) != 1):
+        raise ValueError("invalid parameter: scores must be 2-D with unit column stride")
+    rows, width = scores.shape
+    ld = scores.stride(0) if rows > 1 else width
+    n = width if n is None else n
     ids_ld = 0
     if ids is not None:
         if ids.dtype not in (torch.int64, torch.uint64):

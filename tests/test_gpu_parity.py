@@ -583,6 +583,23 @@ def test_prefilter_small_and_large_batch_paths_agree():
             np.testing.assert_array_equal(one[0, : int(n1[0])].cpu().numpy(), want)
 
 
+def test_chunked_exhaustive_partial_last_chunk(monkeypatch):
+    """rank_records with a score buffer smaller than N (last chunk partial, row-strided
+    view into the buffer) equals the unchunked ranking."""
+    from paper_2210_15748_b200 import index as I
+    rng = np.random.default_rng(21)
+    L, C = 32, 6
+    sizes = rng.integers(1, 40, size=1003)
+    codes = rng.integers(0, 64, size=(int(sizes.sum()), L)).astype(np.int32)
+    cfg = d.IndexConfig(d=4, C=C, L=L, filter=d.FilterConfig(enabled=False))
+    idx = d.build_from_codes(torch.from_numpy(codes).to(DEV), sizes, rng.permutation(5000)[:1003], cfg)
+    qc = rng.integers(0, 64, size=(16, 24, L))
+    want = d.query_codes_batch(idx, qc, 37)
+    monkeypatch.setattr(I, "SCORE_BUFFER_BYTES", 8 * 16 * 300)  # 300-set chunks -> 4 chunks
+    got = d.query_codes_batch(idx, qc, 37)
+    assert got == want
+
+
 def test_filtered_query_matches_reference_pipeline():
     """build_index with the prefilter on: candidates from K5, then K3/K4 over them,
     equals the oracle pipeline given the same centroids and postings."""
