@@ -600,6 +600,39 @@ def test_chunked_exhaustive_partial_last_chunk(monkeypatch):
     assert got == want
 
 
+def test_top_k_beyond_selector(monkeypatch):
+    """top_k > 4096 (device two-key stable sort), exhaustive, chunked and from a
+    candidate list, equals heapq ranking of the oracle scores (ties by doc id)."""
+    from paper_2210_15748_b200 import index as I
+    rng = np.random.default_rng(31)
+    L, C, N = 16, 3, 6000
+    sizes = rng.integers(1, 6, size=N)
+    codes = rng.integers(0, 8, size=(int(sizes.sum()), L)).astype(np.int32)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    ids = rng.permutation(100_000)[:N]
+    cfg = d.IndexConfig(d=4, C=C, L=L, filter=d.FilterConfig(enabled=False))
+    idx = d.build_from_codes(torch.from_numpy(codes).to(DEV), sizes, ids, cfg)
+    qc = rng.integers(0, 8, size=(2, 5, L))
+    scores = c_oracle.score(codes.astype(np.int64), off, qc, idx.lookup.table)
+    for k in (4097, 5000, N + 10):
+        want = [O.rank_topk(scores[r], ids, k) for r in range(2)]
+        assert d.query_codes_batch(idx, qc, k) == want
+        monkeypatch.setattr(I, "SCORE_BUFFER_BYTES", 8 * 2 * 2500)  # chunked
+        assert d.query_codes_batch(idx, qc, k) == want
+        monkeypatch.undo()
+    # candidate lists (prefilter output form) with k above the selector
+    cand = torch.from_numpy(np.stack([rng.permutation(N)[:4500] for _ in range(2)])).to(DEV)
+    n_cand = torch.tensor([4500, 4321], dtype=torch.int32, device=DEV)
+    qrecs, _ = d.engine.codes_to_records(torch.from_numpy(qc.reshape(-1, L).astype(np.int32)).to(DEV), L, C)
+    out_s, out_i = I.rank_records(idx, qrecs, 5, 4400, cand=cand, n_cand=n_cand)
+    for r in range(2):
+        cr = cand[r, : int(n_cand[r])].cpu().numpy()
+        want = O.rank_topk(scores[r][cr], ids[cr], 4400)
+        got_s, got_i = out_s[r].cpu().numpy(), out_i[r].cpu().numpy()
+        valid = got_s >= 0
+        assert [(int(a), float(b)) for a, b in zip(got_i[valid], got_s[valid])] == want
+
+
 def test_filtered_query_matches_reference_pipeline():
     """build_index with the prefilter on: candidates from K5, then K3/K4 over them,
     equals the oracle pipeline given the same centroids and postings."""
