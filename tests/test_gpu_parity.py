@@ -656,6 +656,35 @@ def test_filtered_query_matches_reference_pipeline():
         assert got == want
 
 
+@pytest.mark.parametrize("phi", ["identity", "debiased-sigmoid"])
+def test_filtered_avgphi_query_matches_oracle_pipeline(phi):
+    """avg-phi + weights behind the prefilter (candidate lists with n_cand padding,
+    K3a streaming kernel) through query / query_batch vs the oracle pipeline."""
+    from paper_2210_15748_b200 import scoring
+    rng = np.random.default_rng(81)
+    docs = [(i, rng.standard_normal((int(rng.integers(2, 40)), 16))) for i in range(500)]
+    cfg = d.IndexConfig(d=16, C=4, L=32, seed=1, inner_kind="avg-phi", phi=phi,
+                        filter=d.FilterConfig(enabled=True, centroids=24, probe=2, k_filter=60))
+    idx = d.build_index(docs, cfg)
+    cents, cindex = idx.filter
+    post = cindex.postings
+    codes = idx.codes.cpu().numpy()
+    off = idx.set_off.cpu().numpy()
+    table = scoring.phi_function(phi)(O.sim_lut(4, 32))
+    Qs = rng.standard_normal((5, 12, 16))
+    w = rng.uniform(0, 1, size=12)
+    sc = d.Scorer(d.avg_phi_aggregation(phi), w)
+    batch = d.query_batch(idx, Qs, 10, scorer=sc)
+    for t in range(5):
+        cand = O.filter_candidates(post, 500, cents.vectors, Qs[t], 2, 60)
+        qc = O.hash_matrix(idx.family.planes, 32, 4, Qs[t])
+        s_w = O.score_sets_dense_agg(qc, codes, off, table, "avg-phi", w, sets=cand)
+        want_w = O.rank_topk(s_w, [int(i) for i in idx.doc_ids[cand]], 10)
+        assert batch[t] == want_w
+        s0 = O.score_sets_dense_agg(qc, codes, off, table, "avg-phi", None, sets=cand)
+        assert d.query(idx, Qs[t], top_k=10) == O.rank_topk(s0, [int(i) for i in idx.doc_ids[cand]], 10)
+
+
 # ------------------------------------------------------------ larger shapes
 def test_cfg1_shape_sampled_parity():
     """cfg1 shapes (L=64, C=7, m_i ~ N(70,20) clipped) at 20k sets: 16 query sets
