@@ -19,14 +19,17 @@ concurrent queries on different streams are safe.
 
 from __future__ import annotations
 
+import gc
 import math
+import os
+import threading
 from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
 
 from . import engine
-from .lsh import (SimLookup, SrpFamily, build_sim_lookup, hash_device, sample_srp_family,
+from .lsh import (SimLookup, SrpFamily, build_sim_lookup, default_mode, hash_device, sample_srp_family,
                   to_device_matrix)
 from . import scoring
 from .scoring import Scorer, avg_phi_aggregation, default_scorer, max_aggregation
@@ -108,6 +111,7 @@ class DessertIndex:
     codes: torch.Tensor | None
     lut_dev: torch.Tensor
     doc_ids_dev: torch.Tensor
+    _graphs: dict = field(default_factory=dict, repr=False, compare=False)
 
     @property
     def n_docs(self) -> int:
@@ -444,6 +448,90 @@ def rank_records(index: DessertIndex, qrecs: torch.Tensor, m_q: int, top_k: int,
     return out_s, out_i
 
 
+# ------------------------------------------------- CUDA-graph query path
+# query() on one query set is a fixed sequence of ~12 small kernels; replaying
+# it as a CUDA graph removes the host launch overhead from batch-1 latency.
+# A graph is captured per (query shape, dtype, top_k, probe, k_filter) and is
+# rebuilt when the index's device buffers or prefilter change (add_sets,
+# filter reassignment).  DSRT_QUERY_GRAPHS=0 disables the path.
+_GRAPH_CACHE = 8
+
+
+class _QueryGraph:
+    # Holds the captured tensors (deps) but not the index itself: an index <-> graph
+    # reference cycle would leave dropped indexes to the cyclic GC, which could then
+    # destroy their graphs (and free their pools) in the middle of another capture.
+    def __init__(self, index: DessertIndex, q: torch.Tensor, top_k: int, probe, k_filter):
+        self.top_k, self.probe, self.k_filter = top_k, probe, k_filter
+        self.deps = self._deps(index)
+        self.lock = threading.Lock()
+        self.q_in = torch.empty(q.shape, dtype=q.dtype, device=index.device)
+        self.q_in.copy_(q)
+        self._run(index)  # eager warm-up: lazy initialisation outside the capture
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        gc_on = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+                self.out = self._run(index)
+        finally:
+            if gc_on:
+                gc.enable()
+
+    @staticmethod
+    def _deps(index):
+        return (index.records, index.set_off, index.lut_dev, index.doc_ids_dev, index.filter)
+
+    def valid(self, index) -> bool:
+        return all(a is b for a, b in zip(self.deps, self._deps(index)))
+
+    def _run(self, ix: DessertIndex):
+        Qdev = to_device_matrix(self.q_in, ix.config.d, ix.device)
+        mode = default_mode(Qdev.dtype, Qdev.shape[1], ix.config.C, Qdev.shape[0])
+        _, qrecs, zero = engine.hash_vectors(Qdev, ix.family.device_planes(mode, ix.device), mode,
+                                             ix.config.L, ix.config.C, want_codes=False,
+                                             want_records=True, check_zero=True)
+        m_q = Qdev.shape[0]
+        cand = n_cand = None
+        if ix.filter is not None:
+            cand, n_cand = _candidates(ix, Qdev, m_q, self.probe, self.k_filter)
+        out_s, out_i = rank_records(ix, qrecs, m_q, self.top_k, cand, n_cand)
+        return out_s, out_i, zero, n_cand
+
+    def __call__(self, q: torch.Tensor):
+        self.q_in.copy_(q)
+        self.graph.replay()
+        return tuple(None if t is None else t.cpu() for t in self.out)
+
+
+def _query_graphed(index: DessertIndex, Qa, top_k: int, probe, k_filter):
+    """query() through a cached CUDA graph; None when the graph is busy (another
+    thread) so the caller runs the eager path."""
+    q = Qa if isinstance(Qa, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(Qa))
+    key = (tuple(q.shape), q.dtype, top_k, probe, k_filter)
+    g = index._graphs.get(key)
+    if g is not None and not g.valid(index):
+        index._graphs.pop(key, None)
+        g = None
+    if g is None:
+        if len(index._graphs) >= _GRAPH_CACHE:
+            index._graphs.pop(next(iter(index._graphs)))
+        g = _QueryGraph(index, q, top_k, probe, k_filter)
+        index._graphs[key] = g
+    if not g.lock.acquire(blocking=False):
+        return None
+    try:
+        out_s, out_i, zero, n_cand = g(q)
+    finally:
+        g.lock.release()
+    if int(zero[0]) != 0:
+        raise ValueError("zero vector cannot be hashed (sign of zero projection undefined)")
+    if n_cand is not None and int(n_cand[0]) == 0:
+        return []
+    return _results(out_s, out_i)[0]
+
+
 def query(index: DessertIndex, Q, top_k: int, probe: int | None = None,
           k_filter: int | None = None, scorer: Scorer | None = None,
           threads: int = 1) -> RankedResults:
@@ -457,10 +545,15 @@ def query(index: DessertIndex, Q, top_k: int, probe: int | None = None,
     Qa = Q if isinstance(Q, torch.Tensor) else np.asarray(Q, dtype=np.float64)
     if Qa.ndim != 2 or Qa.shape[0] == 0:
         raise ValueError("empty query: need at least one query vector")
+    plan = score_plan(index, scorer, Qa.shape[0])
+    if (plan is None and index.device.type == "cuda" and Qa.shape[1] == index.config.d
+            and os.environ.get("DSRT_QUERY_GRAPHS", "1") != "0"):
+        res = _query_graphed(index, Qa, top_k, probe, k_filter)
+        if res is not None:
+            return res
     Qdev = to_device_matrix(Qa, index.config.d, index.device)
     _, qrecs = hash_device(index.family, Qdev, want_codes=False)
     m_q = Qdev.shape[0]
-    plan = score_plan(index, scorer, m_q)
     cand = n_cand = None
     if index.filter is not None:
         cand, n_cand = _candidates(index, Qdev, m_q, probe, k_filter)

@@ -633,6 +633,40 @@ def test_top_k_beyond_selector(monkeypatch):
         assert [(int(a), float(b)) for a, b in zip(got_i[valid], got_s[valid])] == want
 
 
+def test_query_graph_invalidation_and_threads(monkeypatch):
+    """query() runs through a cached CUDA graph: it must follow add_sets / filter
+    changes, agree with the eager path, and stay correct under concurrent threads."""
+    import threading
+    rng = np.random.default_rng(44)
+    docs = [(i, rng.standard_normal((int(rng.integers(1, 15)), 32))) for i in range(300)]
+    cfg = d.IndexConfig(d=32, C=5, L=32, seed=4, filter=d.FilterConfig(enabled=False))
+    full = d.build_index(docs, cfg)
+    part = d.build_index(docs[:150], cfg)
+    Qs = [rng.standard_normal((7, 32)) for _ in range(12)]
+    before = [d.query(part, q, 9) for q in Qs]           # graphs captured on `part`
+    d.add_sets(part, docs[150:])
+    after = [d.query(part, q, 9) for q in Qs]
+    assert after == [d.query(full, q, 9) for q in Qs]
+    monkeypatch.setenv("DSRT_QUERY_GRAPHS", "0")
+    assert after == [d.query(part, q, 9) for q in Qs]     # eager path agrees
+    assert before != after
+    monkeypatch.delenv("DSRT_QUERY_GRAPHS")
+    results = {}
+
+    def worker(t):
+        for r in range(20):
+            i = (t * 7 + r) % len(Qs)
+            results[(t, r)] = (i, d.query(full, Qs[i], 9))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for i, res in results.values():
+        assert res == after[i]
+
+
 def test_filtered_query_matches_reference_pipeline():
     """build_index with the prefilter on: candidates from K5, then K3/K4 over them,
     equals the oracle pipeline given the same centroids and postings."""
