@@ -487,29 +487,40 @@ class _QueryGraph:
         return all(a is b for a, b in zip(self.deps, self._deps(index)))
 
     def _run(self, ix: DessertIndex):
-        Qdev = to_device_matrix(self.q_in, ix.config.d, ix.device)
+        q = self.q_in
+        m_q = q.shape[-2]
+        Qdev = to_device_matrix(q.reshape(-1, q.shape[-1]), ix.config.d, ix.device)
         mode = default_mode(Qdev.dtype, Qdev.shape[1], ix.config.C, Qdev.shape[0])
         _, qrecs, zero = engine.hash_vectors(Qdev, ix.family.device_planes(mode, ix.device), mode,
                                              ix.config.L, ix.config.C, want_codes=False,
                                              want_records=True, check_zero=True)
-        m_q = Qdev.shape[0]
         cand = n_cand = None
         if ix.filter is not None:
             cand, n_cand = _candidates(ix, Qdev, m_q, self.probe, self.k_filter)
         out_s, out_i = rank_records(ix, qrecs, m_q, self.top_k, cand, n_cand)
         return out_s, out_i, zero, n_cand
 
-    def __call__(self, q: torch.Tensor):
-        self.q_in.copy_(q)
+    def __call__(self, q: torch.Tensor, to_host: bool = True):
+        self.q_in.copy_(q, non_blocking=True)
         self.graph.replay()
-        return tuple(None if t is None else t.cpu() for t in self.out)
+        if to_host:
+            return tuple(None if t is None else t.cpu() for t in self.out)
+        return tuple(None if t is None else t.clone() for t in self.out)
 
 
-def _query_graphed(index: DessertIndex, Qa, top_k: int, probe, k_filter):
-    """query() through a cached CUDA graph; None when the graph is busy (another
-    thread) so the caller runs the eager path."""
+def _graph_ok(index: DessertIndex, n_q: int) -> bool:
+    """Graphs pin their scratch: used for the prefiltered path and for exhaustive
+    scoring whose score buffer stays small."""
+    return (index.device.type == "cuda" and os.environ.get("DSRT_QUERY_GRAPHS", "1") != "0"
+            and (index.filter is not None or n_q * index.n_docs * 8 <= (256 << 20)))
+
+
+def _query_graphed(index: DessertIndex, Qa, top_k: int, probe, k_filter, to_host: bool = True):
+    """query() / query_batch() through a cached CUDA graph; None when the graph is
+    busy (another thread) so the caller runs the eager path.  Returns
+    (out_s, out_i, n_cand) on the host (to_host) or as device copies."""
     q = Qa if isinstance(Qa, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(Qa))
-    key = (tuple(q.shape), q.dtype, top_k, probe, k_filter)
+    key = (tuple(q.shape), q.dtype, str(q.device), top_k, probe, k_filter)
     g = index._graphs.get(key)
     if g is not None and not g.valid(index):
         index._graphs.pop(key, None)
@@ -522,14 +533,12 @@ def _query_graphed(index: DessertIndex, Qa, top_k: int, probe, k_filter):
     if not g.lock.acquire(blocking=False):
         return None
     try:
-        out_s, out_i, zero, n_cand = g(q)
+        out_s, out_i, zero, n_cand = g(q, to_host)
     finally:
         g.lock.release()
-    if int(zero[0]) != 0:
+    if int(zero[0].item() if zero.is_cuda else zero[0]) != 0:
         raise ValueError("zero vector cannot be hashed (sign of zero projection undefined)")
-    if n_cand is not None and int(n_cand[0]) == 0:
-        return []
-    return _results(out_s, out_i)[0]
+    return out_s, out_i, n_cand
 
 
 def query(index: DessertIndex, Q, top_k: int, probe: int | None = None,
@@ -546,11 +555,13 @@ def query(index: DessertIndex, Q, top_k: int, probe: int | None = None,
     if Qa.ndim != 2 or Qa.shape[0] == 0:
         raise ValueError("empty query: need at least one query vector")
     plan = score_plan(index, scorer, Qa.shape[0])
-    if (plan is None and index.device.type == "cuda" and Qa.shape[1] == index.config.d
-            and os.environ.get("DSRT_QUERY_GRAPHS", "1") != "0"):
+    if plan is None and Qa.shape[1] == index.config.d and _graph_ok(index, 1):
         res = _query_graphed(index, Qa, top_k, probe, k_filter)
         if res is not None:
-            return res
+            out_s, out_i, n_cand = res
+            if n_cand is not None and int(n_cand[0]) == 0:
+                return []
+            return _results(out_s, out_i)[0]
     Qdev = to_device_matrix(Qa, index.config.d, index.device)
     _, qrecs = hash_device(index.family, Qdev, want_codes=False)
     m_q = Qdev.shape[0]
@@ -581,6 +592,11 @@ def query_batch(index: DessertIndex, Qs, top_k: int, probe: int | None = None,
         raise ValueError("empty query: need at least one query vector")
     n_q, m_q, d = t.shape
     plan = score_plan(index, scorer, m_q)
+    if plan is None and d == index.config.d and _graph_ok(index, n_q):
+        res = _query_graphed(index, t, top_k, probe, k_filter, to_host=not return_tensors)
+        if res is not None:
+            out_s, out_i, _ = res
+            return (out_s, out_i) if return_tensors else _results(out_s, out_i)
     Qdev = to_device_matrix(t.reshape(n_q * m_q, d), index.config.d, index.device)
     _, qrecs = hash_device(index.family, Qdev, want_codes=False)
     cand = n_cand = None
