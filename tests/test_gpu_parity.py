@@ -719,6 +719,44 @@ def test_filtered_avgphi_query_matches_oracle_pipeline(phi):
         assert d.query(idx, Qs[t], top_k=10) == O.rank_topk(s0, [int(i) for i in idx.doc_ids[cand]], 10)
 
 
+@pytest.mark.parametrize("seed", range(24))
+def test_random_shapes_sweep(seed):
+    """Randomised (L, C, m_q, set sizes) sweep through every scoring entry point,
+    bit-exact against the C oracle (scores and integer max counts) and the heapq
+    ranking; hot codes make collisions and ties frequent."""
+    rng = np.random.default_rng(1000 + seed)
+    L = int(rng.choice([1, 5, 8, 16, 31, 32, 33, 48, 63, 64, 65, 96, 127, 128]))
+    C = int(rng.integers(1, 17))
+    while C * ((L + 31) // 32) > 32:
+        C = int(rng.integers(1, 17))
+    m_q = int(rng.choice([1, 2, 7, 8, 9, 31, 32, 33, 64, 100, 128, 129, 257]))
+    n_sets = int(rng.integers(1, 120))
+    sizes = rng.integers(1, int(rng.choice([3, 40, 300])) + 1, size=n_sets)
+    r = 1 << C
+    hot = rng.integers(0, r, size=L)
+    codes = rng.integers(0, r, size=(int(sizes.sum()), L))
+    m = rng.random(codes.shape) < rng.uniform(0.2, 0.9)
+    codes[m] = np.broadcast_to(hot, codes.shape)[m]
+    n_q = int(rng.choice([1, 3, 8, 11]))
+    qc = rng.integers(0, r, size=(n_q, m_q, L))
+    qm = rng.random(qc.shape) < rng.uniform(0.2, 0.9)
+    qc[qm] = np.broadcast_to(hot, qc.shape)[qm]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    idx = _index_from_codes(codes, sizes, L, C)
+    lut = O.sim_lut(C, L)
+    want, wmc = c_oracle.score(codes, off, qc, lut, want_counts=True)
+    got, mc = d.score_matrix(idx, qc, want_counts=True)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    np.testing.assert_array_equal(mc.cpu().numpy().astype(np.int64).reshape(wmc.shape), wmc)
+    sets = np.stack([rng.permutation(n_sets)[: max(1, n_sets // 2)] for _ in range(n_q)])
+    got2, _ = d.score_matrix(idx, qc, sets=sets)
+    np.testing.assert_array_equal(got2.cpu().numpy(), np.take_along_axis(want, sets, axis=1))
+    k = int(rng.integers(1, n_sets + 3))
+    res = d.query_codes_batch(idx, qc, k)
+    for q in range(n_q):
+        assert res[q] == O.rank_topk(want[q], np.arange(n_sets), k)
+
+
 # ------------------------------------------------------------ larger shapes
 def test_cfg1_shape_sampled_parity():
     """cfg1 shapes (L=64, C=7, m_i ~ N(70,20) clipped) at 20k sets: 16 query sets
