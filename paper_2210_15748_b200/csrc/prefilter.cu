@@ -973,7 +973,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
         for (int j = 0; j < PT; ++j) tv[j] = -INFINITY;
         float worst = -INFINITY;  // tv[P-1]
-        const float th = (PASS == 1 && row_ok) ? theta[row] : INFINITY;
+        const float th = (PASS != 0 && row_ok) ? theta[row] : INFINITY;
+        int nsub = 0;  // PASS 2: candidates of this (row, split, half)
         int it = 0;
         for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
             const int acc = it & 1;
@@ -1027,9 +1028,16 @@ __global__ void __launch_bounds__(kSThreads, 1)
                         for (int j = 0; j < 32; ++j) {
                             const float v = __uint_as_float(r[j]);
                             if (v >= th) {
-                                const int slot = atomicAdd(list_n + row, 1);
-                                if (slot < kCandMax)
-                                    lists[row * kCandMax + slot] = ScreenCand{v, static_cast<int32_t>(id0 + c0 + j)};
+                                if (PASS == 2) {  // own sub-list per (row, split, half): no atomics
+                                    if (nsub < kCandMax)
+                                        lists[(((row * gridDim.y + blockIdx.y) * kSHalves + half) * kCandMax) + nsub] =
+                                            ScreenCand{v, static_cast<int32_t>(id0 + c0 + j)};
+                                    ++nsub;
+                                } else {
+                                    const int slot = atomicAdd(list_n + row, 1);
+                                    if (slot < kCandMax)
+                                        lists[row * kCandMax + slot] = ScreenCand{v, static_cast<int32_t>(id0 + c0 + j)};
+                                }
                             }
                         }
                     }
@@ -1039,6 +1047,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (PASS == 2 && row_ok) list_n[(row * gridDim.y + blockIdx.y) * kSHalves + half] = nsub;
         if (PASS == 0 && row_ok) {
             // one partial list per (split, column half): n_split * kSHalves lists per row
             float *o = out_vals + ((row * gridDim.y + blockIdx.y) * kSHalves + half) * kMaxPtc;
@@ -1134,6 +1143,56 @@ __global__ void pf_rerank_kernel(const ScreenCand *__restrict__ lists, const int
     warp_topP_merge(es, ei, ex, eid, P);
     if (lane < P) probed[row * P + lane] = ei;
     if (best != nullptr && lane == 0) best[row] = es;  // P == 1: the exact top similarity
+}
+
+// as pf_rerank_kernel, for the prefilter's per-writer sub-lists (pass 2): a row's
+// W = n_split * kSHalves sub-lists are compacted into a 32-entry staging row
+// (overflow of the total -> exact fallback), then re-ranked in float64.
+template <typename TQ>
+__global__ void pf_rerank_sub_kernel(const ScreenCand *__restrict__ sub, const int32_t *__restrict__ sub_n, int W,
+                                     const TQ *__restrict__ Q, const double *__restrict__ cents,
+                                     int64_t n_rows, int d, int P, int32_t *__restrict__ probed,
+                                     int32_t *__restrict__ fallback) {
+    __shared__ ScreenCand stage[8][kCandMax];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (row >= n_rows) return;
+    int total = 0;
+    for (int w0 = 0; w0 < W; w0 += 32) {
+        const int w = w0 + lane;
+        const int cnt = w < W ? sub_n[row * W + w] : 0;
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int base = total + incl - cnt;
+        for (int i = 0; i < cnt && base + i < kCandMax; ++i)
+            stage[warp][base + i] = sub[(row * W + w) * static_cast<int64_t>(kCandMax) + i];
+        total += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    if (total > kCandMax || total < P) {
+        if (lane == 0) fallback[row] = 1;
+        return;
+    }
+    if (lane == 0) fallback[row] = 0;
+    double ex = -INFINITY;
+    int eid = 0x7fffffff;
+    if (lane < total) {
+        const int c = stage[warp][lane].id;
+        const TQ *q = Q + row * d;
+        const double *cv = cents + static_cast<int64_t>(c) * d;
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) acc = fma(as_f64(q[k]), cv[k], acc);
+        ex = acc;
+        eid = c;
+    }
+    double es = -INFINITY;
+    int ei = 0x7fffffff;
+    warp_topP_merge(es, ei, ex, eid, P);
+    if (lane < P) probed[row * P + lane] = ei;
 }
 
 // exact float64 scan for flagged rows (one CTA per row; rare)
@@ -1288,8 +1347,9 @@ static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int 
     w.q16 = align256(static_cast<size_t>(m_tiles * 128) * 128 * 2);
     w.screen = align256(static_cast<size_t>(rows) * w.n_split * kSHalves * kMaxPtc * sizeof(float));
     w.theta = align256(static_cast<size_t>(rows) * sizeof(float));
-    w.lists = align256(static_cast<size_t>(rows) * kCandMax * sizeof(ScreenCand));
-    w.listn = align256(static_cast<size_t>(rows) * sizeof(int32_t));
+    // per-writer candidate sub-lists: (row, split, column half) x kCandMax
+    w.lists = align256(static_cast<size_t>(rows) * w.n_split * kSHalves * kCandMax * sizeof(ScreenCand));
+    w.listn = align256(static_cast<size_t>(rows) * w.n_split * kSHalves * sizeof(int32_t));
     w.probed = align256(static_cast<size_t>(rows) * P * sizeof(int32_t));
     w.fallback = align256(static_cast<size_t>(rows) * sizeof(int32_t));
     w.counts = align256(static_cast<size_t>(n_q) * w.row_words * sizeof(uint32_t));
@@ -1360,11 +1420,11 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     pf_theta_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
         vals, static_cast<int>(w.n_split * kSHalves), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn,
         nullptr, d);
-    rc = launch_screen<1, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
+    rc = launch_screen<2, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
                              listn, idesc);
     if (rc) return rc;
-    pf_rerank_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
-        lists, listn, Q, cents, rows, d, P, probed, fallback);
+    pf_rerank_sub_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+        lists, listn, static_cast<int>(w.n_split * kSHalves), Q, cents, rows, d, P, probed, fallback);
     pf_fallback_kernel<double><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d,
                                                                            P, probed);
     rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, k_c, w.row_words, counts,
