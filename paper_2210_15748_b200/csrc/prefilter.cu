@@ -172,31 +172,6 @@ __global__ void merge_kernel(const Cand *__restrict__ in, int64_t n_rows, int n_
     if (lane < P) probed[row * P + lane] = ti;
 }
 
-// one warp per (query set, query vector, probe slot): +1 per posting entry.
-// counts: uint16 pairs packed in uint32 words, per query set a row of
-// ceil(n_docs/2) words.
-__global__ void count_kernel(const int32_t *__restrict__ probed, int64_t n_q, int m_q, int P,
-                             const int64_t *__restrict__ post_off,
-                             const int64_t *__restrict__ post_docs, int64_t row_words,
-                             uint32_t *__restrict__ counts, int cbits) {
-    const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t total = n_q * m_q * P;
-    if (w >= total) return;
-    const int64_t qs = w / (static_cast<int64_t>(m_q) * P);
-    const int c = probed[w];
-    if (c < 0 || c == 0x7fffffff) return;
-    const int64_t lo = post_off[c], hi = post_off[c + 1];
-    uint32_t *row = counts + qs * row_words;
-    for (int64_t i = lo + lane; i < hi; i += 32) {
-        const int64_t doc = post_docs[i];
-        if (cbits == 8)
-            atomicAdd(row + (doc >> 2), 1u << (8 * (doc & 3)));
-        else
-            atomicAdd(row + (doc >> 1), 1u << (16 * (doc & 1)));
-    }
-}
-
 // ---- chunked counting: CTA per (query set, doc chunk), counters in shared memory
 constexpr int kChunkBytes = 64 * 1024;  // counters per CTA (3 CTAs per SM)
 constexpr int kCntThreads = 512;
@@ -299,16 +274,13 @@ __device__ __forceinline__ uint32_t count_of(const uint32_t *row, int64_t doc) {
     return (row[doc >> 1] >> (16 * (doc & 1))) & 0xffffu;
 }
 
-// one CTA per query set.  Counters are uint16 pairs in uint32 words; every
-// thread handles 8 consecutive docs per uint4 load.
-//  pass 1: count histogram (per-warp privatised bins, only touched docs);
-//  c* = largest c with #(count > c) + hist[c] >= k_filter;
-//  pass 2 (ascending doc order, 8192 docs per step): take every doc with
-//  count > c*, and the first `need` docs with count == c* (block-wide
-//  exclusive scan of the per-thread tie counts); bitonic sort by
-//  (count desc, index asc) in shared memory.
-constexpr int kSelWarps = kSelThreads / 32;
-constexpr int kSelBins = 130;  // per-warp histogram bins (counts >= 129 clamp; exact bins via fallback)
+// Large batches: one CTA per query set.  Counters are u8 (u16) lanes of uint32
+// words.  The count histogram is the sum of the counting pass's chunk
+// histograms; c* = largest c with #(count > c) + hist[c] >= k_filter.  One
+// ordered pass (ascending doc order, 4 x uint4 per thread per step) takes every
+// doc with count > c* and the first `need` docs with count == c* (block-wide
+// exclusive scan of the per-thread tie counts); then a bitonic sort by (count
+// desc, index asc) in shared memory.
 
 template <int CB>  // counter bits: 8 or 16
 __global__ void __launch_bounds__(kSelThreads)
@@ -321,17 +293,11 @@ __global__ void __launch_bounds__(kSelThreads)
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t *buf = reinterpret_cast<uint64_t *>(smem);                    // kSelMax keys
     uint32_t *hist = reinterpret_cast<uint32_t *>(buf + kSelMax);          // max_count+1
-    uint32_t *whist = hist + (max_count + 1);                              // kSelWarps x kSelBins
     __shared__ int s_cstar, s_need, s_slot, s_eq_run, s_eq_step;
     __shared__ int warp_tot[32];
     const int64_t qs = blockIdx.x;
     const uint32_t *row = counts + qs * row_words;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool small_bins = max_count < kSelBins;
-    for (int i = tid; i <= max_count; i += blockDim.x) hist[i] = 0;
-    if (small_bins)
-        for (int i = tid; i < kSelWarps * kSelBins; i += blockDim.x) whist[i] = 0;
-    __syncthreads();
     // each thread owns 4 consecutive uint4 groups per step (4*DPG docs, 64 B):
     // four independent loads in flight, ascending doc order across threads
     constexpr int G = 4;
@@ -348,8 +314,7 @@ __global__ void __launch_bounds__(kSelThreads)
         }
     };
     const int64_t per_step = static_cast<int64_t>(blockDim.x) * G;
-    uint32_t *myh = whist + warp * kSelBins;
-    if (chist != nullptr) {  // histogram from the chunked counting pass
+    {  // global histogram = sum of the chunk histograms of the counting pass
         const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(max_count + 1);
         for (int b = tid; b <= max_count; b += blockDim.x) {
             uint32_t t = 0;
@@ -357,60 +322,6 @@ __global__ void __launch_bounds__(kSelThreads)
             hist[b] = t;
         }
         __syncthreads();
-    } else {
-    // counts 1..3 (the bulk of the touched docs) are counted with SIMD byte /
-    // half-word compares in registers; only counts >= 4 use shared atomics
-    constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
-    uint32_t h1 = 0, h2 = 0, h3 = 0;
-    for (int64_t base = 0; base < n_groups; base += per_step) {
-        const int64_t g0 = base + static_cast<int64_t>(tid) * G;
-        uint32_t w[4 * G];
-        load_groups(g0, w);  // rows are zero-padded past n_docs: no bounds checks
-#pragma unroll
-        for (int q = 0; q < 4 * G; ++q) {
-            const uint32_t x = w[q];
-            if (x == 0u) continue;  // most words hold no touched doc
-            if (CB == 8) {
-                h1 += __popc(__vcmpeq4(x, ONE) & ONE);
-                h2 += __popc(__vcmpeq4(x, 2 * ONE) & ONE);
-                h3 += __popc(__vcmpeq4(x, 3 * ONE) & ONE);
-                if (__vcmpgeu4(x, 4 * ONE) == 0u) continue;
-            } else {
-                h1 += __popc(__vcmpeq2(x, ONE) & ONE);
-                h2 += __popc(__vcmpeq2(x, 2 * ONE) & ONE);
-                h3 += __popc(__vcmpeq2(x, 3 * ONE) & ONE);
-                if (__vcmpgeu2(x, 4 * ONE) == 0u) continue;
-            }
-#pragma unroll
-            for (int k = 0; k < DPW; ++k) {
-                const uint32_t c = (x >> (CB * k)) & MASK;
-                if (c >= 4) {
-                    if (small_bins) atomicAdd(&myh[c], 1u);
-                    else atomicAdd(&hist[tmin<uint32_t>(c, static_cast<uint32_t>(max_count))], 1u);
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
-        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
-        h3 += __shfl_xor_sync(0xffffffffu, h3, o);
-    }
-    if (lane == 0) {
-        uint32_t *dst = small_bins ? myh : hist;
-        if (max_count >= 1) atomicAdd(&dst[1], h1);
-        if (max_count >= 2) atomicAdd(&dst[2], h2);
-        if (max_count >= 3) atomicAdd(&dst[3], h3);
-    }
-    __syncthreads();
-    if (small_bins)
-        for (int b = tid; b <= max_count; b += blockDim.x) {
-            uint32_t t = 0;
-            for (int wv = 0; wv < kSelWarps; ++wv) t += whist[wv * kSelBins + b];
-            hist[b] = t;
-        }
-    __syncthreads();
     }
     if (tid == 0) {
         int64_t cum = 0;
@@ -792,7 +703,7 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
         DSRT_LAUNCH_CHECK();
         return DSRT_OK;
     }
-    const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1 + kSelWarps * kSelBins) * sizeof(uint32_t);
+    const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1) * sizeof(uint32_t);
     if (cb == 8) {
         DSRT_CUDA(cudaFuncSetAttribute(select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         select_kernel<8><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
