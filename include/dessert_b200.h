@@ -100,6 +100,15 @@ int dsrt_tinytable(const void *codes, int code_bytes, const int64_t *set_off, in
                    int C, int32_t *offsets_out, int32_t *ids_out, void *stream);
 
 /*
+ * accumulate_collisions(_batch) (sketch.py:92-153) on one TinyTable:
+ * counts[q, j] = |{t : stored code of j in table t == qcodes[q, t]}|.
+ * offsets (L, r+1), ids (L, m), qcodes (m_q, L) as int32 (codes validated by
+ * the caller); counts (m_q, m) int32.
+ */
+int dsrt_collision_counts(const int32_t *offsets, const int32_t *ids, int L, int r, int m,
+                          const int32_t *qcodes, int m_q, int32_t *counts, void *stream);
+
+/*
  * K3 -- replaces _score_one/_score_chunk/score_candidate (index.py:183-261) for
  * sigma = max with default weights:
  *   score = pairwise_sum_f64(lut[c_q], q < m_q) / m_q,

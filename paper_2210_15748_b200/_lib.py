@@ -55,6 +55,7 @@ SIGNATURES = {
     "dsrt_dsri_scan_sets": (_i64, [_vp, _sz, _sz, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "dsrt_dsri_decode_sets": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i64, _vp, _i32, _vp, _vp]),
     "dsrt_varints_to_postings": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "dsrt_collision_counts": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "dsrt_topk": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_topk_max_k": (_i32, []),
     "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _i32, _i32,

@@ -207,6 +207,35 @@ __global__ void tinytable_kernel(const TC *__restrict__ codes, const int64_t *__
 
 using namespace dsrt;
 
+namespace dsrt {
+// accumulate_collisions_batch (sketch.py:118-153) on a TinyTable: thread per
+// (query row, table) adds 1 to every stored vector in bucket (t, code).
+__global__ void collision_counts_kernel(const int32_t *__restrict__ offsets, const int32_t *__restrict__ ids,
+                                        int L, int r, int m, const int32_t *__restrict__ qcodes, int m_q,
+                                        int32_t *__restrict__ counts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= static_cast<int64_t>(m_q) * L) return;
+    const int q = static_cast<int>(i / L), t = static_cast<int>(i % L);
+    const int h = qcodes[static_cast<int64_t>(q) * L + t];
+    const int lo = offsets[static_cast<int64_t>(t) * (r + 1) + h];
+    const int hi = offsets[static_cast<int64_t>(t) * (r + 1) + h + 1];
+    for (int p = lo; p < hi; ++p) atomicAdd(counts + static_cast<int64_t>(q) * m + ids[static_cast<int64_t>(t) * m + p], 1);
+}
+}  // namespace dsrt
+
+extern "C" int dsrt_collision_counts(const int32_t *offsets, const int32_t *ids, int L, int r, int m,
+                                     const int32_t *qcodes, int m_q, int32_t *counts, void *stream) {
+    DSRT_REQUIRE(L >= 1 && r >= 1 && m >= 1 && m_q >= 0, DSRT_EINVAL, "invalid parameter: L=%d r=%d m=%d", L, r, m);
+    if (m_q == 0) return DSRT_OK;
+    cudaStream_t st = as_stream(stream);
+    DSRT_CUDA(cudaMemsetAsync(counts, 0, static_cast<size_t>(m_q) * m * sizeof(int32_t), st));
+    const int64_t n = static_cast<int64_t>(m_q) * L;
+    collision_counts_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(offsets, ids, L, r, m, qcodes,
+                                                                                 m_q, counts);
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+
 extern "C" int dsrt_tinytable(const void *codes, int code_bytes, const int64_t *set_off, int64_t set,
                               int L, int C, int32_t *offsets_out, int32_t *ids_out, void *stream) {
     DSRT_REQUIRE(L >= 1 && C >= 1 && C <= 24, DSRT_EINVAL, "invalid parameter: L=%d C=%d", L, C);

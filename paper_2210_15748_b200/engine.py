@@ -213,6 +213,13 @@ def train_centroids(samples: torch.Tensor, k: int, iters: int, init_idx):
     return out
 
 
+def collision_counts(offsets, ids, L: int, r: int, m: int, qcodes, out):
+    """TinyTable bucket gather: out (m_q, m) int32 collision counts."""
+    _lib.call("dsrt_collision_counts", _ptr(offsets), _ptr(ids), L, r, m, _ptr(qcodes),
+              qcodes.shape[0], _ptr(out), _stream())
+    return out
+
+
 # ------------------------------------------------------------------- K4
 def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None):
     """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D).

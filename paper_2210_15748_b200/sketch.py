@@ -75,6 +75,55 @@ def build_tiny_table(codes_per_vector, L: int, r: int, device="cuda") -> TinyTab
                      ids=ids.cpu().numpy().astype(_id_dtype(m)))
 
 
+def bucket(table: TinyTable, t: int, h: int) -> np.ndarray:
+    """sketch.py:83-89: the vector ids stored in bucket (t, h), a zero-copy view."""
+    if not 0 <= t < table.L:
+        raise IndexError(f"table index out of range: t={t}, L={table.L}")
+    if not 0 <= h < table.r:
+        raise IndexError(f"hash value out of range: h={h}, r={table.r}")
+    return table.ids[t, int(table.offsets[t, h]): int(table.offsets[t, h + 1])]
+
+
+def _collision_counts(table: TinyTable, codes: np.ndarray, device="cuda") -> np.ndarray:
+    """counts[q, j] on the device (dsrt_collision_counts): bucket gather per (q, t)."""
+    off = torch.from_numpy(np.ascontiguousarray(table.offsets, dtype=np.int32)).to(device)
+    ids = torch.from_numpy(np.ascontiguousarray(table.ids, dtype=np.int32)).to(device)
+    q = torch.from_numpy(np.ascontiguousarray(codes, dtype=np.int32)).to(device)
+    out = torch.empty((codes.shape[0], table.m), dtype=torch.int32, device=device)
+    engine.collision_counts(off, ids, table.L, table.r, table.m, q, out)
+    return out.cpu().numpy()
+
+
+def accumulate_collisions(table: TinyTable, query_codes, out: np.ndarray | None = None) -> np.ndarray:
+    """sketch.py:92-115: per stored vector, the number of tables colliding with one
+    query vector's L codes; ``out`` may supply a buffer of length >= m."""
+    codes = np.asarray(query_codes)
+    if codes.shape != (table.L,):
+        raise ValueError(f"expected {table.L} query codes, got shape {codes.shape}")
+    if codes.min() < 0 or codes.max() >= table.r:
+        raise ValueError(f"code out of range: codes must lie in [0, {table.r})")
+    counts = _collision_counts(table, codes[None, :])[0]
+    if out is None:
+        return counts
+    out[: table.m] = counts
+    return out[: table.m]
+
+
+def accumulate_collisions_batch(table: TinyTable, query_codes, out: np.ndarray | None = None) -> np.ndarray:
+    """sketch.py:118-153: row q = accumulate_collisions(table, query_codes[q]);
+    ``out`` may supply a (>= m_q, >= m) buffer."""
+    codes = np.asarray(query_codes)
+    if codes.ndim != 2 or codes.shape[1] != table.L:
+        raise ValueError(f"expected (m_q, {table.L}) code matrix, got shape {codes.shape}")
+    if codes.min() < 0 or codes.max() >= table.r:  # empty input raises here, as numpy does
+        raise ValueError(f"code out of range: codes must lie in [0, {table.r})")
+    counts = _collision_counts(table, codes)
+    if out is None:
+        return counts
+    out[: codes.shape[0], : table.m] = counts
+    return out[: codes.shape[0], : table.m]
+
+
 class SketchView:
     """Lazy ``index.sketches``: len() and [i] -> TinyTable exported from the device."""
 
