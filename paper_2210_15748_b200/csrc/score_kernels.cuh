@@ -150,7 +150,40 @@ __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], in
     constexpr int R = ((K * W) + 3) & ~3;
     const uint4 *x4 = reinterpret_cast<const uint4 *>(xs);
     int i = 0;
-    if constexpr (W == 1) {
+    if constexpr (W == 1 && PU == 4) {
+        // pointer-walked groups of 4 vectors: loads at immediate offsets, one
+        // add + compare per group instead of re-deriving the address from i
+        const uint4 *p = x4;
+        const uint4 *const pend = x4 + (nv & ~3) * (R / 4);
+        for (; p != pend; p += 4 * (R / 4)) {
+            uint4 xv[4][R / 4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+#pragma unroll
+                for (int u = 0; u < R / 4; ++u) xv[g][u] = p[g * (R / 4) + u];
+#pragma unroll
+            for (int s = 0; s < QPL; ++s) {
+                const int m0 = __vimin3_s32(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xv[0])),
+                                            mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xv[1])));
+                rmin[s] = __vimin3_s32(m0, mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xv[2])),
+                                       mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xv[3])));
+            }
+        }
+        i = nv & ~3;
+        if (nv & 2) {
+            uint4 xa[R / 4], xb[R / 4];
+#pragma unroll
+            for (int u = 0; u < R / 4; ++u) {
+                xa[u] = x4[i * (R / 4) + u];
+                xb[u] = x4[(i + 1) * (R / 4) + u];
+            }
+#pragma unroll
+            for (int s = 0; s < QPL; ++s)
+                rmin[s] = __vimin3_s32(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)),
+                                       mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xb)));
+            i += 2;
+        }
+    } else if constexpr (W == 1) {
 #pragma unroll PU
         for (; i + 2 <= nv; i += 2) {
             uint4 xa[R / 4], xb[R / 4];
@@ -344,8 +377,14 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
 }
 
 // --------------------------------------------------------- candidate lists
-constexpr int kPieceBytes = 3072;  // per-warp staging piece
-constexpr int kBufs = 3;           // per-warp ring depth
+#ifndef DSRT_PIECE_BYTES
+#define DSRT_PIECE_BYTES 3072
+#endif
+#ifndef DSRT_CAND_BUFS
+#define DSRT_CAND_BUFS 3
+#endif
+constexpr int kPieceBytes = DSRT_PIECE_BYTES;  // per-warp staging piece
+constexpr int kBufs = DSRT_CAND_BUFS;          // per-warp ring depth
 constexpr int kCandWarps = 8;
 
 template <int K, int W>
@@ -440,14 +479,18 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     // candidate base + l (vbeg = vend = 0 for an invalid set index), loaded in
     // one batch per 32 candidates instead of a dependent load chain per set.
     const int64_t *cand_row = cand ? cand + qset * cand_ld : nullptr;
-    CandWin pwin, cwin;
+    CandWin pwin;
     // producer iterator (lane-uniform state; lane 0 issues the copies)
     int64_t pe = e_lo, pv, pvend;
     pwin.get(pe, e_hi, cand_row, set_off, n_sets, pv, pvend);
-    if (pvend < 0) { pv = 0; pvend = 0; }
-    int64_t issued = 0;
-    auto issue = [&]() {  // issue the next piece (pe, [pv, ..)) into buffer issued % kBufs
-        const int b = static_cast<int>(issued % kBufs);
+    const bool pvalid0 = pvend >= 0;
+    if (!pvalid0) { pv = 0; pvend = 0; }
+    int issued = 0, consumed = 0, pb = 0;  // pb = issued % kBufs
+    bool pvalid = pvalid0;
+    constexpr uint32_t kDone = 1u << 16, kValid = 1u << 17;
+    auto issue = [&]() -> uint32_t {  // next piece (pe, [pv, ..)) into buffer pb; returns its metadata
+        const int b = pb;
+        pb = pb + 1 == kBufs ? 0 : pb + 1;
         const int64_t nvec = pe < e_hi ? tmin<int64_t>(PV, pvend - pv) : 0;
         if (lane == 0) {
             const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);
@@ -461,30 +504,35 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         }
         ++issued;
         pv += nvec;
+        uint32_t meta = static_cast<uint32_t>(nvec);
         if (pe < e_hi && pv >= pvend) {  // advance to the next candidate
+            meta |= kDone | (pvalid ? kValid : 0u);
             ++pe;
             if (pe < e_hi) {
                 pwin.get(pe, e_hi, cand_row, set_off, n_sets, pv, pvend);
-                if (pvend < 0) { pv = 0; pvend = 0; }
+                pvalid = pvend >= 0;
+                if (!pvalid) { pv = 0; pvend = 0; }
             }
         }
+        return meta;
     };
-    // consumer iterator
-    int64_t ce = e_lo, cv, cvend, slot_col = e_lo;
-    cwin.get(ce, e_hi, cand_row, set_off, n_sets, cv, cvend);
-    bool cvalid = cvend >= 0;
-    if (!cvalid) { cv = 0; cvend = 0; }
-    int64_t consumed = 0;
-    for (int i = 0; i < kBufs; ++i) issue();
+    // Consumer: replays the producer's piece sequence from metadata the
+    // producer recorded at issue time (meta[0] = the oldest outstanding
+    // piece: nvec | kDone | kValid), so the per-piece bookkeeping is a
+    // register rotation instead of a second walk over the candidate list.
+    int64_t ce = e_lo, slot_col = e_lo;
+    uint32_t meta[kBufs];
+#pragma unroll
+    for (int i = 0; i < kBufs; ++i) meta[i] = issue();
+    int b = 0;
+    uint32_t phase = 0;
     while (ce < e_hi) {
-        const int b = static_cast<int>(consumed % kBufs);
-        mbar_wait(&bars[b], static_cast<uint32_t>(consumed / kBufs) & 1);
-        const int64_t nvec = tmin<int64_t>(PV, cvend - cv);
-        if (nvec > 0) scan_vectors<K, W, QPL, 4>(q, rmin, bufs + b * (PV * R), static_cast<int>(nvec));
-        ++consumed;
-        cv += nvec;
-        if (cv >= cvend) {  // candidate complete
-            slots.push(rmin, L, m_q, cvalid);
+        mbar_wait(&bars[b], phase);
+        const uint32_t m0 = meta[0];
+        const int nvec = static_cast<int>(m0 & 0xffffu);
+        if (nvec > 0) scan_vectors<K, W, QPL, 4>(q, rmin, bufs + b * (PV * R), nvec);
+        if (m0 & kDone) {  // candidate complete
+            slots.push(rmin, L, m_q, (m0 & kValid) != 0);
 #pragma unroll
             for (int i = 0; i < QPL; ++i) rmin[i] = L;
             if (slots.n == 32) {
@@ -492,22 +540,21 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
                 slot_col += 32;
             }
             ++ce;
-            if (ce < e_hi) {
-                cwin.get(ce, e_hi, cand_row, set_off, n_sets, cv, cvend);
-                cvalid = cvend >= 0;
-                if (!cvalid) { cv = 0; cvend = 0; }
-            }
         }
         __syncwarp();
-        issue();  // refill the buffer just consumed
+#pragma unroll
+        for (int i = 0; i + 1 < kBufs; ++i) meta[i] = meta[i + 1];
+        meta[kBufs - 1] = issue();  // refill the buffer just consumed
+        ++consumed;
+        if (++b == kBufs) { b = 0; phase ^= 1u; }
     }
     if (slots.n > 0)
         slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
     // drain: wait for outstanding pieces so no bulk copy outlives the CTA
     while (consumed < issued) {
-        const int b = static_cast<int>(consumed % kBufs);
-        mbar_wait(&bars[b], static_cast<uint32_t>(consumed / kBufs) & 1);
+        mbar_wait(&bars[b], phase);
         ++consumed;
+        if (++b == kBufs) { b = 0; phase ^= 1u; }
     }
 }
 
