@@ -82,6 +82,19 @@ struct Slots {
         ++n;
     }
 
+    // split-lane layout (QPL == 1): lanes l and l + 16 hold queries l and
+    // l + 16 after the half-warp combine; lanes < 16 write both
+    __device__ __forceinline__ void push_split(const int (&rmin)[2], int L, int m_q, bool ok) {
+        const int lane = threadIdx.x & 31;
+        uint8_t *row = buf + n * SlotGeom<QPL>::kRow;
+        if (lane < 16) {
+            if (lane < m_q) row[lane] = static_cast<uint8_t>(L - rmin[0]);
+            if (lane + 16 < m_q) row[lane + 16] = static_cast<uint8_t>(L - rmin[1]);
+        }
+        valid |= (ok ? 1u : 0u) << n;
+        ++n;
+    }
+
     // lane i < n scores slot i -> out[col0 + i]; optional uint16 max counts
     __device__ __forceinline__ void flush(int m_q, const double *__restrict__ lut_s,
                                           const double *__restrict__ w_s,
@@ -135,6 +148,72 @@ __device__ __forceinline__ int mismatches(const uint32_t (&q)[K * W], const uint
         mm += __popc(acc);
     }
     return mm;
+}
+
+// Split-lane candidate mapping (m_q in (16, 32]): lane l holds queries
+// (l & 15) and (l & 15) + 16, and half-warp h = l >> 4 scans the set vectors
+// 2p + h, so every broadcast LDS feeds two pairs per lane; the halves are
+// combined (shfl_xor 16) when the set ends.
+template <int K, int W>
+__device__ __forceinline__ void load_queries_split(uint32_t (&q)[2][K * W],
+                                                   const uint32_t *__restrict__ qrecs, int64_t qset,
+                                                   int m_q) {
+    constexpr int R = ((K * W) + 3) & ~3;
+    const int l = threadIdx.x & 15;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const int qi = l + 16 * s;
+        const bool ok = qi < m_q;
+        const uint32_t *src = qrecs + (qset * m_q + (ok ? qi : 0)) * R;
+#pragma unroll
+        for (int i = 0; i < K * W; ++i) q[s][i] = ok ? __ldg(src + i) : 0u;
+    }
+}
+
+template <int K, int W>
+__device__ __forceinline__ int min3(int a, int b, int c) {
+    if constexpr (W == 1) return __vimin3_s32(a, b, c);
+    else return min(a, min(b, c));
+}
+
+template <int K, int W>
+__device__ __forceinline__ void scan_split(const uint32_t (&q)[2][K * W], int (&rmin)[2],
+                                           const uint32_t *xs, int nv) {
+    constexpr int R = ((K * W) + 3) & ~3;
+    const int h = (threadIdx.x >> 4) & 1;
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(xs) + h * (R / 4);
+    const int np = nv >> 1;  // full vector pairs; half h takes vector 2p + h
+    int p = 0;
+#pragma unroll 2
+    for (; p + 2 <= np; p += 2) {
+        uint4 xa[R / 4], xb[R / 4];
+#pragma unroll
+        for (int u = 0; u < R / 4; ++u) {
+            xa[u] = x4[(2 * p) * (R / 4) + u];
+            xb[u] = x4[(2 * p + 2) * (R / 4) + u];
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            rmin[s] = min3<K, W>(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)),
+                                 mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xb)));
+    }
+    if (p < np) {
+        uint4 xa[R / 4];
+#pragma unroll
+        for (int u = 0; u < R / 4; ++u) xa[u] = x4[(2 * p) * (R / 4) + u];
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            rmin[s] = min(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)));
+    }
+    if (nv & 1) {  // the odd last vector: both halves take it (min is idempotent)
+        const uint4 *xl = reinterpret_cast<const uint4 *>(xs) + (nv - 1) * (R / 4);
+        uint4 xa[R / 4];
+#pragma unroll
+        for (int u = 0; u < R / 4; ++u) xa[u] = xl[u];
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            rmin[s] = min(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)));
+    }
 }
 
 // Process vectors [0, nv) of a shared-memory record array.  For W = 1 two
@@ -430,7 +509,7 @@ struct CandWin {
 #ifndef DSRT_CAND_MINB
 #define DSRT_CAND_MINB 2
 #endif
-template <int K, int W, int QPL>
+template <int K, int W, int QPL, bool SPLIT = false>
 __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     score_cand_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
                       int64_t n_sets, const int64_t *__restrict__ cand,
@@ -467,11 +546,14 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     const int64_t e_hi = tmin(e_lo + run_len, nc);
     if (e_lo >= e_hi) return;
 
-    uint32_t q[QPL][K * W];
-    load_queries<K, W, QPL>(q, qrecs, qset, m_q, true);
-    int rmin[QPL];
+    static_assert(!SPLIT || QPL == 1, "split-lane mapping covers m_q <= 32");
+    constexpr int QR = SPLIT ? 2 : QPL;  // query vectors held per lane
+    uint32_t q[QR][K * W];
+    if constexpr (SPLIT) load_queries_split<K, W>(q, qrecs, qset, m_q);
+    else load_queries<K, W, QPL>(q, qrecs, qset, m_q, true);
+    int rmin[QR];
 #pragma unroll
-    for (int s = 0; s < QPL; ++s) rmin[s] = L;
+    for (int s = 0; s < QR; ++s) rmin[s] = L;
     Slots<QPL> slots{slot_mem + warp * SlotGeom<QPL>::kBytes};
     double *out_row = scores != nullptr ? scores + qset * cand_ld : nullptr;
 
@@ -530,11 +612,20 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         mbar_wait(&bars[b], phase);
         const uint32_t m0 = meta[0];
         const int nvec = static_cast<int>(m0 & 0xffffu);
-        if (nvec > 0) scan_vectors<K, W, QPL, 4>(q, rmin, bufs + b * (PV * R), nvec);
+        if (nvec > 0) {
+            if constexpr (SPLIT) scan_split<K, W>(q, rmin, bufs + b * (PV * R), nvec);
+            else scan_vectors<K, W, QPL, 4>(q, rmin, bufs + b * (PV * R), nvec);
+        }
         if (m0 & kDone) {  // candidate complete
-            slots.push(rmin, L, m_q, (m0 & kValid) != 0);
+            if constexpr (SPLIT) {
 #pragma unroll
-            for (int i = 0; i < QPL; ++i) rmin[i] = L;
+                for (int i = 0; i < 2; ++i) rmin[i] = min(rmin[i], __shfl_xor_sync(kFull, rmin[i], 16));
+                slots.push_split(rmin, L, m_q, (m0 & kValid) != 0);
+            } else {
+                slots.push(rmin, L, m_q, (m0 & kValid) != 0);
+            }
+#pragma unroll
+            for (int i = 0; i < QR; ++i) rmin[i] = L;
             if (slots.n == 32) {
                 slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
                 slot_col += 32;
@@ -586,14 +677,14 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
     return DSRT_OK;
 }
 
-template <int K, int W, int QPL>
+template <int K, int W, int QPL, bool SPLIT = false>
 static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_sets,
                        const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
                        const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
                        const double *weights, double *scores, uint16_t *mc, int mc_stride,
                        int mc_q0, cudaStream_t st) {
     const size_t smem = cand_smem_static<QPL>() + (L + 1 + m_q) * sizeof(double);
-    auto kern = score_cand_kernel<K, W, QPL>;
+    auto kern = score_cand_kernel<K, W, QPL, SPLIT>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     DSRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCandWarps * 32, smem));
@@ -637,10 +728,17 @@ struct ScoreArgs {
 
 template <int K, int W, int QPL>
 static int run_one(const ScoreArgs &a, cudaStream_t st) {
-    if (a.cand_mode)
+    if (a.cand_mode) {
+        if constexpr (QPL == 1 && W <= 2 && K <= 8) {
+            if (a.m_q > 16 && a.qs_override != -1)  // split-lane mapping (-1 forces the plain one)
+                return launch_cand<K, W, QPL, true>(a.recs, a.set_off, a.n_sets, a.cand, a.n_cand,
+                                                    a.cand_ld, a.qrecs, a.n_qsets, a.m_q, a.L, a.lut,
+                                                    a.weights, a.scores, a.mc, a.mc_stride, a.mc_q0, st);
+        }
         return launch_cand<K, W, QPL>(a.recs, a.set_off, a.n_sets, a.cand, a.n_cand, a.cand_ld,
                                       a.qrecs, a.n_qsets, a.m_q, a.L, a.lut, a.weights, a.scores, a.mc,
                                       a.mc_stride, a.mc_q0, st);
+    }
     // register-block several query sets per warp when there are enough of them
     if constexpr (QPL == 1 && W <= 2 && K <= 8) {
         const int qs = a.qs_override > 0 ? a.qs_override : (a.n_qsets >= 256 ? (W == 1 ? 4 : 2) : 1);

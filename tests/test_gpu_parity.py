@@ -417,6 +417,54 @@ def test_agg_random_long_sets_vs_oracle():
         np.testing.assert_array_equal(got.cpu().numpy()[0], want)
 
 
+@pytest.mark.parametrize("L,C", [(32, 7), (64, 7), (32, 8), (16, 3)])
+def test_candidate_split_lane_mapping(L, C, monkeypatch):
+    """Candidate lists with 16 < m_q <= 32 take the split-lane kernel (two query
+    vectors per lane, half-warps on alternate set vectors).  Odd / even / 1-vector
+    sets, sets spanning several staging pieces, duplicate and invalid candidates,
+    uint16 max counts; equal to the oracle and to the plain mapping (DSRT_QS=-1)."""
+    rng = np.random.default_rng(L * 100 + C)
+    r = 1 << C
+    sizes = np.concatenate([[1, 2, 3, 4, 5, 96, 97, 191, 193, 300], rng.integers(1, 140, size=50)])
+    hot = rng.integers(0, r, size=L)
+    codes = rng.integers(0, r, size=(int(sizes.sum()), L))
+    mask = rng.random(codes.shape) < 0.6
+    codes[mask] = np.broadcast_to(hot, codes.shape)[mask]
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    idx = _index_from_codes(codes, sizes, L, C)
+    N = len(sizes)
+    for m_q in (17, 24, 31, 32):
+        n_q = 5
+        qc = rng.integers(0, r, size=(n_q, m_q, L))
+        qm = rng.random(qc.shape) < 0.6
+        qc[qm] = np.broadcast_to(hot, qc.shape)[qm]
+        sets = np.stack([rng.permutation(N)[:40] for _ in range(n_q)])
+        sets[0, 3] = sets[0, 4]  # a duplicate candidate
+        want = c_oracle.score(codes.astype(np.int64), off, qc, idx.lookup.table, sets=sets)
+        got, _ = d.score_matrix(idx, qc, sets=sets)
+        np.testing.assert_array_equal(got.cpu().numpy(), want, err_msg=f"m_q={m_q}")
+        monkeypatch.setenv("DSRT_QS", "-1")
+        plain, _ = d.score_matrix(idx, qc, sets=sets)
+        monkeypatch.delenv("DSRT_QS")
+        np.testing.assert_array_equal(plain.cpu().numpy(), want)
+        # raw ABI: invalid set index -> NaN, max counts
+        qrecs, _ = engine.codes_to_records(torch.from_numpy(qc.reshape(-1, L).astype(np.int32)).to(DEV), L, C)
+        cand = torch.from_numpy(sets).to(DEV).clone()
+        cand[1, 0] = N + 5
+        n_cand = torch.tensor([40, 39, 1, 0, 40], dtype=torch.int32, device=DEV)
+        out, mc = engine.score_candidates(idx.records, idx.set_off, qrecs, m_q, L, C, idx.lut_dev,
+                                          cand, n_cand, want_counts=True)
+        o = out.cpu().numpy()
+        assert np.isnan(o[1, 0])
+        for q, n in enumerate([40, 39, 1, 0, 40]):
+            lo = 1 if q == 1 else 0
+            np.testing.assert_array_equal(o[q, lo:n], want[q, lo:n])
+        cnt = c_oracle.score(codes.astype(np.int64), off, qc, idx.lookup.table, sets=sets,
+                             want_counts=True)[1]
+        np.testing.assert_array_equal(mc.cpu().numpy()[0].astype(np.uint16), cnt[0])
+        np.testing.assert_array_equal(mc.cpu().numpy()[4].astype(np.uint16), cnt[4])
+
+
 # ------------------------------------------------------ k-means (K7, f4)
 def test_train_centroids_golden(golden_kmeans):
     """Native train_centroids vs the reference's, bit for bit (TC path at d=128,
