@@ -14,9 +14,11 @@
 //                     in one ordered pass, then a shared-memory bitonic sort.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cooperative_groups.h>
 
 #include "tc_common.cuh"
 
+namespace cg = cooperative_groups;
 namespace dsrt {
 
 constexpr int kPRows = 32;      // query rows per CTA
@@ -189,6 +191,107 @@ __global__ void chunk_bounds_kernel(const int64_t *__restrict__ post_off, const 
     bnd[i] = j == nch ? hi : lo + lower_bound_i64(post_docs + lo, hi - lo, j * D);
 }
 
+// Counting walk of one (query set, doc chunk): warp w takes the probed rows
+// w, w + NWARP, ...; lane j of the warp fetches row j's posting sub-range for
+// the chunk (independent loads, not a dependent chain per posting), a warp scan
+// turns the sub-range lengths into one flat index space, and the lanes then
+// stream the doc ids 4 loads deep, each lane advancing its own segment cursor.
+template <int CB, int NWARP>
+__device__ __forceinline__ void count_postings(uint32_t *sc, const int32_t *__restrict__ prow, int MP,
+                                               const int64_t *__restrict__ bnd, int nch, int ch,
+                                               const int64_t *__restrict__ post_docs, int64_t doc0) {
+    constexpr int DPW = 32 / CB;
+    __shared__ int64_t seg_base[NWARP][32];  // flat index -> post_docs index offset
+    __shared__ int32_t seg_end[NWARP][32];   // inclusive prefix of segment lengths
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r0 = 0; r0 < MP; r0 += NWARP * 32) {
+        const int r = r0 + warp + NWARP * lane;
+        int64_t a = 0;
+        int len = 0;
+        if (r < MP) {
+            const int c = prow[r];
+            if (c >= 0 && c != 0x7fffffff) {
+                const int64_t *bc = bnd + static_cast<int64_t>(c) * (nch + 1) + ch;
+                a = bc[0];
+                len = static_cast<int>(bc[1] - a);
+            }
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        seg_base[warp][lane] = a - (incl - len);
+        seg_end[warp][lane] = incl;
+        __syncwarp();
+        int seg = 0;
+        for (int i0 = 0; i0 < total; i0 += 8 * 32) {
+            int64_t dd[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = i0 + u * 32 + lane;
+                dd[u] = -1;
+                if (i < total) {
+                    while (i >= seg_end[warp][seg]) ++seg;
+                    dd[u] = post_docs[seg_base[warp][seg] + i] - doc0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (dd[u] >= 0) atomicAdd(&sc[dd[u] / DPW], 1u << (CB * static_cast<int>(dd[u] % DPW)));
+        }
+        __syncwarp();
+    }
+}
+
+// Count histogram of a chunk of u8 counters in shared memory (NT threads).
+// Words whose bytes are all <= 3 (nearly all) are tallied without compares:
+// byte-lane sums of bit 0, bit 1 and bit0 & bit1 give n1 + n3, n2 + n3 and n3;
+// the rare words holding a count >= 4 go byte by byte through shared atomics.
+template <int NT>
+__device__ __forceinline__ void chunk_hist8(const uint32_t *sc, uint32_t *hist, int max_count) {
+    constexpr int W_CH = kChunkBytes / 4;
+    constexpr uint32_t M = 0x01010101u;
+    static_assert(W_CH / NT <= 64, "byte-lane sums must not overflow");
+    uint32_t A = 0, B = 0, Cc = 0;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(sc);
+    for (int i = threadIdx.x; i < W_CH / 4; i += NT) {
+        const uint4 v = s4[i];
+        const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t x = xs[k];
+            if (x & 0xfcfcfcfcu) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t c = (x >> (8 * b)) & 0xffu;
+                    if (c != 0u) atomicAdd(&hist[tmin<uint32_t>(c, static_cast<uint32_t>(max_count))], 1u);
+                }
+                x = 0u;
+            }
+            const uint32_t b0 = x & M, b1 = (x >> 1) & M;
+            A += b0;
+            B += b1;
+            Cc += b0 & b1;
+        }
+    }
+    const uint32_t n3 = (Cc * M) >> 24;
+    uint32_t h1 = ((A * M) >> 24) - n3, h2 = ((B * M) >> 24) - n3, h3 = n3;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+        h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+        h3 += __shfl_xor_sync(0xffffffffu, h3, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (max_count >= 1) atomicAdd(&hist[1], h1);
+        if (max_count >= 2) atomicAdd(&hist[2], h2);
+        if (max_count >= 3) atomicAdd(&hist[3], h3);
+    }
+}
+
 // counts of one doc chunk for one query set in shared memory, then its count
 // histogram (hist_bins = max_count + 1) and the counter words of the row
 template <int CB>
@@ -204,30 +307,18 @@ __global__ void __launch_bounds__(kCntThreads)
     uint32_t *hist = sc + W_CH;
     const int ch = blockIdx.x;
     const int64_t qs = blockIdx.y;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     for (int i = tid; i < W_CH / 4; i += kCntThreads) reinterpret_cast<uint4 *>(sc)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i <= max_count; i += kCntThreads) hist[i] = 0;
     __syncthreads();
-    const int64_t doc0 = ch * D;
-    for (int r = warp; r < MP; r += kCntThreads / 32) {
-        const int c = probed[qs * MP + r];
-        if (c < 0 || c == 0x7fffffff) continue;
-        const int64_t a = bnd[static_cast<int64_t>(c) * (nch + 1) + ch];
-        const int64_t b = bnd[static_cast<int64_t>(c) * (nch + 1) + ch + 1];
-        for (int64_t i = a + lane; i < b; i += 4 * 32) {  // 4 loads in flight per lane
-            int64_t dd[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) dd[u] = i + u * 32 < b ? post_docs[i + u * 32] - doc0 : -1;
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (dd[u] >= 0)
-                    atomicAdd(&sc[dd[u] / DPW], 1u << (CB * static_cast<int>(dd[u] % DPW)));
-        }
-    }
+    count_postings<CB, kCntThreads / 32>(sc, probed + qs * MP, MP, bnd, nch, ch, post_docs, ch * D);
     __syncthreads();
     // histogram of this chunk's counts: 1..3 by SIMD compares, >= 4 by shared atomics
     constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
     uint32_t h1 = 0, h2 = 0, h3 = 0;
+    if constexpr (CB == 8) {
+        chunk_hist8<kCntThreads>(sc, hist, max_count);
+    } else {
     for (int i = tid; i < W_CH; i += kCntThreads) {
         const uint32_t x = sc[i];
         if (x == 0u) continue;
@@ -258,6 +349,7 @@ __global__ void __launch_bounds__(kCntThreads)
         if (max_count >= 1) atomicAdd(&hist[1], h1);
         if (max_count >= 2) atomicAdd(&hist[2], h2);
         if (max_count >= 3) atomicAdd(&hist[3], h3);
+    }
     }
     __syncthreads();
     uint32_t *gh = chist + (qs * nch + ch) * static_cast<int64_t>(max_count + 1);
@@ -624,6 +716,268 @@ __global__ void __launch_bounds__(kFinThreads)
     if (tid == 0) n_cand[qs] = outn;
 }
 
+// ---- u8 counters (m_q * probe <= 255), any batch: sort-free placement.
+// The output order (count desc, index asc) is a counting sort keyed by count,
+// so every selected doc's final slot follows from histograms alone:
+//   hit (count c > c*):  #(count > c, all chunks) + #(count == c, earlier
+//                        chunks) + rank among count == c in this chunk;
+//   tie (count == c*):   H + #(count == c*, earlier chunks) + rank in chunk,
+//                        kept while < need  (H = #(count > c*) = k_filter - need).
+// CTA per (query set, chunk): the plan (c*, H, need) and the bases come from
+// the counting pass's chunk histograms; ties are ranked by a block scan in doc
+// order; the chunk's hits (< k_filter of them) are compacted in doc order and
+// ranked per count by one warp with __match_any_sync.  No atomics, no sort.
+constexpr int kPlaceThreads = 512;
+constexpr int kPlaceWarps = kPlaceThreads / 32;
+static size_t place_smem(int max_count, int k_filter) {
+    return kChunkBytes + 16 + static_cast<size_t>(2 * (max_count + 1)) * sizeof(uint32_t) +
+           static_cast<size_t>(k_filter) * sizeof(uint32_t);
+}
+
+// Shared tail of the placement kernels: above[] holds the global count
+// histogram and pre[] the counts of earlier chunks (both [max_count + 1], in
+// shared memory, synced); cw the chunk's nw counter words (after `bar`, if any).
+__device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t *bar, int ch, int64_t qs,
+                                            int max_count, int k_filter, uint32_t *above, uint32_t *pre,
+                                            uint32_t *hl, int64_t *__restrict__ cand,
+                                            int32_t *__restrict__ n_cand) {
+    constexpr int W_CH = kChunkBytes / 4;      // counter words per chunk
+    constexpr int SW = W_CH / kPlaceThreads;   // words per thread strip (128 docs)
+    constexpr uint32_t ONE = 0x01010101u;
+    __shared__ uint32_t s_tot[2][kPlaceWarps];
+    __shared__ int s_cstar, s_need, s_H;
+    const int nb = max_count + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) {  // descending suffix scan of the histogram: c*, H, need; above[c] for c >= c*
+        const uint32_t g1 = nb > 1 ? above[1] : 0u;
+        uint32_t carry = 0;
+        int cstar = -1;
+        for (int top = max_count; top >= 1 && cstar < 0; top -= 32) {
+            const int b = top - lane;
+            const uint32_t g = b >= 1 ? above[b] : 0u;
+            uint32_t incl = g;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, b >= 1 && carry + incl >= static_cast<uint32_t>(k_filter));
+            if (b >= 1) above[b] = carry + incl - g;
+            if (hit != 0u) cstar = top - (__ffs(hit) - 1);
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (cstar >= 1) {
+                s_cstar = cstar;
+                s_H = static_cast<int>(above[cstar]);
+                s_need = k_filter - s_H;
+            } else {  // fewer than k_filter touched docs: take all of them
+                s_cstar = 1;
+                s_H = static_cast<int>(above[1]);
+                s_need = static_cast<int>(g1);
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t cstar = static_cast<uint32_t>(s_cstar);
+    const int need = s_need, H = s_H;
+    const uint32_t ceq = cstar * ONE;
+    if (bar != nullptr) mbar_wait(bar, 0);
+    // tie / hit counts of this thread's strip; 16-byte groups visited in a rotated
+    // order so a warp's LDS.128 spread over all banks (counting is order-free)
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(cw) + tid * (SW / 4);
+    const int ng = tmax(0, tmin(SW / 4, nw / 4 - tid * (SW / 4)));
+    uint32_t le = 0, lg = 0;        // byte-lane sums (<= 32 per lane)
+    uint32_t emask = 0, gmask = 0;  // bit q: word q of the strip holds a tie / a hit
+#pragma unroll
+    for (int u = 0; u < SW / 4; ++u) {
+        const int g = (u + tid) & (SW / 4 - 1);
+        if (g < ng) {
+            const uint4 v = s4[g];
+            const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t e = __vcmpeq4(xs[k], ceq) & ONE, t = __vcmpgtu4(xs[k], ceq) & ONE;
+                le += e;
+                lg += t;
+                emask |= (e != 0u ? 1u : 0u) << (4 * g + k);
+                gmask |= (t != 0u ? 1u : 0u) << (4 * g + k);
+            }
+        }
+    }
+    const uint32_t eqn = (le * ONE) >> 24, gtn = (lg * ONE) >> 24;
+    // block exclusive scans of (ties, hits) in thread = doc order
+    uint32_t xe = eqn, xg = gtn;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ye = __shfl_up_sync(0xffffffffu, xe, o);
+        const uint32_t yg = __shfl_up_sync(0xffffffffu, xg, o);
+        if (lane >= o) { xe += ye; xg += yg; }
+    }
+    if (lane == 31) { s_tot[0][warp] = xe; s_tot[1][warp] = xg; }
+    __syncthreads();
+    uint32_t be = 0, bg = 0, nh = 0;
+#pragma unroll
+    for (int i = 0; i < kPlaceWarps; ++i) {
+        const uint32_t te = s_tot[0][i], tg = s_tot[1][i];
+        be += i < warp ? te : 0u;
+        bg += i < warp ? tg : 0u;
+        nh += tg;
+    }
+    int64_t *out = cand + qs * k_filter;
+    const uint32_t *sw = cw + tid * SW;
+    const int64_t doc0 = static_cast<int64_t>(ch) * W_CH * 4;  // first doc of the chunk
+    const int sdoc0 = tid * SW * 4;                               // first doc of the strip, in the chunk
+    // ties: global tie rank = pre[c*] + rank in chunk; slot H + rank while rank < need
+    int64_t trank = static_cast<int64_t>(pre[cstar]) + be + (xe - eqn);
+    if (eqn > 0 && trank < need) {
+        for (uint32_t wm = emask; wm != 0u && trank < need; wm &= wm - 1u) {
+            const int q = __ffs(wm) - 1;
+            uint32_t m = __vcmpeq4(sw[q], ceq) & 0x80808080u;
+            while (m != 0u) {
+                const int byte = (__ffs(m) - 1) >> 3;
+                m &= m - 1u;
+                if (trank < need) out[H + trank] = doc0 + sdoc0 + q * 4 + byte;
+                ++trank;
+            }
+        }
+    }
+    // hits: compact (doc in chunk, count) in doc order
+    if (gtn > 0) {
+        uint32_t pos = bg + (xg - gtn);
+        for (uint32_t wm = gmask; wm != 0u; wm &= wm - 1u) {
+            const int q = __ffs(wm) - 1;
+            const uint32_t x = sw[q];
+            uint32_t m = __vcmpgtu4(x, ceq) & 0x80808080u;
+            while (m != 0u) {
+                const int byte = (__ffs(m) - 1) >> 3;
+                m &= m - 1u;
+                hl[pos++] = (static_cast<uint32_t>(sdoc0 + q * 4 + byte) << 8) | ((x >> (8 * byte)) & 0xffu);
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0 && nh > 0) {  // rank hits per count in doc order, 32 at a time
+        // pre[c] becomes this chunk's running slot base for count c
+        for (int b = lane + static_cast<int>(cstar) + 1; b < nb; b += 32) pre[b] += above[b];
+        __syncwarp();
+        for (uint32_t i0 = 0; i0 < nh; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool act = i < nh;
+            const uint32_t e = act ? hl[i] : 0u;
+            const uint32_t c = act ? (e & 0xffu) : 0x100u + lane;  // inactive lanes: unique keys
+            const unsigned peers = __match_any_sync(0xffffffffu, c);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            uint32_t base = 0;
+            if (act) base = pre[c];
+            __syncwarp();
+            if (act) {
+                out[base + rank] = doc0 + static_cast<int64_t>(e >> 8);
+                if (rank == 0) pre[c] = base + __popc(peers);
+            }
+            __syncwarp();
+        }
+    }
+    if (ch == 0) {
+        const int total = H + need;  // == k_filter unless fewer docs were touched
+        for (int i = total + tid; i < k_filter; i += kPlaceThreads) out[i] = -1;
+        if (tid == 0) n_cand[qs] = total;
+    }
+}
+
+// Separate counting pass (written counter rows + chunk histograms): the chunk's
+// words stream into shared memory (bulk copy) while the plan is summed.
+__global__ void __launch_bounds__(kPlaceThreads, 2)
+    sel_place_kernel(const uint32_t *__restrict__ counts, int64_t row_words, int nch, int max_count,
+                     int k_filter, const uint32_t *__restrict__ chist, int64_t *__restrict__ cand,
+                     int32_t *__restrict__ n_cand) {
+    constexpr int W_CH = kChunkBytes / 4;
+    extern __shared__ __align__(128) uint8_t psm_b[];
+    uint32_t *cw = reinterpret_cast<uint32_t *>(psm_b);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(psm_b + kChunkBytes);
+    const int nb = max_count + 1;
+    uint32_t *above = reinterpret_cast<uint32_t *>(psm_b + kChunkBytes + 16);
+    uint32_t *pre = above + nb;
+    uint32_t *hl = pre + nb;
+    const int ch = blockIdx.x;
+    const int64_t qs = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int64_t cw0 = static_cast<int64_t>(ch) * W_CH;
+    const int nw = static_cast<int>(tmin<int64_t>(W_CH, row_words - cw0));  // multiple of 4
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nw) * 4u);
+        bulk_g2s(cw, counts + qs * row_words + cw0, static_cast<uint32_t>(nw) * 4u, bar);
+    }
+    const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(nb);
+    for (int b = tid; b < nb; b += kPlaceThreads) {
+        uint32_t g = 0, p = 0;
+        for (int c = 0; c < nch; ++c) {
+            const uint32_t v = gh[c * static_cast<int64_t>(nb) + b];
+            g += v;
+            p += c < ch ? v : 0u;
+        }
+        above[b] = g;
+        pre[b] = p;
+    }
+    __syncthreads();
+    place_chunk(cw, nw, bar, ch, qs, max_count, k_filter, above, pre, hl, cand, n_cand);
+}
+
+// Fused counting + placement for n_docs <= kMaxFusedChunks * 64K (u8 counters):
+// a thread-block cluster of the nch chunk CTAs of one query set counts in
+// shared memory, exchanges the chunk histograms over distributed shared
+// memory, and places straight from the shared counters -- no counter rows in
+// HBM, one launch.
+constexpr int kMaxFusedChunks = 16;
+static size_t fused_smem(int max_count, int k_filter) {
+    return place_smem(max_count, k_filter) + static_cast<size_t>(max_count + 1) * sizeof(uint32_t);
+}
+
+__global__ void __launch_bounds__(kPlaceThreads, 2)
+    count_place_kernel(const int32_t *__restrict__ probed, int MP, const int64_t *__restrict__ bnd, int nch,
+                       const int64_t *__restrict__ post_docs, int64_t row_words, int max_count, int k_filter,
+                       int64_t *__restrict__ cand, int32_t *__restrict__ n_cand) {
+    constexpr int W_CH = kChunkBytes / 4;
+    extern __shared__ __align__(128) uint8_t psm_b[];
+    uint32_t *cw = reinterpret_cast<uint32_t *>(psm_b);
+    const int nb = max_count + 1;
+    uint32_t *above = reinterpret_cast<uint32_t *>(psm_b + kChunkBytes + 16);
+    uint32_t *pre = above + nb;
+    uint32_t *hl = pre + nb;
+    uint32_t *hist = hl + k_filter;  // this chunk's histogram (read by the cluster)
+    cg::cluster_group cluster = cg::this_cluster();
+    const int ch = static_cast<int>(cluster.block_rank());
+    const int64_t qs = blockIdx.y;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < W_CH / 4; i += kPlaceThreads) reinterpret_cast<uint4 *>(cw)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < nb; i += kPlaceThreads) hist[i] = 0;
+    __syncthreads();
+    count_postings<8, kPlaceWarps>(cw, probed + qs * MP, MP, bnd, nch, ch, post_docs,
+                                   static_cast<int64_t>(ch) * W_CH * 4);
+    __syncthreads();
+    chunk_hist8<kPlaceThreads>(cw, hist, max_count);
+    cluster.sync();  // every chunk histogram complete
+    for (int b = tid; b < nb; b += kPlaceThreads) {
+        uint32_t g = 0, p = 0;
+        for (int c = 0; c < nch; ++c) {
+            const uint32_t v = cluster.map_shared_rank(hist, c)[b];
+            g += v;
+            p += c < ch ? v : 0u;
+        }
+        above[b] = g;
+        pre[b] = p;
+    }
+    // the remote reads must finish before any CTA of the cluster exits
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    __syncthreads();
+    const int nw = static_cast<int>(tmin<int64_t>(W_CH, row_words - static_cast<int64_t>(ch) * W_CH));
+    place_chunk(cw, nw, nullptr, ch, qs, max_count, k_filter, above, pre, hl, cand, n_cand);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 static size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 // counters: uint8 when m_q*probe <= 255, else uint16; rows padded to 16 bytes
 static int counter_bits(int max_count) { return max_count <= 255 ? 8 : 16; }
@@ -655,6 +1009,17 @@ static size_t count_ws_bytes(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n
     return b;
 }
 
+// The fused cluster kernel saves a launch and the counter round trip, which
+// pays at small batches (latency); at large batches the 16-CTA clusters
+// schedule worse than the two plain kernels (cfg3 batch 256: 0.95 vs 0.78 ms
+// prefilter).  DSRT_FUSED_SELECT=0 / 1 forces either path (tests run both).
+static bool fused_enabled(int64_t n_q) {
+    const char *e = getenv("DSRT_FUSED_SELECT");
+    if (e != nullptr && e[0] == '0') return false;
+    if (e != nullptr && e[0] == '1') return true;
+    return small_batch(n_q);
+}
+
 // counts (written whole by the chunked pass; no memset) -> candidates.  cws:
 // count_ws_bytes workspace.
 static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int P, const int64_t *post_off,
@@ -674,11 +1039,40 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
         chunk_bounds_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(post_off, post_docs, k_c,
                                                                                   nch, chunk_docs(cb), bnd);
     }
+    if (cb == 8 && nch <= kMaxFusedChunks && fused_enabled(n_q)) {  // one cluster per query set
+        const size_t fsmem = fused_smem(max_count, k_filter);
+        DSRT_CUDA(cudaFuncSetAttribute(count_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+        DSRT_CUDA(cudaFuncSetAttribute(count_place_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q));
+        cfg.blockDim = dim3(kPlaceThreads);
+        cfg.dynamicSmemBytes = fsmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(nch);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DSRT_CUDA(cudaLaunchKernelEx(&cfg, count_place_kernel, probed, m_q * P, static_cast<const int64_t *>(bnd), nch,
+                                     post_docs, row_words, max_count, k_filter, cand, n_cand));
+        DSRT_LAUNCH_CHECK();
+        return DSRT_OK;
+    }
     const size_t csmem = kChunkBytes + (max_count + 1) * sizeof(uint32_t);
     auto ck = cb == 8 ? count_chunk_kernel<8> : count_chunk_kernel<16>;
     DSRT_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
     ck<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kCntThreads, csmem, st>>>(
         probed, m_q * P, bnd, nch, post_docs, row_words, max_count, counts, chist);
+    if (cb == 8) {  // sort-free placement (any batch)
+        const size_t psmem = place_smem(max_count, k_filter);
+        DSRT_CUDA(cudaFuncSetAttribute(sel_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+        sel_place_kernel<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kPlaceThreads, psmem, st>>>(
+            counts, row_words, nch, max_count, k_filter, chist, cand, n_cand);
+        DSRT_LAUNCH_CHECK();
+        return DSRT_OK;
+    }
     if (small_batch(n_q)) {  // chunk-parallel selection: plan -> chunk scans -> final sort
         uint8_t *sws = cws + count_ws_chunks(n_q, m_q, P, k_c, n_docs);
         SelPlan *plan = reinterpret_cast<SelPlan *>(sws);

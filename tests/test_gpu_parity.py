@@ -631,6 +631,44 @@ def test_prefilter_small_and_large_batch_paths_agree():
             np.testing.assert_array_equal(one[0, : int(n1[0])].cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("k_filter", [1, 5, 64, 1000, 4096, 16384])
+def test_prefilter_selection_many_chunks(k_filter, fused, monkeypatch):
+    """Selection over 330k docs (6 counter chunks of 64k docs) with hand-made postings:
+    dense postings give counts 1..m_q*probe with equal counts spread over every chunk,
+    so the per-count slot bases, the cross-chunk tie ranks and the < k_filter case are
+    all exercised; batch 1 and a batch of 24 query sets vs the oracle, through the fused
+    cluster kernel and the two-kernel count -> place path."""
+    from paper_2210_15748_b200 import prefilter as pf
+    monkeypatch.setenv("DSRT_FUSED_SELECT", fused)
+    rng = np.random.default_rng(5)
+    n_docs, k, dd = 330_000, 48, 128
+    C = rng.standard_normal((k, dd))
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    post = []
+    for c in range(k):
+        frac = [0.3, 0.05, 0.002, 0.0002][c % 4]
+        lo = int(rng.integers(0, n_docs // 2))
+        cand_docs = np.arange(lo, n_docs) if c % 5 else np.arange(n_docs)
+        post.append(np.sort(rng.choice(cand_docs, size=max(1, int(frac * len(cand_docs))),
+                                       replace=False)).astype(np.int64))
+    off = np.concatenate([[0], np.cumsum([len(p) for p in post])])
+    cindex = pf.CentroidIndex(n_docs=n_docs, post_off=torch.from_numpy(off).to(DEV),
+                              post_docs=torch.from_numpy(np.concatenate(post)).to(DEV))
+    cents = d.Centroids(k=k, seed=0, vectors=C)
+    n_q, m_q, probe = 24, 8, 5
+    Q = rng.standard_normal((n_q * m_q, dd))
+    got, n = pf.filter_candidates_device(cindex, cents, torch.from_numpy(Q).to(DEV), m_q, probe, k_filter)
+    for q in (0, 1, 7, 23):
+        want = O.filter_candidates(post, n_docs, C, Q[q * m_q:(q + 1) * m_q], probe, k_filter)
+        assert int(n[q]) == len(want)
+        np.testing.assert_array_equal(got[q, : int(n[q])].cpu().numpy(), want)
+        assert np.all(got[q, int(n[q]):].cpu().numpy() == -1)
+        one, n1 = pf.filter_candidates_device(cindex, cents, torch.from_numpy(Q[q * m_q:(q + 1) * m_q]).to(DEV),
+                                              m_q, probe, k_filter)
+        np.testing.assert_array_equal(one[0, : int(n1[0])].cpu().numpy(), want)
+
+
 def test_chunked_exhaustive_partial_last_chunk(monkeypatch):
     """rank_records with a score buffer smaller than N (last chunk partial, row-strided
     view into the buffer) equals the unchunked ranking."""
