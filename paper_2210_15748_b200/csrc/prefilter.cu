@@ -1202,7 +1202,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
     pf_screen_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_c,
                      int64_t n_rows, int64_t k_c, int64_t tiles_per_split, int P,
                      float *__restrict__ out_vals, const float *__restrict__ theta,
-                     ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n, uint32_t idesc) {
+                     ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n, uint32_t idesc,
+                     float *__restrict__ cmaxes) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1308,6 +1309,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
 #pragma unroll
                     for (int j = 0; j < w; ++j) m16[j] = fmaxf(m16[j], m16[j + w]);
                 const float cmax = m16[0];
+                // chunk maxima for the chunk-driven candidate pass ([chunk][row]: coalesced)
+                if (PASS == 0 && cmaxes != nullptr && row_ok) cmaxes[((id0 + c0) >> 5) * n_rows + row] = cmax;
                 if (PASS == 0) {
                     // top-P of the chunk maxima: P real values of the row, so their
                     // P-th best A'_P <= A_P and theta' = A'_P - 2 eps keeps pass 1 a
@@ -1413,6 +1416,73 @@ __global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int
     if (lane == 0) {
         theta[row] = aP - eps2;
         list_n[row] = 0;
+    }
+}
+
+// Candidate pass driven by the pass-0 chunk maxima (replaces a second GEMM):
+// warp = (32 query rows, span of kCSpan 32-centroid chunks).  Lane l scans row
+// l's chunk maxima (cmaxes is [chunk][row], so the warp's loads coalesce); for
+// every (row, chunk) whose maximum reaches theta[row] the warp recomputes the
+// chunk's 32 approximations (lane = centroid) from the screen's own fp16
+// operands with fp32 FMA -- within eps of exact, like the tensor-core values --
+// and appends those >= theta to the row's list (> kCandMax: exact fallback).
+// Soundness: an exact top-P centroid has approx >= exact - eps >= theta under
+// either rounding, so its chunk's maximum reaches theta and it is appended.
+// span: chunks per warp (multiple of 8), sized by the host for enough warps.
+__global__ void __launch_bounds__(256)
+    pf_chunk_cand_kernel(const float *__restrict__ cmaxes, int64_t n_chunks, int span, const float *__restrict__ theta,
+                         const __half *__restrict__ q16, const __half *__restrict__ c16, int64_t k_c,
+                         int64_t n_rows, ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int64_t j0 = (static_cast<int64_t>(blockIdx.y) * 8 + warp) * span;
+    if (j0 >= n_chunks) return;
+    const int64_t j1 = tmin<int64_t>(j0 + span, n_chunks);
+    const int64_t row = r0 + lane;
+    const bool row_ok = row < n_rows;
+    const float th = row_ok ? theta[row] : INFINITY;
+    for (int64_t jb = j0; jb < j1; jb += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            v[u] = (row_ok && jb + u < j1) ? __ldg(cmaxes + (jb + u) * n_rows + row) : -INFINITY;
+#pragma unroll 1
+        for (int u = 0; u < 8; ++u) {
+            unsigned m = __ballot_sync(0xffffffffu, v[u] >= th);
+            while (m != 0u) {
+                const int l = __ffs(m) - 1;
+                m &= m - 1u;
+                const int64_t rr = r0 + l;
+                const float thr = __shfl_sync(0xffffffffu, th, l);
+                const int64_t cid = (jb + u) * 32 + lane;
+                float acc = -INFINITY;
+                if (cid < k_c) {
+                    const uint4 *qv = reinterpret_cast<const uint4 *>(q16 + rr * 128);
+                    const uint4 *cv = reinterpret_cast<const uint4 *>(c16 + cid * 128);
+                    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint4 qa = __ldg(qv + k), ca = __ldg(cv + k);
+                        const __half2 *qh = reinterpret_cast<const __half2 *>(&qa);
+                        const __half2 *ch2 = reinterpret_cast<const __half2 *>(&ca);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 qf = __half22float2(qh[e]), cf = __half22float2(ch2[e]);
+                            a0 = fmaf(qf.x, cf.x, a0);
+                            a1 = fmaf(qf.y, cf.y, a1);
+                        }
+                    }
+                    acc = a0 + a1;
+                }
+                const bool ok = acc >= thr;
+                const unsigned okm = __ballot_sync(0xffffffffu, ok);
+                int base = 0;
+                if (lane == 0) base = atomicAdd(list_n + rr, __popc(okm));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const int slot = base + __popc(okm & ((1u << lane) - 1u));
+                if (ok && slot < kCandMax) lists[rr * kCandMax + slot] = ScreenCand{acc, static_cast<int32_t>(cid)};
+            }
+        }
     }
 }
 
@@ -1614,10 +1684,10 @@ namespace dsrt {
 template <int PASS, int PT>
 static int launch_screen(dim3 g, size_t smem, cudaStream_t st, const CUtensorMap &mq, const CUtensorMap &mc,
                          int64_t rows, int64_t k_c, int64_t tps, int P, float *vals, const float *theta,
-                         ScreenCand *lists, int32_t *listn, uint32_t idesc) {
+                         ScreenCand *lists, int32_t *listn, uint32_t idesc, float *cmaxes = nullptr) {
     DSRT_CUDA(cudaFuncSetAttribute(pf_screen_kernel<PASS, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     pf_screen_kernel<PASS, PT><<<g, kSThreads, smem, st>>>(mq, mc, rows, k_c, tps, P, vals, theta, lists,
-                                                           listn, idesc);
+                                                           listn, idesc, cmaxes);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
@@ -1634,9 +1704,10 @@ extern "C" int dsrt_to_f16_rows(const double *src, int64_t n, int d, double scal
 
 namespace dsrt {
 struct TcWs {
-    size_t q16, screen, theta, lists, listn, probed, fallback, counts, cnt_ws, total;
+    size_t q16, screen, theta, lists, listn, probed, fallback, counts, cnt_ws, cmax, total;
     int64_t n_split, row_words, tiles_per_split;
 };
+constexpr size_t kCmaxCap = size_t(1) << 30;
 static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int P) {
     TcWs w{};
     const int64_t rows = n_q * m_q;
@@ -1659,7 +1730,11 @@ static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int 
     w.fallback = align256(static_cast<size_t>(rows) * sizeof(int32_t));
     w.counts = align256(static_cast<size_t>(n_q) * w.row_words * sizeof(uint32_t));
     w.cnt_ws = count_ws_bytes(n_q, m_q, P, k_c, n_docs);
-    w.total = w.q16 + w.screen + w.theta + w.lists + w.listn + w.probed + w.fallback + w.counts + w.cnt_ws;
+    // pass-0 chunk maxima for the chunk-driven candidate pass (else a second GEMM pass)
+    const size_t cmax = static_cast<size_t>(n_tiles) * (kSN / 32) * rows * sizeof(float);
+    w.cmax = cmax <= kCmaxCap ? align256(cmax) : 0;
+    w.total = w.q16 + w.screen + w.theta + w.lists + w.listn + w.probed + w.fallback + w.counts + w.cnt_ws +
+              w.cmax;
     return w;
 }
 }  // namespace dsrt
@@ -1702,7 +1777,8 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     int32_t *probed = reinterpret_cast<int32_t *>(ws + o); o += w.probed;
     int32_t *fallback = reinterpret_cast<int32_t *>(ws + o); o += w.fallback;
     uint32_t *counts = reinterpret_cast<uint32_t *>(ws + o); o += w.counts;
-    uint8_t *cnt_ws = ws + o;
+    uint8_t *cnt_ws = ws + o; o += w.cnt_ws;
+    float *cmaxes = w.cmax > 0 ? reinterpret_cast<float *>(ws + o) : nullptr;
     const int64_t rows = n_q * m_q;
     const int64_t m_tiles = (rows + 127) / 128;
     DSRT_CUDA(cudaMemsetAsync(q16, 0, w.q16, st));
@@ -1717,19 +1793,32 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     const size_t smem = 1024 + 2 * 128 * 128 + kSStages * 2 * kSN * 128;
     dim3 g(static_cast<unsigned>(m_tiles), static_cast<unsigned>(w.n_split));
     const uint32_t idesc = idesc_f16(128, kSN, 0, 0);
-    rc = P <= 4 ? launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc)
-       : P <= 8 ? launch_screen<0, 8>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc)
-                : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc);
+    rc = P <= 4 ? launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes)
+       : P <= 8 ? launch_screen<0, 8>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes)
+                : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes);
     if (rc) return rc;
     // eps in normalised units (|q^| = 1, |c*s| <= 1)
     pf_theta_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
         vals, static_cast<int>(w.n_split * kSHalves), rows, P, static_cast<float>(2.0 * kScreenEps), theta, listn,
         nullptr, d);
-    rc = launch_screen<2, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
-                             listn, idesc);
-    if (rc) return rc;
-    pf_rerank_sub_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
-        lists, listn, static_cast<int>(w.n_split * kSHalves), Q, cents, rows, d, P, probed, fallback);
+    if (cmaxes != nullptr) {  // candidates from the chunk maxima + fp16 SIMT recompute
+        const int64_t n_chunks = ((k_c + kSN - 1) / kSN) * (kSN / 32);
+        const int64_t rgroups = (rows + 31) / 32;
+        // ~32 warps per SM of work, spans of 8..64 chunks
+        const int64_t want = 32LL * sm_count();
+        const int span = static_cast<int>(tmax<int64_t>(8, tmin<int64_t>(64, ((n_chunks * rgroups / want) + 7) / 8 * 8)));
+        const dim3 gc(static_cast<unsigned>(rgroups), static_cast<unsigned>((n_chunks + 8LL * span - 1) / (8LL * span)));
+        pf_chunk_cand_kernel<<<gc, 256, 0, st>>>(cmaxes, n_chunks, span, theta, q16,
+                                                  static_cast<const __half *>(cents_f16), k_c, rows, lists, listn);
+        pf_rerank_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+            lists, listn, Q, cents, rows, d, P, probed, fallback);
+    } else {  // second GEMM pass collecting approx >= theta
+        rc = launch_screen<2, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, nullptr, theta, lists,
+                                 listn, idesc);
+        if (rc) return rc;
+        pf_rerank_sub_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
+            lists, listn, static_cast<int>(w.n_split * kSHalves), Q, cents, rows, d, P, probed, fallback);
+    }
     pf_fallback_kernel<double><<<static_cast<unsigned>(rows), 256, 0, st>>>(fallback, Q, cents, rows, k_c, d,
                                                                            P, probed);
     rc = launch_count_select(probed, n_q, m_q, P, post_off, post_docs, n_docs, k_c, w.row_words, counts,
