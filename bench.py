@@ -58,16 +58,65 @@ def _dist():
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + clock-event reasons sampled DURING the timed region.
+
+    NVML (nvidia-ml-py) polled from a thread every ~2 ms, so even a 10 ms timed
+    region gets samples; start() returns after the first sample.  Falls back to
+    `nvidia-smi -lms 100` when NVML is unavailable.  Samples are also written to
+    gpurun_out/clocks_rank<i>.csv."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
-        self.proc = None
         self.gpu = gpu_index
         self.path = os.path.join(REPO, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+        self.samples = []
+        self.thread = None
+        self.proc = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+
+            p = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def start(self):
+        import threading
+
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = self._handle(nv)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.stop_evt = threading.Event()
+            first = threading.Event()
+
+            def loop():
+                while not self.stop_evt.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.perf_counter(), sm, mx, rs))
+                    except Exception:
+                        pass
+                    first.set()
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            first.wait(1.0)
+            return
+        except Exception:
+            self.thread = None
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
@@ -79,6 +128,23 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self.stop_evt.set()
+            self.thread.join(timeout=5)
+            sm = [s[1] for s in self.samples]
+            mx = [s[2] for s in self.samples]
+            reasons = sorted({nm for s in self.samples for nm, bit in self.REASONS.items() if s[3] & bit})
+            try:
+                os.makedirs(os.path.dirname(self.path), exist_ok=True)
+                with open(self.path, "w") as fh:
+                    fh.write("t_s,sm_mhz,sm_max_mhz,reasons_mask\n")
+                    for t, a, b, r in self.samples:
+                        fh.write(f"{t:.4f},{a},{b},{r:#x}\n")
+            except Exception:
+                pass
+            return {"sm_mhz": float(np.median(sm)) if sm else None,
+                    "sm_max_mhz": float(max(mx)) if mx else None, "reasons": reasons,
+                    "samples": len(sm), "source": "nvml, 2 ms poll"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         self.proc.terminate()
@@ -103,7 +169,7 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": float(max(mx)) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -366,6 +432,8 @@ def run_gpu(args):
 def _clocks_and_time(step_fn, steps, warmup, local, stream):
     import torch
 
+    if os.environ.get("DSRT_PROFILE_STEPS"):  # ncu --profile-from-start off: capture the steps only
+        torch.cuda.cudart().cudaProfilerStart()
     for _ in range(warmup):
         step_fn(False)
     torch.cuda.synchronize()

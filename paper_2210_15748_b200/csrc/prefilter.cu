@@ -1433,6 +1433,7 @@ __global__ void __launch_bounds__(256)
     pf_chunk_cand_kernel(const float *__restrict__ cmaxes, int64_t n_chunks, int span, const float *__restrict__ theta,
                          const __half *__restrict__ q16, const __half *__restrict__ c16, int64_t k_c,
                          int64_t n_rows, ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n) {
+    __shared__ float qf[8][128];  // the current match's query row, as float
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
     const int64_t j0 = (static_cast<int64_t>(blockIdx.y) * 8 + warp) * span;
@@ -1441,46 +1442,60 @@ __global__ void __launch_bounds__(256)
     const int64_t row = r0 + lane;
     const bool row_ok = row < n_rows;
     const float th = row_ok ? theta[row] : INFINITY;
+    // one (row, chunk) match: lane = centroid of the chunk
+    auto process = [&](int l, int64_t j) {
+        const int64_t rr = r0 + l;
+        const float thr = __shfl_sync(0xffffffffu, th, l);
+        {  // stage the query row as float (lane k: dims 4k .. 4k+3)
+            const uint2 h = __ldg(reinterpret_cast<const uint2 *>(q16 + rr * 128) + lane);
+            const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&h.x));
+            const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&h.y));
+            reinterpret_cast<float4 *>(qf[warp])[lane] = make_float4(a.x, a.y, b.x, b.y);
+        }
+        __syncwarp();
+        const int64_t cid = j * 32 + lane;
+        float acc = -INFINITY;
+        if (cid < k_c) {
+            const uint4 *cv = reinterpret_cast<const uint4 *>(c16 + cid * 128);
+            uint4 c[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) c[k] = __ldg(cv + k);
+            float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const __half2 *ch2 = reinterpret_cast<const __half2 *>(&c[k]);
+                const float4 q0 = reinterpret_cast<const float4 *>(qf[warp])[2 * k];
+                const float4 q1 = reinterpret_cast<const float4 *>(qf[warp])[2 * k + 1];
+                const float2 c0 = __half22float2(ch2[0]), c1 = __half22float2(ch2[1]);
+                const float2 c2 = __half22float2(ch2[2]), c3 = __half22float2(ch2[3]);
+                a0 = fmaf(q0.x, c0.x, a0); a1 = fmaf(q0.y, c0.y, a1);
+                a0 = fmaf(q0.z, c1.x, a0); a1 = fmaf(q0.w, c1.y, a1);
+                a0 = fmaf(q1.x, c2.x, a0); a1 = fmaf(q1.y, c2.y, a1);
+                a0 = fmaf(q1.z, c3.x, a0); a1 = fmaf(q1.w, c3.y, a1);
+            }
+            acc = a0 + a1;
+        }
+        __syncwarp();
+        const bool ok = acc >= thr;
+        const unsigned okm = __ballot_sync(0xffffffffu, ok);
+        int base = 0;
+        if (lane == 0 && okm != 0u) base = atomicAdd(list_n + rr, __popc(okm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int slot = base + __popc(okm & ((1u << lane) - 1u));
+        if (ok && slot < kCandMax) lists[rr * kCandMax + slot] = ScreenCand{acc, static_cast<int32_t>(cid)};
+    };
     for (int64_t jb = j0; jb < j1; jb += 8) {
         float v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
             v[u] = (row_ok && jb + u < j1) ? __ldg(cmaxes + (jb + u) * n_rows + row) : -INFINITY;
-#pragma unroll 1
+#pragma unroll
         for (int u = 0; u < 8; ++u) {
             unsigned m = __ballot_sync(0xffffffffu, v[u] >= th);
             while (m != 0u) {
                 const int l = __ffs(m) - 1;
                 m &= m - 1u;
-                const int64_t rr = r0 + l;
-                const float thr = __shfl_sync(0xffffffffu, th, l);
-                const int64_t cid = (jb + u) * 32 + lane;
-                float acc = -INFINITY;
-                if (cid < k_c) {
-                    const uint4 *qv = reinterpret_cast<const uint4 *>(q16 + rr * 128);
-                    const uint4 *cv = reinterpret_cast<const uint4 *>(c16 + cid * 128);
-                    float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint4 qa = __ldg(qv + k), ca = __ldg(cv + k);
-                        const __half2 *qh = reinterpret_cast<const __half2 *>(&qa);
-                        const __half2 *ch2 = reinterpret_cast<const __half2 *>(&ca);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 qf = __half22float2(qh[e]), cf = __half22float2(ch2[e]);
-                            a0 = fmaf(qf.x, cf.x, a0);
-                            a1 = fmaf(qf.y, cf.y, a1);
-                        }
-                    }
-                    acc = a0 + a1;
-                }
-                const bool ok = acc >= thr;
-                const unsigned okm = __ballot_sync(0xffffffffu, ok);
-                int base = 0;
-                if (lane == 0) base = atomicAdd(list_n + rr, __popc(okm));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                const int slot = base + __popc(okm & ((1u << lane) - 1u));
-                if (ok && slot < kCandMax) lists[rr * kCandMax + slot] = ScreenCand{acc, static_cast<int32_t>(cid)};
+                process(l, jb + u);
             }
         }
     }
@@ -1805,7 +1820,7 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
         const int64_t n_chunks = ((k_c + kSN - 1) / kSN) * (kSN / 32);
         const int64_t rgroups = (rows + 31) / 32;
         // ~32 warps per SM of work, spans of 8..64 chunks
-        const int64_t want = 32LL * sm_count();
+        const int64_t want = 512LL * sm_count();  // many short spans: matches are latency-bound
         const int span = static_cast<int>(tmax<int64_t>(8, tmin<int64_t>(64, ((n_chunks * rgroups / want) + 7) / 8 * 8)));
         const dim3 gc(static_cast<unsigned>(rgroups), static_cast<unsigned>((n_chunks + 8LL * span - 1) / (8LL * span)));
         pf_chunk_cand_kernel<<<gc, 256, 0, st>>>(cmaxes, n_chunks, span, theta, q16,
