@@ -33,10 +33,14 @@ struct RowView {
 // prefix such that exactly `need` elements are >= (descending) or <=
 // (ascending) it, counting ties into the last bin.  Returns (prefix, mask,
 // remaining) through shared memory.
+// Leading bytes shared by every candidate key are skipped: one pass ORs and
+// ANDs the keys and the select starts at the first byte where they differ
+// (scores in [0, 1] share their sign/exponent byte).  The digit of each pass
+// is chosen by a warp-wide scan of the 256 bins (8 per lane), not a serial loop.
 template <bool DESC, typename KeyF, typename PredF>
 __device__ void radix_select(int64_t n, int64_t need, KeyF keyf, PredF pred, uint32_t *hist,
                              uint64_t *out_prefix, uint64_t *out_mask, int64_t *out_rem) {
-    __shared__ uint64_t s_prefix, s_mask;
+    __shared__ uint64_t s_prefix, s_mask, s_or, s_and;
     __shared__ int64_t s_rem;
     __shared__ int s_done;
     if (threadIdx.x == 0) {
@@ -44,9 +48,39 @@ __device__ void radix_select(int64_t n, int64_t need, KeyF keyf, PredF pred, uin
         s_mask = 0;
         s_rem = need;
         s_done = 0;
+        s_or = 0;
+        s_and = ~0ull;
     }
     __syncthreads();
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    {
+        uint64_t o = 0, a = ~0ull;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            if (!pred(i)) continue;
+            const uint64_t k = keyf(i);
+            o |= k;
+            a &= k;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            o |= __shfl_xor_sync(0xffffffffu, o, off);
+            a &= __shfl_xor_sync(0xffffffffu, a, off);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicOr(reinterpret_cast<unsigned long long *>(&s_or), o);
+            atomicAnd(reinterpret_cast<unsigned long long *>(&s_and), a);
+        }
+    }
+    __syncthreads();
+    const uint64_t diff = s_or ^ s_and;  // bits that differ between candidates
+    int top = 56;
+    while (top > 0 && ((diff >> top) & 255u) == 0u) top -= 8;
+    if (threadIdx.x == 0) {  // the common leading bytes are part of every prefix
+        const uint64_t lead = top >= 56 ? 0ull : (~0ull << (top + 8));
+        s_prefix = s_and & lead;
+        s_mask = lead;
+    }
+    __syncthreads();
+    for (int shift = top; shift >= 0; shift -= 8) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
         __syncthreads();
         const uint64_t prefix = s_prefix, mask = s_mask;
@@ -56,22 +90,38 @@ __device__ void radix_select(int64_t n, int64_t need, KeyF keyf, PredF pred, uin
             if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int64_t rem = s_rem, cum = 0;
-            int sel = DESC ? 0 : 255;
-            for (int t = 0; t < 256; ++t) {
-                const int dgt = DESC ? 255 - t : t;
-                const int64_t h = hist[dgt];
-                if (cum + h >= rem) {
-                    sel = dgt;
-                    break;
-                }
-                cum += h;
+        if (threadIdx.x < 32) {  // warp 0: bins in selection order, 8 per lane
+            const int lane = threadIdx.x;
+            uint32_t h[8];
+            int64_t loc = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int dgt = DESC ? 255 - (lane * 8 + t) : lane * 8 + t;
+                h[t] = hist[dgt];
+                loc += h[t];
             }
-            s_rem = rem - cum;
-            s_prefix = prefix | (static_cast<uint64_t>(sel) << shift);
-            s_mask = mask | (255ull << shift);
-            if (static_cast<int64_t>(hist[sel]) == s_rem) s_done = 1;  // take the whole bin
+            int64_t incl = loc;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            const int64_t rem = s_rem;
+            const unsigned hitm = __ballot_sync(0xffffffffu, incl >= rem);
+            const int owner = hitm ? __ffs(hitm) - 1 : 31;
+            if (lane == owner) {
+                int64_t cum = incl - loc;
+                int t = 0;
+                for (; t < 7; ++t) {
+                    if (cum + h[t] >= rem) break;
+                    cum += h[t];
+                }
+                const int sel = DESC ? 255 - (lane * 8 + t) : lane * 8 + t;
+                s_rem = rem - cum;
+                s_prefix = prefix | (static_cast<uint64_t>(sel) << shift);
+                s_mask = mask | (255ull << shift);
+                if (static_cast<int64_t>(h[t]) == rem - cum) s_done = 1;  // take the whole bin
+            }
         }
         __syncthreads();
         if (s_done) break;
@@ -95,9 +145,11 @@ __global__ void __launch_bounds__(kTopkThreads)
                 double *__restrict__ out_s, uint64_t *__restrict__ out_id,
                 int64_t *__restrict__ out_pos) {
     extern __shared__ __align__(16) uint8_t smem[];
+    int cap = 1;  // winner buffer: pow2 >= k (at most k winners are collected)
+    while (cap < k) cap <<= 1;
     uint64_t *bkey = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *bid = bkey + kTopkMax;
-    int64_t *bpos = reinterpret_cast<int64_t *>(bid + kTopkMax);
+    uint64_t *bid = bkey + cap;
+    int64_t *bpos = reinterpret_cast<int64_t *>(bid + cap);
     __shared__ uint32_t hist[256];
     __shared__ uint64_t t_prefix, t_mask, i_prefix, i_mask;
     __shared__ int64_t t_rem, i_rem;
@@ -154,7 +206,7 @@ __global__ void __launch_bounds__(kTopkThreads)
             }
             if (take) {
                 const int slot = atomicAdd(&cnt, 1);
-                if (slot < kTopkMax) {
+                if (slot < cap) {
                     bkey[slot] = key;
                     bid[slot] = rv.id(i);
                     bpos[slot] = i;
@@ -163,7 +215,7 @@ __global__ void __launch_bounds__(kTopkThreads)
         }
     }
     __syncthreads();
-    const int m = tmin<int64_t>(cnt, kTopkMax);
+    const int m = tmin(cnt, cap);
     int p2 = 1;
     while (p2 < m) p2 <<= 1;
     for (int i = m + threadIdx.x; i < p2; i += blockDim.x) {  // sentinels sort last
@@ -226,9 +278,14 @@ extern "C" int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, 
                  (long long)n, (long long)ld);
     if (n_rows == 0) return DSRT_OK;
     DSRT_REQUIRE(n_rows < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many rows");
-    const size_t smem = kTopkMax * (2 * sizeof(uint64_t) + sizeof(int64_t));
-    DSRT_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    topk_kernel<<<static_cast<unsigned>(n_rows), kTopkThreads, smem, as_stream(stream)>>>(
+    int cap = 1;
+    while (cap < k) cap <<= 1;
+    const size_t smem = static_cast<size_t>(cap) * (2 * sizeof(uint64_t) + sizeof(int64_t));
+    DSRT_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kTopkMax * (2 * sizeof(uint64_t) + sizeof(int64_t)))));
+    // short rows (candidate lists): small CTAs, many per SM
+    const int threads = n <= 8192 ? 256 : kTopkThreads;
+    topk_kernel<<<static_cast<unsigned>(n_rows), threads, smem, as_stream(stream)>>>(
         scores, ld, ids, ids_ld, n_valid, n, k, out_scores, out_ids, out_pos);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
