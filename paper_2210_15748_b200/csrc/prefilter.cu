@@ -352,8 +352,9 @@ __global__ void __launch_bounds__(kCntThreads)
     }
     }
     __syncthreads();
-    uint32_t *gh = chist + (qs * nch + ch) * static_cast<int64_t>(max_count + 1);
-    for (int i = tid; i <= max_count; i += kCntThreads) gh[i] = hist[i];
+    // chist[(qs * nb + bin) * nch + chunk]: one bin's chunk counts are contiguous
+    for (int i = tid; i <= max_count; i += kCntThreads)
+        chist[(qs * (max_count + 1) + i) * static_cast<int64_t>(nch) + ch] = hist[i];
     // counter words of the row (chunks tile the whole padded row)
     const int64_t w0 = static_cast<int64_t>(ch) * W_CH;
     const int64_t nw = tmin<int64_t>(W_CH, row_words - w0);
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(kSelThreads)
         const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(max_count + 1);
         for (int b = tid; b <= max_count; b += blockDim.x) {
             uint32_t t = 0;
-            for (int c = 0; c < nch; ++c) t += gh[c * static_cast<int64_t>(max_count + 1) + b];
+            for (int c = 0; c < nch; ++c) t += gh[b * static_cast<int64_t>(nch) + c];
             hist[b] = t;
         }
         __syncthreads();
@@ -551,7 +552,7 @@ __global__ void sel_plan_kernel(const uint32_t *__restrict__ chist, int nch, int
     const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(max_count + 1);
     for (int b = threadIdx.x; b <= max_count; b += blockDim.x) {
         uint32_t t = 0;
-        for (int c = 0; c < nch; ++c) t += gh[c * static_cast<int64_t>(max_count + 1) + b];
+        for (int c = 0; c < nch; ++c) t += gh[b * static_cast<int64_t>(nch) + c];
         ph[b] = t;
     }
     __syncthreads();
@@ -571,7 +572,7 @@ __global__ void sel_plan_kernel(const uint32_t *__restrict__ chist, int nch, int
         int32_t run = 0;
         for (int c = 0; c < nch; ++c) {
             tie_base[qs * nch + c] = run;
-            run += static_cast<int32_t>(gh[c * static_cast<int64_t>(max_count + 1) + cstar]);
+            run += static_cast<int32_t>(gh[cstar * static_cast<int64_t>(nch) + c]);
         }
     }
 }
@@ -912,12 +913,22 @@ __global__ void __launch_bounds__(kPlaceThreads, 2)
         bulk_g2s(cw, counts + qs * row_words + cw0, static_cast<uint32_t>(nw) * 4u, bar);
     }
     const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(nb);
-    for (int b = tid; b < nb; b += kPlaceThreads) {
+    for (int b = tid; b < nb; b += kPlaceThreads) {  // a bin's nch chunk counts are contiguous
+        const uint32_t *gb = gh + b * static_cast<int64_t>(nch);
         uint32_t g = 0, p = 0;
-        for (int c = 0; c < nch; ++c) {
-            const uint32_t v = gh[c * static_cast<int64_t>(nb) + b];
-            g += v;
-            p += c < ch ? v : 0u;
+        if ((nch & 3) == 0) {  // 16-byte loads, all issued before the sums
+#pragma unroll 4
+            for (int c = 0; c < nch; c += 4) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(gb + c));
+                g += v.x + v.y + v.z + v.w;
+                p += (c < ch ? v.x : 0u) + (c + 1 < ch ? v.y : 0u) + (c + 2 < ch ? v.z : 0u) + (c + 3 < ch ? v.w : 0u);
+            }
+        } else {
+            for (int c = 0; c < nch; ++c) {
+                const uint32_t v = __ldg(gb + c);
+                g += v;
+                p += c < ch ? v : 0u;
+            }
         }
         above[b] = g;
         pre[b] = p;
