@@ -655,6 +655,7 @@ def run_cfg3(args):
     mb = engine.microbench_int()
     p_int = mb["lop3_ops_per_s"] * 4.0
     rec_bytes = cand_vec * engine.record_words(L, C) * 4
+    traffic3, t3d = _ncu_traffic("cfg3", cand_vec / 82221078.0)
     line = {
         "metric": "query sets/sec (cfg3: 1M sets, prefilter probe 4 / k_filter 4096, L=32 C=7, top-100, batch 256)",
         "value": 256 / (ms * 1e-3), "unit": "query sets/s", "n_gpus": 1, "steps": args.steps,
@@ -675,13 +676,19 @@ def run_cfg3(args):
         "roofline": {"bound": "int", "unit": "Gcompare/s", "kernel": "score_cand_kernel<7,1,1>",
                      "kernel_ms": sc_ms, "achieved": compares / (sc_ms * 1e-3) / 1e9,
                      "peak": p_int / 1e9, "frac": compares / (sc_ms * 1e-3) / p_int,
-                     "traffic": None,
+                     "traffic": traffic3,
+                     "traffic_detail": None if traffic3 is None else dict(
+                         t3d, algorithmic_bytes=rec_bytes, ratio=traffic3 / rec_bytes,
+                         note="candidate sets differ per query set, so every candidate's records "
+                              "stream once per query set"),
                      "per_launch": {"compares": compares, "candidate_vectors": cand_vec,
                                     "code_bytes": rec_bytes,
                                     "hbm_floor_ms": rec_bytes / 6456.2e9 * 1e3},
                      "peak_source": "measured in-run: LOP3 lane-ops/s x 4"},
         "clocks": clk, "int_microbench": mb,
-        "gpu_launches": 11 * args.steps,  # hash, f16 rows, screen x2, theta, rerank, fallback, count, select, score, top-k
+        # plane permute, hash, f16 rows, screen, theta, chunk candidates, re-rank, fallback,
+        # count, place, score, top-k
+        "gpu_launches": 12 * args.steps,
     }
     print(json.dumps(line))
     return 0
