@@ -1742,6 +1742,7 @@ static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int 
     const int sms = sm_count();
     // about one wave of CTAs: fewer splits amortise each row's list warm-up
     int64_t bs = tmax<int64_t>(1, tmin<int64_t>(n_tiles, (sms + m_tiles / 2) / m_tiles));
+    if (const char *e = getenv("DSRT_SCREEN_SPLIT")) bs = tmax<int64_t>(1, tmin<int64_t>(n_tiles, atoi(e)));
     w.n_split = bs;
     w.tiles_per_split = (n_tiles + bs - 1) / bs;
     w.n_split = (n_tiles + w.tiles_per_split - 1) / w.tiles_per_split;

@@ -631,9 +631,10 @@ def test_prefilter_small_and_large_batch_paths_agree():
             np.testing.assert_array_equal(one[0, : int(n1[0])].cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("mq_probe", [(8, 5), (64, 8)])  # u8 and u16 (m_q*probe > 255) counters
 @pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("k_filter", [1, 5, 64, 1000, 4096, 16384])
-def test_prefilter_selection_many_chunks(k_filter, fused, monkeypatch):
+def test_prefilter_selection_many_chunks(k_filter, fused, mq_probe, monkeypatch):
     """Selection over 330k docs (6 counter chunks of 64k docs) with hand-made postings:
     dense postings give counts 1..m_q*probe with equal counts spread over every chunk,
     so the per-count slot bases, the cross-chunk tie ranks and the < k_filter case are
@@ -656,7 +657,7 @@ def test_prefilter_selection_many_chunks(k_filter, fused, monkeypatch):
     cindex = pf.CentroidIndex(n_docs=n_docs, post_off=torch.from_numpy(off).to(DEV),
                               post_docs=torch.from_numpy(np.concatenate(post)).to(DEV))
     cents = d.Centroids(k=k, seed=0, vectors=C)
-    n_q, m_q, probe = 24, 8, 5
+    n_q, (m_q, probe) = 24, mq_probe
     Q = rng.standard_normal((n_q * m_q, dd))
     got, n = pf.filter_candidates_device(cindex, cents, torch.from_numpy(Q).to(DEV), m_q, probe, k_filter)
     for q in (0, 1, 7, 23):
