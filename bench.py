@@ -446,6 +446,8 @@ def _clocks_and_time(step_fn, steps, warmup, local, stream):
         step_fn(True)
     t1.record(stream)
     torch.cuda.synchronize()
+    if os.environ.get("DSRT_PROFILE_STEPS"):
+        torch.cuda.cudart().cudaProfilerStop()
     return t0.elapsed_time(t1) / steps, clocks.stop()
 
 
