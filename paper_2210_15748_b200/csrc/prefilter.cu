@@ -1208,7 +1208,9 @@ __device__ __forceinline__ bool s_better(float sa, int ia, float sb, int ib) {
 constexpr int kCandMax = 32;
 constexpr int kMaxPtc = 12;
 
-template <int PASS, int PT>
+// RT = query-row tiles per CTA sharing every streamed centroid tile (RT = 2 halves
+// the B-tile stream per row; the pass is bound by that stream, not the MMA).
+template <int PASS, int PT, int RT = 1>
 __global__ void __launch_bounds__(kSThreads, 1)
     pf_screen_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_c,
                      int64_t n_rows, int64_t k_c, int64_t tiles_per_split, int P,
@@ -1219,12 +1221,12 @@ __global__ void __launch_bounds__(kSThreads, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int kA = 2 * 128 * 128, kB = 2 * kSN * 128;
-    uint8_t *sa = smem;
-    uint8_t *sb = smem + kA;
+    uint8_t *sa = smem;           // RT x kA
+    uint8_t *sb = smem + RT * kA;
     __shared__ uint64_t full[kSStages], empty[kSStages], tfull[2], tempty[2], bar_a;
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 128;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * 128 * RT;
     const int64_t n_tiles_total = (k_c + kSN - 1) / kSN;
     const int64_t t_lo = blockIdx.y * tiles_per_split;
     const int64_t t_hi = tmin<int64_t>(t_lo + tiles_per_split, n_tiles_total);
@@ -1242,16 +1244,19 @@ __global__ void __launch_bounds__(kSThreads, 1)
         mbar_init(&bar_a, 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(&tmem_base, 256);
+    if (warp == 1) tmem_alloc(&tmem_base, 256 * RT);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base;
     if (warp == 0) {
         if (lane == 0) {
-            mbar_arrive_expect_tx(&bar_a, kA);
-            tma_load_2d(sa, &map_q, 0, static_cast<int>(m0), &bar_a);
-            tma_load_2d(sa + 128 * 128, &map_q, 64, static_cast<int>(m0), &bar_a);
+            mbar_arrive_expect_tx(&bar_a, RT * kA);
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+                tma_load_2d(sa + r * kA, &map_q, 0, static_cast<int>(m0 + r * 128), &bar_a);
+                tma_load_2d(sa + r * kA + 128 * 128, &map_q, 64, static_cast<int>(m0 + r * 128), &bar_a);
+            }
             int it = 0;
             for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
                 const int st = it % kSStages;
@@ -1270,12 +1275,15 @@ __global__ void __launch_bounds__(kSThreads, 1)
                 mbar_wait(&full[st], (it / kSStages) & 1);
                 if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
                 tc_fence_after();
-                const uint32_t d = tmem + acc * kSN;
-                for (int kb = 0; kb < 2; ++kb) {
-                    const uint64_t ad = umma_desc_sw128(sa + kb * 128 * 128);
-                    const uint64_t bd = umma_desc_sw128(sb + st * kB + kb * kSN * 128);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) umma_f16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                for (int r = 0; r < RT; ++r) {
+                    const uint32_t d = tmem + (acc * RT + r) * kSN;
+                    for (int kb = 0; kb < 2; ++kb) {
+                        const uint64_t ad = umma_desc_sw128(sa + r * kA + kb * 128 * 128);
+                        const uint64_t bd = umma_desc_sw128(sb + st * kB + kb * kSN * 128);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) umma_f16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                    }
                 }
                 umma_commit(&empty[st]);
                 umma_commit(&tfull[acc]);
@@ -1284,22 +1292,32 @@ __global__ void __launch_bounds__(kSThreads, 1)
     } else {
         const int quarter = warp & 3;                // TMEM lanes 32*quarter .. +31
         const int half = (warp - 2) / 4;             // which column slice of each tile
-        const int64_t row = m0 + quarter * 32 + lane;
-        const bool row_ok = row < n_rows;
-        float tv[PT];
+        float tvs[RT][PT];
+        float worsts[RT];  // tvs[r][P-1]
+        int nsubs[RT];     // PASS 2: candidates of this (row, split, half)
 #pragma unroll
-        for (int j = 0; j < PT; ++j) tv[j] = -INFINITY;
-        float worst = -INFINITY;  // tv[P-1]
-        const float th = (PASS != 0 && row_ok) ? theta[row] : INFINITY;
-        int nsub = 0;  // PASS 2: candidates of this (row, split, half)
+        for (int r = 0; r < RT; ++r) {
+#pragma unroll
+            for (int j = 0; j < PT; ++j) tvs[r][j] = -INFINITY;
+            worsts[r] = -INFINITY;
+            nsubs[r] = 0;
+        }
         int it = 0;
         for (int64_t t = t_lo; t < t_hi; ++t, ++it) {
             const int acc = it & 1;
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
-            const uint32_t base = tmem + acc * kSN + (static_cast<uint32_t>(quarter * 32) << 16);
             const int64_t id0 = t * kSN;
             const bool full_tile = id0 + kSN <= k_c;
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+            const int64_t row = m0 + r * 128 + quarter * 32 + lane;
+            const bool row_ok = row < n_rows;
+            float (&tv)[PT] = tvs[r];
+            float &worst = worsts[r];
+            int &nsub = nsubs[r];
+            const float th = (PASS != 0 && row_ok) ? theta[row] : INFINITY;
+            const uint32_t base = tmem + (acc * RT + r) * kSN + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
             for (int c0 = half * (kSN / kSHalves); c0 < (half + 1) * (kSN / kSHalves); c0 += 32) {
                 uint32_t r[32];
@@ -1362,21 +1380,27 @@ __global__ void __launch_bounds__(kSThreads, 1)
                     }
                 }
             }
+            }  // r
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        if (PASS == 2 && row_ok) list_n[(row * gridDim.y + blockIdx.y) * kSHalves + half] = nsub;
-        if (PASS == 0 && row_ok) {
-            // one partial list per (split, column half): n_split * kSHalves lists per row
-            float *o = out_vals + ((row * gridDim.y + blockIdx.y) * kSHalves + half) * kMaxPtc;
 #pragma unroll
-            for (int j = 0; j < kMaxPtc; ++j) o[j] = j < PT ? tv[j < PT ? j : 0] : -INFINITY;
+        for (int r = 0; r < RT; ++r) {
+            const int64_t row = m0 + r * 128 + quarter * 32 + lane;
+            if (row >= n_rows) continue;
+            if (PASS == 2) list_n[(row * gridDim.y + blockIdx.y) * kSHalves + half] = nsubs[r];
+            if (PASS == 0) {
+                // one partial list per (split, column half): n_split * kSHalves lists per row
+                float *o = out_vals + ((row * gridDim.y + blockIdx.y) * kSHalves + half) * kMaxPtc;
+#pragma unroll
+                for (int j = 0; j < kMaxPtc; ++j) o[j] = j < PT ? tvs[r][j < PT ? j : 0] : -INFINITY;
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 256);
+    if (warp == 1) tmem_dealloc(tmem, 256 * RT);
 }
 
 // theta = (P-th best approx over all splits) - 2 eps
@@ -1707,13 +1731,13 @@ extern "C" int dsrt_prefilter(const double *Q, int64_t n_q, int m_q, int d, cons
 
 // ---------------------------------------------------------- TC entry points
 namespace dsrt {
-template <int PASS, int PT>
+template <int PASS, int PT, int RT = 1>
 static int launch_screen(dim3 g, size_t smem, cudaStream_t st, const CUtensorMap &mq, const CUtensorMap &mc,
                          int64_t rows, int64_t k_c, int64_t tps, int P, float *vals, const float *theta,
                          ScreenCand *lists, int32_t *listn, uint32_t idesc, float *cmaxes = nullptr) {
-    DSRT_CUDA(cudaFuncSetAttribute(pf_screen_kernel<PASS, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    pf_screen_kernel<PASS, PT><<<g, kSThreads, smem, st>>>(mq, mc, rows, k_c, tps, P, vals, theta, lists,
-                                                           listn, idesc, cmaxes);
+    DSRT_CUDA(cudaFuncSetAttribute(pf_screen_kernel<PASS, PT, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    pf_screen_kernel<PASS, PT, RT><<<g, kSThreads, smem, st>>>(mq, mc, rows, k_c, tps, P, vals, theta, lists,
+                                                               listn, idesc, cmaxes);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
@@ -1734,20 +1758,28 @@ struct TcWs {
     int64_t n_split, row_words, tiles_per_split;
 };
 constexpr size_t kCmaxCap = size_t(1) << 30;
+// Query-row tiles per screen CTA: 2 once there are enough rows to fill the GPU
+// with 256-row CTAs (each streamed centroid tile then feeds two MMAs).
+static int screen_rt(int64_t rows) {
+    if (const char *e = getenv("DSRT_SCREEN_RT")) return atoi(e) >= 2 ? 2 : 1;
+    return (rows + 255) / 256 >= 8 ? 2 : 1;
+}
 static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int P) {
     TcWs w{};
     const int64_t rows = n_q * m_q;
-    const int64_t m_tiles = (rows + 127) / 128;
+    const int rt = screen_rt(rows);
+    const int64_t m_tiles = (rows + 128 * rt - 1) / (128 * rt);  // CTA row tiles
     const int64_t n_tiles = (k_c + kSN - 1) / kSN;
     const int sms = sm_count();
     // about one wave of CTAs: fewer splits amortise each row's list warm-up
-    int64_t bs = tmax<int64_t>(1, tmin<int64_t>(n_tiles, (sms + m_tiles / 2) / m_tiles));
+    int64_t bs = rt == 1 ? (sms + m_tiles / 2) / m_tiles : sms / m_tiles;
+    bs = tmax<int64_t>(1, tmin<int64_t>(n_tiles, bs));
     if (const char *e = getenv("DSRT_SCREEN_SPLIT")) bs = tmax<int64_t>(1, tmin<int64_t>(n_tiles, atoi(e)));
     w.n_split = bs;
     w.tiles_per_split = (n_tiles + bs - 1) / bs;
     w.n_split = (n_tiles + w.tiles_per_split - 1) / w.tiles_per_split;
     w.row_words = row_words_for(n_docs, m_q * P);
-    w.q16 = align256(static_cast<size_t>(m_tiles * 128) * 128 * 2);
+    w.q16 = align256(static_cast<size_t>(m_tiles * 128 * rt) * 128 * 2);
     w.screen = align256(static_cast<size_t>(rows) * w.n_split * kSHalves * kMaxPtc * sizeof(float));
     w.theta = align256(static_cast<size_t>(rows) * sizeof(float));
     // per-writer candidate sub-lists: (row, split, column half) x kCandMax
@@ -1807,11 +1839,13 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     uint8_t *cnt_ws = ws + o; o += w.cnt_ws;
     float *cmaxes = w.cmax > 0 ? reinterpret_cast<float *>(ws + o) : nullptr;
     const int64_t rows = n_q * m_q;
+    const int rt = screen_rt(rows);
     const int64_t m_tiles = (rows + 127) / 128;
+    const int64_t q_rows = ((rows + 128 * rt - 1) / (128 * rt)) * 128 * rt;  // padded, zero-filled
     DSRT_CUDA(cudaMemsetAsync(q16, 0, w.q16, st));
     to_f16_rows_kernel<double><<<static_cast<unsigned>((rows + 7) / 8), 256, 0, st>>>(Q, rows, d, 0.0, q16);
     CUtensorMap mq, mc;
-    int rc = make_tmap_2d(&mq, q16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, m_tiles * 128, 256, 64, 128,
+    int rc = make_tmap_2d(&mq, q16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, q_rows, 256, 64, 128,
                           CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
     rc = make_tmap_2d(&mc, cents_f16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 128, k_c, 256, 64, kSN,
@@ -1820,9 +1854,15 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     const size_t smem = 1024 + 2 * 128 * 128 + kSStages * 2 * kSN * 128;
     dim3 g(static_cast<unsigned>(m_tiles), static_cast<unsigned>(w.n_split));
     const uint32_t idesc = idesc_f16(128, kSN, 0, 0);
-    rc = P <= 4 ? launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes)
-       : P <= 8 ? launch_screen<0, 8>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes)
-                : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes);
+    if (rt == 2 && P <= 4) {  // two row tiles per CTA share each centroid tile
+        const dim3 g2(static_cast<unsigned>(q_rows / 256), static_cast<unsigned>(w.n_split));
+        rc = launch_screen<0, 4, 2>(g2, smem + 2 * 128 * 128, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals,
+                                    nullptr, nullptr, nullptr, idesc, cmaxes);
+    } else {
+        rc = P <= 4 ? launch_screen<0, 4>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes)
+           : P <= 8 ? launch_screen<0, 8>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes)
+                    : launch_screen<0, 12>(g, smem, st, mq, mc, rows, k_c, w.tiles_per_split, P, vals, nullptr, nullptr, nullptr, idesc, cmaxes);
+    }
     if (rc) return rc;
     // eps in normalised units (|q^| = 1, |c*s| <= 1)
     pf_theta_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
