@@ -283,8 +283,9 @@ extern "C" int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, 
     const size_t smem = static_cast<size_t>(cap) * (2 * sizeof(uint64_t) + sizeof(int64_t));
     DSRT_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(kTopkMax * (2 * sizeof(uint64_t) + sizeof(int64_t)))));
-    // short rows (candidate lists): small CTAs, many per SM
-    const int threads = n <= 8192 ? 256 : kTopkThreads;
+    // short rows (candidate lists) in a large batch: small CTAs, several per SM; a small
+    // batch keeps 1024 threads per row (latency)
+    const int threads = (n <= 8192 && n_rows >= sm_count()) ? 256 : kTopkThreads;
     topk_kernel<<<static_cast<unsigned>(n_rows), threads, smem, as_stream(stream)>>>(
         scores, ld, ids, ids_ld, n_valid, n, k, out_scores, out_ids, out_pos);
     DSRT_LAUNCH_CHECK();
