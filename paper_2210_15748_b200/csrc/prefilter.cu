@@ -1791,7 +1791,8 @@ static TcWs tc_ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, int 
     w.cnt_ws = count_ws_bytes(n_q, m_q, P, k_c, n_docs);
     // pass-0 chunk maxima for the chunk-driven candidate pass (else a second GEMM pass)
     const size_t cmax = static_cast<size_t>(n_tiles) * (kSN / 32) * rows * sizeof(float);
-    w.cmax = cmax <= kCmaxCap ? align256(cmax) : 0;
+    const char *g2 = getenv("DSRT_SCREEN_GEMM2");  // tests: force the second-GEMM candidate pass
+    w.cmax = (cmax <= kCmaxCap && !(g2 != nullptr && g2[0] == '1')) ? align256(cmax) : 0;
     w.total = w.q16 + w.screen + w.theta + w.lists + w.listn + w.probed + w.fallback + w.counts + w.cnt_ws +
               w.cmax;
     return w;

@@ -243,7 +243,9 @@ def test_topk_n_valid_and_per_row_ids():
 
 
 # ----------------------------------------------------------------- prefilter
-def test_prefilter_golden(golden_prefilter):
+@pytest.mark.parametrize("gemm2", ["0", "1"])  # chunk-max candidates / second screen GEMM
+def test_prefilter_golden(golden_prefilter, gemm2, monkeypatch):
+    monkeypatch.setenv("DSRT_SCREEN_GEMM2", gemm2)
     g = golden_prefilter
     sizes = g["doc_sizes"]
     off = np.concatenate([[0], np.cumsum(sizes)])
@@ -898,8 +900,10 @@ def _tc_prefilter_case(seed, n_docs, k, dup_noise=None):
     return rng, docs, C
 
 
+@pytest.mark.parametrize("gemm2", ["0", "1"])  # chunk-max candidates / second screen GEMM
 @pytest.mark.parametrize("seed,dup", [(1, None), (2, 1e-5), (3, 1e-3)])
-def test_prefilter_tensor_core_screen_exact(seed, dup):
+def test_prefilter_tensor_core_screen_exact(seed, dup, gemm2, monkeypatch):
+    monkeypatch.setenv("DSRT_SCREEN_GEMM2", gemm2)
     from paper_2210_15748_b200 import prefilter as pf
     rng, docs, C = _tc_prefilter_case(seed, 3000, 1000, dup)
     cents = d.Centroids(k=C.shape[0], seed=0, vectors=C)
@@ -916,8 +920,9 @@ def test_prefilter_tensor_core_screen_exact(seed, dup):
         cand, n_cand = pf.filter_candidates_device(cindex, cents, Qd, m_q, probe, kf, use_tc=True)
         got = cand[0, : int(n_cand[0])].cpu().numpy()
         np.testing.assert_array_equal(got, want, err_msg=f"case {t} probe {probe}")
-    # batched: many query sets at once vs the exact SIMT kernel
-    Qb = torch.from_numpy(rng.standard_normal((40 * 32, 128))).to(DEV)
+    # batched: many query sets at once vs the exact SIMT kernel (2240 rows: two-row-tile
+    # screen CTAs with a partial last tile)
+    Qb = torch.from_numpy(rng.standard_normal((70 * 32, 128))).to(DEV)
     a, na = pf.filter_candidates_device(cindex, cents, Qb, 32, 4, 300, use_tc=True)
     b, nb = pf.filter_candidates_device(cindex, cents, Qb, 32, 4, 300, use_tc=False)
     assert torch.equal(na, nb) and torch.equal(a, b)
