@@ -180,11 +180,14 @@ size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n
 /*
  * K5, tensor-core screen (same results as dsrt_prefilter): tcgen05 fp16 GEMM of
  * normalised Q rows against centroids_f16 = fp16(centroids / cent_max_norm).
- * Pass 0 finds each row's probe-th best approximate similarity A_P; pass 1
- * collects every centroid with approx >= A_P - 2 eps (eps = the screen's
- * rigorous error bound), which are re-ranked in float64 (ties -> lower
- * centroid id); rows with more than 32 such centroids fall back to the exact
- * float64 scan.  d = 128, probe <= 12.
+ * The GEMM pass keeps each row's probe-th best 32-column chunk maximum A'_P and
+ * records every chunk maximum; every centroid of a chunk reaching
+ * A'_P - 2 eps (eps = the screen's rigorous error bound) is re-approximated
+ * from the same fp16 operands and kept if >= A'_P - 2 eps (a second GEMM pass
+ * collects them instead when the chunk-maximum buffer would exceed 1 GB).  The
+ * kept centroids are re-ranked in float64 (ties -> lower centroid id); rows with
+ * more than 32 fall back to the exact float64 scan.  Selection as
+ * dsrt_prefilter.  d = 128, probe <= 12.
  */
 int dsrt_prefilter_tc(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
                       const void *centroids_f16, double cent_max_norm, int64_t k_c,
