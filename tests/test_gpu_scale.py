@@ -4,9 +4,11 @@
   (scores and top-100), plus top-k invariants for all 1,000 query sets.
 * cfg3 pipeline at full size (1M sets, 65,536 centroids): prefilter candidates
   (oracle filter_candidates over the device postings), candidate scores and
-  top-100 for 4 query sets.
+  top-100 for 16 query sets (>= 16).
 * cfg4 shape (L=32, C=8 codes from records): 2 query sets x 300k sets exact,
   and sampled (query set, set) pairs for 1,024 query sets.
+* cfg4 at full size: one query set over all 8,000,000 sets (~560M vectors) exact
+  vs the C oracle, streamed in 500k-set chunks, and its top-1,000.
 """
 
 import numpy as np
@@ -77,7 +79,8 @@ def test_cfg3_pipeline_full_size_parity():
     centroids = prefilter.Centroids(k=n_cent, seed=0, vectors=cvec.cpu().numpy())
     cindex = prefilter.build_centroid_index(X, centroids, set_off=idx.set_off, n_docs=n_sets)
     idx.filter = (centroids, cindex)
-    Qv = workloads.gpu_queries(X, off, 4, 32, seed=502)
+    n_chk = 16
+    Qv = workloads.gpu_queries(X, off, n_chk, 32, seed=502)
     # spot-check the native postings: argmax of a vector sample, float64
     samp = torch.arange(0, X.shape[0], 997, device=DEV)
     Xs = X[samp].double()
@@ -92,10 +95,10 @@ def test_cfg3_pipeline_full_size_parity():
     postings = [pdocs[po[c]:po[c + 1]] for c in range(n_cent)]
     res = d.query_batch(idx, Qv, 100)
     qc, _ = d.lsh.hash_device(idx.family, Qv.reshape(-1, 128).contiguous(), want_records=False)
-    qcodes = qc.cpu().numpy().astype(np.int64).reshape(4, 32, L)
+    qcodes = qc.cpu().numpy().astype(np.int64).reshape(n_chk, 32, L)
     records = idx.records.cpu().numpy()
     lut = idx.lookup.table
-    for r in range(4):
+    for r in range(n_chk):
         Qr = Qv[r].double().cpu().numpy()
         cand = O.filter_candidates(postings, n_sets, centroids.vectors, Qr, probe, k_filter)
         got_c, n_c = prefilter.filter_candidates_device(cindex, centroids, Qv[r].double(), 32,
@@ -137,3 +140,35 @@ def test_cfg4_shape_sampled_parity():
     for r in range(2):
         top = O.rank_topk(want2[r], np.arange(n_sets), 1000)
         assert [x for x, _ in top] == list(out_i[r].cpu().numpy())
+
+
+def test_cfg4_full_size_one_query_set():
+    """cfg4 at BASELINE size: query set 0 scored over all 8M sets by the device
+    (exhaustive K3) vs the C oracle on the codes read back from the records, in
+    500k-set chunks (the full int32 code matrix would be 72 GB on the host); then
+    the device top-1,000 vs the oracle ranking (score desc, id asc)."""
+    n_sets, L, C, top_k = 8_000_000, 32, 8, 1000
+    sizes = workloads.set_sizes(n_sets, 70, 25, seed=400)
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
+    recs, Qv = workloads.gpu_codes_only(sizes, cfg, n_centroids=262_144, n_qsets=2, m_q=32,
+                                        seed=401, device=DEV)
+    idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
+    qc, qrecs = d.lsh.hash_device(idx.family, Qv[:1].reshape(-1, 128).contiguous())
+    qcodes = qc.cpu().numpy().astype(np.int64).reshape(1, 32, L)
+    off = workloads.offsets(sizes)
+    got, _ = engine.score_all(idx.records, idx.set_off, qrecs, 32, L, C, idx.lut_dev)
+    got = got[0].cpu().numpy()
+    lut = idx.lookup.table
+    step = 500_000
+    want = np.empty(n_sets, dtype=np.float64)
+    for s0 in range(0, n_sets, step):
+        s1 = min(n_sets, s0 + step)
+        v0, v1 = int(off[s0]), int(off[s1])
+        codes = _records_to_codes_dev(recs[v0:v1], L, C).cpu().numpy()
+        want[s0:s1] = c_oracle.score(codes, off[s0:s1 + 1] - v0, qcodes, lut)[0]
+        del codes
+    np.testing.assert_array_equal(got, want)
+    order = np.lexsort((np.arange(n_sets), -want))[:top_k]
+    out_s, out_i = d.query_codes_batch(idx, qcodes, top_k, return_tensors=True)
+    np.testing.assert_array_equal(out_i[0].cpu().numpy().astype(np.int64), order)
+    np.testing.assert_array_equal(out_s[0].cpu().numpy(), want[order])
