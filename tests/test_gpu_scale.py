@@ -1,7 +1,8 @@
 """Parity at BASELINE.json sizes (GPU).
 
 * cfg1 at full size: all 100,000 sets x 8 query sets, bit-exact vs the C oracle
-  (scores and top-100), plus top-k invariants for all 1,000 query sets.
+  (scores and top-100), top-k invariants for all 1,000 query sets, and 4,096
+  sampled (query set, set) pairs across all 1,000.
 * cfg3 pipeline at full size (1M sets, 65,536 centroids): prefilter candidates
   (oracle filter_candidates over the device postings), candidate scores and
   top-100 for 16 query sets (>= 16).
@@ -62,6 +63,16 @@ def test_cfg1_full_size_parity():
     # invariants for all 1000 rows: sorted by (score desc, id asc), unique ids
     assert np.all((S[:, :-1] > S[:, 1:]) | ((S[:, :-1] == S[:, 1:]) & (I[:, :-1] < I[:, 1:])))
     assert all(len(set(row)) == 100 for row in I)
+    # 4096 random (query set, set) pairs across all 1000 query sets vs the oracle
+    qa, _ = d.lsh.hash_device(idx.family, Qv.reshape(-1, 128).contiguous(), want_records=False)
+    qall = qa.cpu().numpy().astype(np.int64).reshape(1000, 32, L)
+    full, _ = d.score_matrix(idx, qall)
+    rng = np.random.default_rng(17)
+    qs = rng.integers(0, 1000, size=4096)
+    ss = rng.integers(0, n_sets, size=4096)
+    g = full[torch.from_numpy(qs).to(DEV), torch.from_numpy(ss).to(DEV)].cpu().numpy()
+    w = c_oracle.score(codes, off, qall[qs], idx.lookup.table, sets=ss[:, None])[:, 0]
+    np.testing.assert_array_equal(g, w)
 
 
 def test_cfg3_pipeline_full_size_parity():
