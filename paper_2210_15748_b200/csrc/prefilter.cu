@@ -1328,18 +1328,28 @@ __global__ void __launch_bounds__(kSThreads, 1)
                     for (int j = 0; j < 32; ++j)
                         if (id0 + c0 + j >= k_c) r[j] = __float_as_uint(-INFINITY);
                 }
-                // chunk maximum (tree, independent FMNMX) -> one vote per 32 values
-                float m16[16];
+                // chunk maximum (trees over the two 16-column halves, independent FMNMX)
+                // -> one vote per 32 values
+                float ma[8], mb[8];
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    m16[j] = fmaxf(__uint_as_float(r[j]), __uint_as_float(r[j + 16]));
+                for (int j = 0; j < 8; ++j) {
+                    ma[j] = fmaxf(__uint_as_float(r[j]), __uint_as_float(r[j + 8]));
+                    mb[j] = fmaxf(__uint_as_float(r[j + 16]), __uint_as_float(r[j + 24]));
+                }
 #pragma unroll
-                for (int w = 8; w > 0; w >>= 1)
+                for (int w = 4; w > 0; w >>= 1)
 #pragma unroll
-                    for (int j = 0; j < w; ++j) m16[j] = fmaxf(m16[j], m16[j + w]);
-                const float cmax = m16[0];
-                // chunk maxima for the chunk-driven candidate pass ([chunk][row]: coalesced)
-                if (PASS == 0 && cmaxes != nullptr && row_ok) cmaxes[((id0 + c0) >> 5) * n_rows + row] = cmax;
+                    for (int j = 0; j < w; ++j) {
+                        ma[j] = fmaxf(ma[j], ma[j + w]);
+                        mb[j] = fmaxf(mb[j], mb[j + w]);
+                    }
+                const float cmax = fmaxf(ma[0], mb[0]);
+                // half-chunk maxima for the chunk-driven candidate pass ([chunk][row]: coalesced),
+                // as fp16 rounded UP (an upper bound: a half reaching theta is never missed)
+                if (PASS == 0 && cmaxes != nullptr && row_ok)
+                    reinterpret_cast<uint32_t *>(cmaxes)[((id0 + c0) >> 5) * n_rows + row] =
+                        static_cast<uint32_t>(__half_as_ushort(__float2half_ru(ma[0]))) |
+                        (static_cast<uint32_t>(__half_as_ushort(__float2half_ru(mb[0]))) << 16);
                 if (PASS == 0) {
                     // top-P of the chunk maxima: P real values of the row, so their
                     // P-th best A'_P <= A_P and theta' = A'_P - 2 eps keeps pass 1 a
@@ -1464,10 +1474,13 @@ __global__ void pf_theta_kernel(const float *__restrict__ vals, int n_split, int
 // Soundness: an exact top-P centroid has approx >= exact - eps >= theta under
 // either rounding, so its chunk's maximum reaches theta and it is appended.
 // span: chunks per warp (multiple of 8), sized by the host for enough warps.
+// cmaxes holds per (chunk, row) the two 16-column half maxima as fp16 rounded up;
+// only halves reaching theta are recomputed (2 lanes per centroid, 64 dims each).
 __global__ void __launch_bounds__(256)
-    pf_chunk_cand_kernel(const float *__restrict__ cmaxes, int64_t n_chunks, int span, const float *__restrict__ theta,
-                         const __half *__restrict__ q16, const __half *__restrict__ c16, int64_t k_c,
-                         int64_t n_rows, ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n) {
+    pf_chunk_cand_kernel(const uint32_t *__restrict__ cmaxes, int64_t n_chunks, int span,
+                         const float *__restrict__ theta, const __half *__restrict__ q16,
+                         const __half *__restrict__ c16, int64_t k_c, int64_t n_rows,
+                         ScreenCand *__restrict__ lists, int32_t *__restrict__ list_n) {
     __shared__ float qf[8][128];  // the current match's query row, as float
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
@@ -1477,8 +1490,9 @@ __global__ void __launch_bounds__(256)
     const int64_t row = r0 + lane;
     const bool row_ok = row < n_rows;
     const float th = row_ok ? theta[row] : INFINITY;
-    // one (row, chunk) match: lane = centroid of the chunk
-    auto process = [&](int l, int64_t j) {
+    const int part = lane >> 4;  // which 64 dims of the centroid this lane sums
+    // one (row, chunk half) match: lanes (c, c + 16) share centroid c of the half
+    auto process = [&](int l, int64_t j, int hh) {
         const int64_t rr = r0 + l;
         const float thr = __shfl_sync(0xffffffffu, th, l);
         {  // stage the query row as float (lane k: dims 4k .. 4k+3)
@@ -1488,19 +1502,19 @@ __global__ void __launch_bounds__(256)
             reinterpret_cast<float4 *>(qf[warp])[lane] = make_float4(a.x, a.y, b.x, b.y);
         }
         __syncwarp();
-        const int64_t cid = j * 32 + lane;
-        float acc = -INFINITY;
+        const int64_t cid = j * 32 + hh * 16 + (lane & 15);
+        float acc = 0.f;
         if (cid < k_c) {
-            const uint4 *cv = reinterpret_cast<const uint4 *>(c16 + cid * 128);
-            uint4 c[16];
+            const uint4 *cv = reinterpret_cast<const uint4 *>(c16 + cid * 128) + part * 8;
+            uint4 c[8];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) c[k] = __ldg(cv + k);
+            for (int k = 0; k < 8; ++k) c[k] = __ldg(cv + k);
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < 8; ++k) {
                 const __half2 *ch2 = reinterpret_cast<const __half2 *>(&c[k]);
-                const float4 q0 = reinterpret_cast<const float4 *>(qf[warp])[2 * k];
-                const float4 q1 = reinterpret_cast<const float4 *>(qf[warp])[2 * k + 1];
+                const float4 q0 = reinterpret_cast<const float4 *>(qf[warp])[part * 16 + 2 * k];
+                const float4 q1 = reinterpret_cast<const float4 *>(qf[warp])[part * 16 + 2 * k + 1];
                 const float2 c0 = __half22float2(ch2[0]), c1 = __half22float2(ch2[1]);
                 const float2 c2 = __half22float2(ch2[2]), c3 = __half22float2(ch2[3]);
                 a0 = fmaf(q0.x, c0.x, a0); a1 = fmaf(q0.y, c0.y, a1);
@@ -1510,8 +1524,9 @@ __global__ void __launch_bounds__(256)
             }
             acc = a0 + a1;
         }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
         __syncwarp();
-        const bool ok = acc >= thr;
+        const bool ok = lane < 16 && cid < k_c && acc >= thr;
         const unsigned okm = __ballot_sync(0xffffffffu, ok);
         int base = 0;
         if (lane == 0 && okm != 0u) base = atomicAdd(list_n + rr, __popc(okm));
@@ -1520,17 +1535,21 @@ __global__ void __launch_bounds__(256)
         if (ok && slot < kCandMax) lists[rr * kCandMax + slot] = ScreenCand{acc, static_cast<int32_t>(cid)};
     };
     for (int64_t jb = j0; jb < j1; jb += 8) {
-        float v[8];
+        uint32_t v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            v[u] = (row_ok && jb + u < j1) ? __ldg(cmaxes + (jb + u) * n_rows + row) : -INFINITY;
+            v[u] = (row_ok && jb + u < j1) ? __ldg(cmaxes + (jb + u) * n_rows + row) : 0xfc00fc00u;  // -inf
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            unsigned m = __ballot_sync(0xffffffffu, v[u] >= th);
+            const bool h0 = __half2float(__ushort_as_half(static_cast<unsigned short>(v[u] & 0xffffu))) >= th;
+            const bool h1 = __half2float(__ushort_as_half(static_cast<unsigned short>(v[u] >> 16))) >= th;
+            const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+            unsigned m = m0 | m1;
             while (m != 0u) {
                 const int l = __ffs(m) - 1;
                 m &= m - 1u;
-                process(l, jb + u);
+                if ((m0 >> l) & 1u) process(l, jb + u, 0);
+                if ((m1 >> l) & 1u) process(l, jb + u, 1);
             }
         }
     }
@@ -1876,7 +1895,7 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
         const int64_t want = 512LL * sm_count();  // many short spans: matches are latency-bound
         const int span = static_cast<int>(tmax<int64_t>(8, tmin<int64_t>(64, ((n_chunks * rgroups / want) + 7) / 8 * 8)));
         const dim3 gc(static_cast<unsigned>(rgroups), static_cast<unsigned>((n_chunks + 8LL * span - 1) / (8LL * span)));
-        pf_chunk_cand_kernel<<<gc, 256, 0, st>>>(cmaxes, n_chunks, span, theta, q16,
+        pf_chunk_cand_kernel<<<gc, 256, 0, st>>>(reinterpret_cast<const uint32_t *>(cmaxes), n_chunks, span, theta, q16,
                                                   static_cast<const __half *>(cents_f16), k_c, rows, lists, listn);
         pf_rerank_kernel<double><<<static_cast<unsigned>((rows * 32 + 255) / 256), 256, 0, st>>>(
             lists, listn, Q, cents, rows, d, P, probed, fallback);
