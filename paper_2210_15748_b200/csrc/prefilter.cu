@@ -367,7 +367,7 @@ __device__ __forceinline__ uint32_t count_of(const uint32_t *row, int64_t doc) {
     return (row[doc >> 1] >> (16 * (doc & 1))) & 0xffffu;
 }
 
-// Large batches: one CTA per query set.  Counters are u8 (u16) lanes of uint32
+// u16 counters (m_q * probe > 255), large batches: one CTA per query set.  Counters are u8 (u16) lanes of uint32
 // words.  The count histogram is the sum of the counting pass's chunk
 // histograms; c* = largest c with #(count > c) + hist[c] >= k_filter.  One
 // ordered pass (ascending doc order, 4 x uint4 per thread per step) takes every
@@ -1096,8 +1096,8 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
         int64_t *ties = reinterpret_cast<int64_t *>(hits + static_cast<size_t>(n_q) * k_filter);
         sel_plan_kernel<<<static_cast<unsigned>(n_q), 128, (max_count + 1) * sizeof(uint32_t), st>>>(
             chist, nch, max_count, k_filter, plan, tie_base, hits_n);
-        auto sk = cb == 8 ? sel_scan_kernel<8> : sel_scan_kernel<16>;
-        sk<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kScanThreads, 0, st>>>(
+        // (u8 counters never get here: they are placed above)
+        sel_scan_kernel<16><<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kScanThreads, 0, st>>>(
             counts, row_words, nch, k_filter, plan, tie_base, hits_n, hits, ties);
         int p2 = 1;
         while (p2 < k_filter) p2 <<= 1;
@@ -1109,15 +1109,9 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
         return DSRT_OK;
     }
     const size_t smem = kSelMax * sizeof(uint64_t) + (max_count + 1) * sizeof(uint32_t);
-    if (cb == 8) {
-        DSRT_CUDA(cudaFuncSetAttribute(select_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        select_kernel<8><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
-            counts, row_words, n_docs, max_count, k_filter, cand, n_cand, chist, nch);
-    } else {
-        DSRT_CUDA(cudaFuncSetAttribute(select_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        select_kernel<16><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
-            counts, row_words, n_docs, max_count, k_filter, cand, n_cand, chist, nch);
-    }
+    DSRT_CUDA(cudaFuncSetAttribute(select_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    select_kernel<16><<<static_cast<unsigned>(n_q), kSelThreads, smem, st>>>(
+        counts, row_words, n_docs, max_count, k_filter, cand, n_cand, chist, nch);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
@@ -1145,8 +1139,9 @@ static PrefilterWs ws_layout(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs, 
 // tcgen05.  Pass 0 finds a lower bound A'_P <= A_P of each row's P-th best
 // approx value: the P-th best of the 32-column chunk maxima (P real values of
 // the row; one insertion per chunk instead of per value).  Every centroid with
-// approx >= A'_P - 2 eps (pass 1, a second cheap GEMM sweep) is re-ranked in
-// float64 -- that set provably contains the exact top-P, ties included; rows
+// approx >= A'_P - 2 eps (found from the recorded half-chunk maxima, or by a
+// second GEMM sweep) is re-ranked in float64 -- that set provably contains the
+// exact top-P, ties included; rows
 // with more than kCandMax such centroids fall back to the exact float64 scan.  eps bounds |approx - exact| for unit-bounded rows:
 // fp16 operand rounding 2u(1+u) with u = 2^-11 plus fp32 accumulation.
 // ====================================================================
