@@ -197,22 +197,21 @@ __device__ __forceinline__ void scan_split(const uint32_t (&q)[2][K * W], int (&
             rmin[s] = min3<K, W>(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)),
                                  mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xb)));
     }
-    if (p < np) {
-        uint4 xa[R / 4];
+    // one tail block for the last 1-3 vectors: half h takes 2p + h and 2p + 2 + h,
+    // indices clamped to nv - 1 (a repeated vector leaves the minimum unchanged)
+    if (2 * p < nv) {
+        const int va = min(2 * p + h, nv - 1), vb = min(2 * p + 2 + h, nv - 1);
+        const uint4 *xr = reinterpret_cast<const uint4 *>(xs);
+        uint4 xa[R / 4], xb[R / 4];
 #pragma unroll
-        for (int u = 0; u < R / 4; ++u) xa[u] = x4[(2 * p) * (R / 4) + u];
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-            rmin[s] = min(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)));
-    }
-    if (nv & 1) {  // the odd last vector: both halves take it (min is idempotent)
-        const uint4 *xl = reinterpret_cast<const uint4 *>(xs) + (nv - 1) * (R / 4);
-        uint4 xa[R / 4];
-#pragma unroll
-        for (int u = 0; u < R / 4; ++u) xa[u] = xl[u];
+        for (int u = 0; u < R / 4; ++u) {
+            xa[u] = xr[va * (R / 4) + u];
+            xb[u] = xr[vb * (R / 4) + u];
+        }
 #pragma unroll
         for (int s = 0; s < 2; ++s)
-            rmin[s] = min(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)));
+            rmin[s] = min3<K, W>(rmin[s], mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xa)),
+                                 mismatches<K, W>(q[s], reinterpret_cast<const uint32_t *>(xb)));
     }
 }
 
