@@ -738,10 +738,14 @@ static size_t place_smem(int max_count, int k_filter) {
 // Shared tail of the placement kernels: above[] holds the global count
 // histogram and pre[] the counts of earlier chunks (both [max_count + 1], in
 // shared memory, synced); cw the chunk's nw counter words (after `bar`, if any).
+// plan (optional): (c*, H, need) precomputed by sel_plan8_kernel, in which case
+// pre[] already holds this chunk's slot bases (pre[c*] = its first tie rank,
+// pre[c] = #(count > c) + earlier chunks' count-c docs for c > c*) and above[]
+// is unused.
 __device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t *bar, int ch, int64_t qs,
                                             int max_count, int k_filter, uint32_t *above, uint32_t *pre,
                                             uint32_t *hl, int64_t *__restrict__ cand,
-                                            int32_t *__restrict__ n_cand) {
+                                            int32_t *__restrict__ n_cand, const int4 *plan = nullptr) {
     constexpr int W_CH = kChunkBytes / 4;      // counter words per chunk
     constexpr int SW = W_CH / kPlaceThreads;   // words per thread strip (128 docs)
     constexpr uint32_t ONE = 0x01010101u;
@@ -749,7 +753,14 @@ __device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t
     __shared__ int s_cstar, s_need, s_H;
     const int nb = max_count + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (warp == 0) {  // descending suffix scan of the histogram: c*, H, need; above[c] for c >= c*
+    if (plan != nullptr) {
+        if (tid == 0) {
+            const int4 pl = *plan;
+            s_cstar = pl.x;
+            s_H = pl.y;
+            s_need = pl.z;
+        }
+    } else if (warp == 0) {  // descending suffix scan of the histogram: c*, H, need; above[c] for c >= c*
         const uint32_t g1 = nb > 1 ? above[1] : 0u;
         uint32_t carry = 0;
         int cstar = -1;
@@ -861,7 +872,8 @@ __device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t
     __syncthreads();
     if (warp == 0 && nh > 0) {  // rank hits per count in doc order, 32 at a time
         // pre[c] becomes this chunk's running slot base for count c
-        for (int b = lane + static_cast<int>(cstar) + 1; b < nb; b += 32) pre[b] += above[b];
+        if (plan == nullptr)
+            for (int b = lane + static_cast<int>(cstar) + 1; b < nb; b += 32) pre[b] += above[b];
         __syncwarp();
         for (uint32_t i0 = 0; i0 < nh; i0 += 32) {
             const uint32_t i = i0 + lane;
@@ -887,12 +899,76 @@ __device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t
     }
 }
 
+// Placement plan per query set (u8 counters), computed once instead of by each
+// of its chunk CTAs: c*, H, need from the summed chunk histograms, and per chunk
+// the slot bases (tie base at c*, hit bases above it) -> plan[qs], bases[qs][ch][c].
+__global__ void __launch_bounds__(256)
+    sel_plan8_kernel(const uint32_t *__restrict__ chist, int nch, int max_count, int k_filter,
+                     int4 *__restrict__ plan, uint32_t *__restrict__ bases) {
+    extern __shared__ uint32_t pl_s[];  // [nb] histogram -> suffix counts
+    __shared__ int s_cstar, s_H, s_need;
+    const int nb = max_count + 1;
+    const int64_t qs = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(nb);
+    for (int b = tid; b < nb; b += blockDim.x) {
+        const uint32_t *gb = gh + b * static_cast<int64_t>(nch);
+        uint32_t g = 0;
+        for (int c = 0; c < nch; ++c) g += __ldg(gb + c);
+        pl_s[b] = g;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        const uint32_t g1 = nb > 1 ? pl_s[1] : 0u;
+        uint32_t carry = 0;
+        int cstar = -1;
+        for (int top = max_count; top >= 1 && cstar < 0; top -= 32) {
+            const int b = top - lane;
+            const uint32_t g = b >= 1 ? pl_s[b] : 0u;
+            uint32_t incl = g;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, b >= 1 && carry + incl >= static_cast<uint32_t>(k_filter));
+            if (b >= 1) pl_s[b] = carry + incl - g;
+            if (hit != 0u) cstar = top - (__ffs(hit) - 1);
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (cstar >= 1) {
+                s_cstar = cstar;
+                s_H = static_cast<int>(pl_s[cstar]);
+                s_need = k_filter - s_H;
+            } else {
+                s_cstar = 1;
+                s_H = static_cast<int>(pl_s[1]);
+                s_need = static_cast<int>(g1);
+            }
+            plan[qs] = make_int4(s_cstar, s_H, s_need, 0);
+        }
+    }
+    __syncthreads();
+    const int cstar = s_cstar;
+    for (int b = tid; b < nb; b += blockDim.x) {
+        if (b < cstar) continue;
+        const uint32_t *gb = gh + b * static_cast<int64_t>(nch);
+        uint32_t run = b == cstar ? 0u : pl_s[b];  // ties rank from 0; hits after #(count > b)
+        for (int c = 0; c < nch; ++c) {
+            bases[(qs * nch + c) * static_cast<int64_t>(nb) + b] = run;
+            run += __ldg(gb + c);
+        }
+    }
+}
+
 // Separate counting pass (written counter rows + chunk histograms): the chunk's
-// words stream into shared memory (bulk copy) while the plan is summed.
+// words stream into shared memory (bulk copy) while its slot bases are loaded.
 __global__ void __launch_bounds__(kPlaceThreads, 2)
     sel_place_kernel(const uint32_t *__restrict__ counts, int64_t row_words, int nch, int max_count,
-                     int k_filter, const uint32_t *__restrict__ chist, int64_t *__restrict__ cand,
-                     int32_t *__restrict__ n_cand) {
+                     int k_filter, const int4 *__restrict__ plan, const uint32_t *__restrict__ bases,
+                     int64_t *__restrict__ cand, int32_t *__restrict__ n_cand) {
     constexpr int W_CH = kChunkBytes / 4;
     extern __shared__ __align__(128) uint8_t psm_b[];
     uint32_t *cw = reinterpret_cast<uint32_t *>(psm_b);
@@ -912,29 +988,10 @@ __global__ void __launch_bounds__(kPlaceThreads, 2)
         mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nw) * 4u);
         bulk_g2s(cw, counts + qs * row_words + cw0, static_cast<uint32_t>(nw) * 4u, bar);
     }
-    const uint32_t *gh = chist + qs * nch * static_cast<int64_t>(nb);
-    for (int b = tid; b < nb; b += kPlaceThreads) {  // a bin's nch chunk counts are contiguous
-        const uint32_t *gb = gh + b * static_cast<int64_t>(nch);
-        uint32_t g = 0, p = 0;
-        if ((nch & 3) == 0) {  // 16-byte loads, all issued before the sums
-#pragma unroll 4
-            for (int c = 0; c < nch; c += 4) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4 *>(gb + c));
-                g += v.x + v.y + v.z + v.w;
-                p += (c < ch ? v.x : 0u) + (c + 1 < ch ? v.y : 0u) + (c + 2 < ch ? v.z : 0u) + (c + 3 < ch ? v.w : 0u);
-            }
-        } else {
-            for (int c = 0; c < nch; ++c) {
-                const uint32_t v = __ldg(gb + c);
-                g += v;
-                p += c < ch ? v : 0u;
-            }
-        }
-        above[b] = g;
-        pre[b] = p;
-    }
+    const uint32_t *bs = bases + (qs * nch + ch) * static_cast<int64_t>(nb);
+    for (int b = tid; b < nb; b += kPlaceThreads) pre[b] = __ldg(bs + b);
     __syncthreads();
-    place_chunk(cw, nw, bar, ch, qs, max_count, k_filter, above, pre, hl, cand, n_cand);
+    place_chunk(cw, nw, bar, ch, qs, max_count, k_filter, above, pre, hl, cand, n_cand, plan + qs);
 }
 
 // Fused counting + placement for n_docs <= kMaxFusedChunks * 64K (u8 counters):
@@ -1001,10 +1058,12 @@ static int64_t row_words_for(int64_t n_docs, int max_count) {
 static int n_chunks_for(int64_t n_docs, int max_count) {
     return static_cast<int>((n_docs + chunk_docs(counter_bits(max_count)) - 1) / chunk_docs(counter_bits(max_count)));
 }
+// bounds (unless cached) | chunk histograms | placement plans | per-chunk slot bases
 static size_t count_ws_chunks(int64_t n_q, int m_q, int P, int64_t k_c, int64_t n_docs) {
     const int mc = m_q * P, nch = n_chunks_for(n_docs, mc);
     return align256(static_cast<size_t>(k_c) * (nch + 1) * sizeof(int64_t)) +
-           align256(static_cast<size_t>(n_q) * nch * (mc + 1) * sizeof(uint32_t));
+           2 * align256(static_cast<size_t>(n_q) * nch * (mc + 1) * sizeof(uint32_t)) +
+           align256(static_cast<size_t>(n_q) * sizeof(int4));
 }
 static bool small_batch(int64_t n_q) { return n_q * 8 <= sm_count(); }
 // + the small-batch selection buffers (plans, tie bases, hit counts, hits, ties)
@@ -1076,11 +1135,16 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
     DSRT_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
     ck<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kCntThreads, csmem, st>>>(
         probed, m_q * P, bnd, nch, post_docs, row_words, max_count, counts, chist);
-    if (cb == 8) {  // sort-free placement (any batch)
+    if (cb == 8) {  // sort-free placement (any batch): plan per query set, then place per chunk
+        const size_t hb = align256(static_cast<size_t>(n_q) * nch * (max_count + 1) * sizeof(uint32_t));
+        uint32_t *bases = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(chist) + hb);
+        int4 *plan = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(bases) + hb);
+        sel_plan8_kernel<<<static_cast<unsigned>(n_q), 256, (max_count + 1) * sizeof(uint32_t), st>>>(
+            chist, nch, max_count, k_filter, plan, bases);
         const size_t psmem = place_smem(max_count, k_filter);
         DSRT_CUDA(cudaFuncSetAttribute(sel_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
         sel_place_kernel<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kPlaceThreads, psmem, st>>>(
-            counts, row_words, nch, max_count, k_filter, chist, cand, n_cand);
+            counts, row_words, nch, max_count, k_filter, plan, bases, cand, n_cand);
         DSRT_LAUNCH_CHECK();
         return DSRT_OK;
     }
