@@ -250,8 +250,10 @@ __device__ __forceinline__ void count_postings(uint32_t *sc, const int32_t *__re
 // Words whose bytes are all <= 3 (nearly all) are tallied without compares:
 // byte-lane sums of bit 0, bit 1 and bit0 & bit1 give n1 + n3, n2 + n3 and n3;
 // the rare words holding a count >= 4 go byte by byte through shared atomics.
+// sum_s (optional, W_CH / 128 words): bit g = 16-byte group g holds a count >= 2.
 template <int NT>
-__device__ __forceinline__ void chunk_hist8(const uint32_t *sc, uint32_t *hist, int max_count) {
+__device__ __forceinline__ void chunk_hist8(const uint32_t *sc, uint32_t *hist, int max_count,
+                                            uint32_t *sum_s = nullptr) {
     constexpr int W_CH = kChunkBytes / 4;
     constexpr uint32_t M = 0x01010101u;
     static_assert(W_CH / NT <= 64, "byte-lane sums must not overflow");
@@ -259,6 +261,10 @@ __device__ __forceinline__ void chunk_hist8(const uint32_t *sc, uint32_t *hist, 
     const uint4 *s4 = reinterpret_cast<const uint4 *>(sc);
     for (int i = threadIdx.x; i < W_CH / 4; i += NT) {
         const uint4 v = s4[i];
+        if (sum_s != nullptr) {
+            const unsigned f = __ballot_sync(0xffffffffu, ((v.x | v.y | v.z | v.w) & 0xfefefefeu) != 0u);
+            if ((threadIdx.x & 31) == 0) sum_s[i >> 5] = f;
+        }
         const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -298,7 +304,8 @@ template <int CB>
 __global__ void __launch_bounds__(kCntThreads)
     count_chunk_kernel(const int32_t *__restrict__ probed, int MP, const int64_t *__restrict__ bnd,
                        int nch, const int64_t *__restrict__ post_docs, int64_t row_words,
-                       int max_count, uint32_t *__restrict__ counts, uint32_t *__restrict__ chist) {
+                       int max_count, uint32_t *__restrict__ counts, uint32_t *__restrict__ chist,
+                       uint32_t *__restrict__ gsum) {
     constexpr int DPW = 32 / CB;
     constexpr uint32_t MASK = (1u << CB) - 1u;
     constexpr int W_CH = kChunkBytes / 4;          // counter words per chunk
@@ -317,7 +324,11 @@ __global__ void __launch_bounds__(kCntThreads)
     constexpr uint32_t ONE = CB == 8 ? 0x01010101u : 0x00010001u;
     uint32_t h1 = 0, h2 = 0, h3 = 0;
     if constexpr (CB == 8) {
-        chunk_hist8<kCntThreads>(sc, hist, max_count);
+        __shared__ uint32_t sum_s[kChunkBytes / 4 / 128];
+        chunk_hist8<kCntThreads>(sc, hist, max_count, sum_s);
+        __syncthreads();
+        for (int i = tid; i < kChunkBytes / 4 / 128; i += kCntThreads)
+            gsum[(qs * nch + ch) * (kChunkBytes / 4 / 128) + i] = sum_s[i];
     } else {
     for (int i = tid; i < W_CH; i += kCntThreads) {
         const uint32_t x = sc[i];
@@ -745,7 +756,8 @@ static size_t place_smem(int max_count, int k_filter) {
 __device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t *bar, int ch, int64_t qs,
                                             int max_count, int k_filter, uint32_t *above, uint32_t *pre,
                                             uint32_t *hl, int64_t *__restrict__ cand,
-                                            int32_t *__restrict__ n_cand, const int4 *plan = nullptr) {
+                                            int32_t *__restrict__ n_cand, const int4 *plan = nullptr,
+                                            uint32_t gmask2 = 0xffu) {
     constexpr int W_CH = kChunkBytes / 4;      // counter words per chunk
     constexpr int SW = W_CH / kPlaceThreads;   // words per thread strip (128 docs)
     constexpr uint32_t ONE = 0x01010101u;
@@ -802,6 +814,24 @@ __device__ __forceinline__ void place_chunk(const uint32_t *cw, int nw, uint64_t
     const int ng = tmax(0, tmin(SW / 4, nw / 4 - tid * (SW / 4)));
     uint32_t le = 0, lg = 0;        // byte-lane sums (<= 32 per lane)
     uint32_t emask = 0, gmask = 0;  // bit q: word q of the strip holds a tie / a hit
+    // with c* >= 2 only groups holding a count >= 2 can hold ties or hits
+    const uint32_t gsel = cstar >= 2u ? gmask2 : 0xffu;
+    if (gsel != 0xffu) {
+        for (uint32_t gm = gsel; gm != 0u; gm &= gm - 1u) {
+            const int g = __ffs(gm) - 1;
+            if (g >= ng) break;
+            const uint4 v = s4[g];
+            const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t e = __vcmpeq4(xs[k], ceq) & ONE, t = __vcmpgtu4(xs[k], ceq) & ONE;
+                le += e;
+                lg += t;
+                emask |= (e != 0u ? 1u : 0u) << (4 * g + k);
+                gmask |= (t != 0u ? 1u : 0u) << (4 * g + k);
+            }
+        }
+    } else
 #pragma unroll
     for (int u = 0; u < SW / 4; ++u) {
         const int g = (u + tid) & (SW / 4 - 1);
@@ -968,7 +998,8 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(kPlaceThreads, 2)
     sel_place_kernel(const uint32_t *__restrict__ counts, int64_t row_words, int nch, int max_count,
                      int k_filter, const int4 *__restrict__ plan, const uint32_t *__restrict__ bases,
-                     int64_t *__restrict__ cand, int32_t *__restrict__ n_cand) {
+                     const uint32_t *__restrict__ gsum, int64_t *__restrict__ cand,
+                     int32_t *__restrict__ n_cand) {
     constexpr int W_CH = kChunkBytes / 4;
     extern __shared__ __align__(128) uint8_t psm_b[];
     uint32_t *cw = reinterpret_cast<uint32_t *>(psm_b);
@@ -990,8 +1021,11 @@ __global__ void __launch_bounds__(kPlaceThreads, 2)
     }
     const uint32_t *bs = bases + (qs * nch + ch) * static_cast<int64_t>(nb);
     for (int b = tid; b < nb; b += kPlaceThreads) pre[b] = __ldg(bs + b);
+    // this strip's 8 group flags (count >= 2) from the counting pass's summary
+    static_assert(W_CH / 4 / kPlaceThreads == 8, "one summary byte per thread strip");
+    const uint32_t sbits = (__ldg(gsum + (qs * nch + ch) * (W_CH / 128) + tid / 4) >> (8 * (tid & 3))) & 0xffu;
     __syncthreads();
-    place_chunk(cw, nw, bar, ch, qs, max_count, k_filter, above, pre, hl, cand, n_cand, plan + qs);
+    place_chunk(cw, nw, bar, ch, qs, max_count, k_filter, above, pre, hl, cand, n_cand, plan + qs, sbits);
 }
 
 // Fused counting + placement for n_docs <= kMaxFusedChunks * 64K (u8 counters):
@@ -1063,7 +1097,8 @@ static size_t count_ws_chunks(int64_t n_q, int m_q, int P, int64_t k_c, int64_t 
     const int mc = m_q * P, nch = n_chunks_for(n_docs, mc);
     return align256(static_cast<size_t>(k_c) * (nch + 1) * sizeof(int64_t)) +
            2 * align256(static_cast<size_t>(n_q) * nch * (mc + 1) * sizeof(uint32_t)) +
-           align256(static_cast<size_t>(n_q) * sizeof(int4));
+           align256(static_cast<size_t>(n_q) * sizeof(int4)) +
+           align256(static_cast<size_t>(n_q) * nch * (kChunkBytes / 4 / 128) * sizeof(uint32_t));
 }
 static bool small_batch(int64_t n_q) { return n_q * 8 <= sm_count(); }
 // + the small-batch selection buffers (plans, tie bases, hit counts, hits, ties)
@@ -1130,21 +1165,23 @@ static int launch_count_select(const int32_t *probed, int64_t n_q, int m_q, int 
         DSRT_LAUNCH_CHECK();
         return DSRT_OK;
     }
+    const size_t hb = align256(static_cast<size_t>(n_q) * nch * (max_count + 1) * sizeof(uint32_t));
+    uint32_t *bases = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(chist) + hb);
+    int4 *plan = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(bases) + hb);
+    uint32_t *gsum = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(plan) +
+                                                  align256(static_cast<size_t>(n_q) * sizeof(int4)));
     const size_t csmem = kChunkBytes + (max_count + 1) * sizeof(uint32_t);
     auto ck = cb == 8 ? count_chunk_kernel<8> : count_chunk_kernel<16>;
     DSRT_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
     ck<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kCntThreads, csmem, st>>>(
-        probed, m_q * P, bnd, nch, post_docs, row_words, max_count, counts, chist);
+        probed, m_q * P, bnd, nch, post_docs, row_words, max_count, counts, chist, gsum);
     if (cb == 8) {  // sort-free placement (any batch): plan per query set, then place per chunk
-        const size_t hb = align256(static_cast<size_t>(n_q) * nch * (max_count + 1) * sizeof(uint32_t));
-        uint32_t *bases = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(chist) + hb);
-        int4 *plan = reinterpret_cast<int4 *>(reinterpret_cast<uint8_t *>(bases) + hb);
         sel_plan8_kernel<<<static_cast<unsigned>(n_q), 256, (max_count + 1) * sizeof(uint32_t), st>>>(
             chist, nch, max_count, k_filter, plan, bases);
         const size_t psmem = place_smem(max_count, k_filter);
         DSRT_CUDA(cudaFuncSetAttribute(sel_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
         sel_place_kernel<<<dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n_q)), kPlaceThreads, psmem, st>>>(
-            counts, row_words, nch, max_count, k_filter, plan, bases, cand, n_cand);
+            counts, row_words, nch, max_count, k_filter, plan, bases, gsum, cand, n_cand);
         DSRT_LAUNCH_CHECK();
         return DSRT_OK;
     }
