@@ -216,6 +216,10 @@ __device__ __forceinline__ void count_postings(uint32_t *sc, const int32_t *__re
                 len = static_cast<int>(bc[1] - a);
             }
         }
+        // pull the row's posting sub-range toward L2 now; the flattened loads below
+        // then mostly hit L2 instead of waiting on HBM batch after batch
+        for (int64_t ln = (a * 8) & ~int64_t(127); ln < (a + len) * 8; ln += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char *>(post_docs) + ln));
         int incl = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
