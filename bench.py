@@ -689,8 +689,8 @@ def run_cfg3(args):
                      "peak_source": "measured in-run: LOP3 lane-ops/s x 4"},
         "clocks": clk, "int_microbench": mb,
         # plane permute, hash, f16 rows, screen, theta, chunk candidates, re-rank, fallback,
-        # count, place, score, top-k
-        "gpu_launches": 12 * args.steps,
+        # count, placement plan, place, score, top-k
+        "gpu_launches": 13 * args.steps,
     }
     print(json.dumps(line))
     return 0
