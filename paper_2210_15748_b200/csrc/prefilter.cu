@@ -1634,6 +1634,7 @@ __global__ void __launch_bounds__(256)
         const int slot = base + __popc(okm & ((1u << lane) - 1u));
         if (ok && slot < kCandMax) lists[rr * kCandMax + slot] = ScreenCand{acc, static_cast<int32_t>(cid)};
     };
+    __shared__ uint32_t mq[8][16];  // per warp: the match ballots of the 8 chunks x 2 halves
     for (int64_t jb = j0; jb < j1; jb += 8) {
         uint32_t v[8];
 #pragma unroll
@@ -1644,14 +1645,24 @@ __global__ void __launch_bounds__(256)
             const bool h0 = __half2float(__ushort_as_half(static_cast<unsigned short>(v[u] & 0xffffu))) >= th;
             const bool h1 = __half2float(__ushort_as_half(static_cast<unsigned short>(v[u] >> 16))) >= th;
             const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
-            unsigned m = m0 | m1;
+            if (lane == 0) {
+                mq[warp][2 * u] = m0;
+                mq[warp][2 * u + 1] = m1;
+            }
+        }
+        __syncwarp();
+        // one rolled loop over the matches keeps a single copy of process() (the
+        // unrolled form thrashed the instruction cache)
+#pragma unroll 1
+        for (int k = 0; k < 16; ++k) {
+            unsigned m = mq[warp][k];
             while (m != 0u) {
                 const int l = __ffs(m) - 1;
                 m &= m - 1u;
-                if ((m0 >> l) & 1u) process(l, jb + u, 0);
-                if ((m1 >> l) & 1u) process(l, jb + u, 1);
+                process(l, jb + (k >> 1), k & 1);
             }
         }
+        __syncwarp();
     }
 }
 
