@@ -612,7 +612,7 @@ def run_cfg3(args):
             kev["prefilter"].append((e[0], e[1]))
             kev["score"].append((e[1], e[2]))
         last["cand"], last["n_cand"] = cand, n_cand
-        return engine.topk(scores, top_k, ids=idx.doc_ids_dev[cand.clamp(min=0)], n_valid=n_cand)
+        return engine.topk(scores, top_k, ids=idx.doc_ids_dev, n_valid=n_cand, id_index=cand)
 
     # per-stage kernel times from eager steps with events between the stages
     for _ in range(3):

@@ -164,6 +164,15 @@ int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, int64_t ids
               const int32_t *n_valid, int64_t n, int64_t n_rows, int k, double *out_scores,
               uint64_t *out_ids, int64_t *out_pos, void *stream);
 int dsrt_topk_max_k(void);
+/*
+ * dsrt_topk for candidate lists: the id of element i of row r is
+ * ids[id_index[r * id_index_ld + i]] (doc ids of the candidate set indices),
+ * read in the kernel instead of a separate gather.  Elements i < n_valid[r]
+ * must hold valid indices.
+ */
+int dsrt_topk_indexed(const double *scores, int64_t ld, const uint64_t *ids, const int64_t *id_index,
+                      int64_t id_index_ld, const int32_t *n_valid, int64_t n, int64_t n_rows, int k,
+                      double *out_scores, uint64_t *out_ids, int64_t *out_pos, void *stream);
 
 /*
  * K5 -- replaces prefilter.filter_candidates (prefilter.py:111-144).

@@ -20,10 +20,13 @@ struct RowView {
     const double *s;
     const uint64_t *ids;
     int64_t row, ids_ld;
+    const int64_t *ix = nullptr;  // optional per-row index into ids (candidate lists)
+    int64_t ix_ld = 0;
     __device__ __forceinline__ uint64_t key(int64_t i) const {
         return static_cast<uint64_t>(__double_as_longlong(__ldg(s + i)));
     }
     __device__ __forceinline__ uint64_t id(int64_t i) const {
+        if (ix != nullptr) return __ldg(ids + __ldg(ix + row * ix_ld + i));
         if (ids == nullptr) return static_cast<uint64_t>(i);
         return ids_ld ? __ldg(ids + row * ids_ld + i) : __ldg(ids + i);
     }
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(kTopkThreads)
     topk_kernel(const double *__restrict__ scores, int64_t ld, const uint64_t *__restrict__ ids,
                 int64_t ids_ld, const int32_t *__restrict__ n_valid, int64_t n, int k,
                 double *__restrict__ out_s, uint64_t *__restrict__ out_id,
-                int64_t *__restrict__ out_pos) {
+                int64_t *__restrict__ out_pos, const int64_t *__restrict__ ix, int64_t ix_ld) {
     extern __shared__ __align__(16) uint8_t smem[];
     int cap = 1;  // winner buffer: pow2 >= k (at most k winners are collected)
     while (cap < k) cap <<= 1;
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kTopkThreads)
     __shared__ int cnt;
 
     const int64_t row = blockIdx.x;
-    RowView rv{scores + row * ld, ids, row, ids_ld};
+    RowView rv{scores + row * ld, ids, row, ids_ld, ix, ix_ld};
     int64_t nr = n;
     if (n_valid) nr = tmin<int64_t>(n, tmax<int64_t>(0, __ldg(n_valid + row)));
     const int64_t kk = tmin<int64_t>(k, nr);
@@ -268,9 +271,9 @@ using namespace dsrt;
 
 extern "C" int dsrt_topk_max_k(void) { return kTopkMax; }
 
-extern "C" int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, int64_t ids_ld,
-                         const int32_t *n_valid, int64_t n, int64_t n_rows, int k,
-                         double *out_scores, uint64_t *out_ids, int64_t *out_pos, void *stream) {
+static int topk_launch(const double *scores, int64_t ld, const uint64_t *ids, int64_t ids_ld,
+                       const int64_t *ix, int64_t ix_ld, const int32_t *n_valid, int64_t n, int64_t n_rows,
+                       int k, double *out_scores, uint64_t *out_ids, int64_t *out_pos, void *stream) {
     DSRT_REQUIRE(k >= 1, DSRT_EINVAL, "invalid parameter: top_k must be >= 1, got %d", k);
     DSRT_REQUIRE(k <= kTopkMax, DSRT_EUNSUPPORTED,
                  "invalid parameter: top_k=%d exceeds the device top-k limit %d", k, kTopkMax);
@@ -287,7 +290,24 @@ extern "C" int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, 
     // batch keeps 1024 threads per row (latency)
     const int threads = (n <= 8192 && n_rows >= sm_count()) ? 256 : kTopkThreads;
     topk_kernel<<<static_cast<unsigned>(n_rows), threads, smem, as_stream(stream)>>>(
-        scores, ld, ids, ids_ld, n_valid, n, k, out_scores, out_ids, out_pos);
+        scores, ld, ids, ids_ld, n_valid, n, k, out_scores, out_ids, out_pos, ix, ix_ld);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
+}
+
+extern "C" int dsrt_topk(const double *scores, int64_t ld, const uint64_t *ids, int64_t ids_ld,
+                         const int32_t *n_valid, int64_t n, int64_t n_rows, int k,
+                         double *out_scores, uint64_t *out_ids, int64_t *out_pos, void *stream) {
+    return topk_launch(scores, ld, ids, ids_ld, nullptr, 0, n_valid, n, n_rows, k, out_scores, out_ids,
+                       out_pos, stream);
+}
+
+extern "C" int dsrt_topk_indexed(const double *scores, int64_t ld, const uint64_t *ids,
+                                 const int64_t *id_index, int64_t id_index_ld, const int32_t *n_valid,
+                                 int64_t n, int64_t n_rows, int k, double *out_scores, uint64_t *out_ids,
+                                 int64_t *out_pos, void *stream) {
+    DSRT_REQUIRE(ids != nullptr && id_index != nullptr, DSRT_EINVAL,
+                 "invalid parameter: dsrt_topk_indexed needs ids and id_index");
+    return topk_launch(scores, ld, ids, 0, id_index, id_index_ld, n_valid, n, n_rows, k, out_scores, out_ids,
+                       out_pos, stream);
 }

@@ -221,11 +221,14 @@ def collision_counts(offsets, ids, L: int, r: int, m: int, qcodes, out):
 
 
 # ------------------------------------------------------------------- K4
-def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None):
+def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=None, n=None,
+         id_index: torch.Tensor | None = None):
     """Row-wise top-k by (score desc, id asc); ids shared (1-D) or per row (2-D).
 
     ``scores`` may be a row-strided view (unit column stride), e.g. the first
-    columns of a wider score buffer; the kernel reads rows at stride ld."""
+    columns of a wider score buffer; the kernel reads rows at stride ld.
+    ``id_index`` (rows, n) int64: element i of row r has id ids[id_index[r, i]]
+    (candidate lists; 1-D ids), read in the kernel."""
     if not scores.is_cuda or scores.dtype != torch.float64:
         raise ValueError("invalid parameter: scores must be a float64 CUDA tensor")
     if scores.dim() != 2 or (scores.shape[1] > 1 and scores.stride(1) != 1):
@@ -244,6 +247,13 @@ def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=
     out_s = torch.empty((rows, k), dtype=torch.float64, device=scores.device)
     out_i = torch.empty((rows, k), dtype=torch.int64, device=scores.device)
     out_p = torch.empty((rows, k), dtype=torch.int64, device=scores.device)
+    if id_index is not None:
+        _need(id_index, torch.int64, "id_index")
+        if ids is None or ids.dim() != 1 or id_index.dim() != 2 or id_index.shape[0] != rows:
+            raise ValueError("invalid parameter: id_index needs 1-D ids and one index row per score row")
+        _lib.call("dsrt_topk_indexed", _ptr(scores), ld, _ptr(ids), _ptr(id_index), id_index.stride(0),
+                  _ptr(n_valid), n, rows, k, _ptr(out_s), _ptr(out_i), _ptr(out_p), _stream())
+        return out_s, out_i, out_p
     _lib.call("dsrt_topk", _ptr(scores), ld, _ptr(ids), ids_ld, _ptr(n_valid), n, rows, k,
               _ptr(out_s), _ptr(out_i), _ptr(out_p), _stream())
     return out_s, out_i, out_p

@@ -296,12 +296,17 @@ def add_sets(index: DessertIndex, docs) -> DessertIndex:
 
 
 # --------------------------------------------------------------------- query
-def _rank(scores: torch.Tensor, top_k: int, ids: torch.Tensor, n_valid=None):
-    """Row-wise (score desc, doc_id asc) top-k on the device."""
+def _rank(scores: torch.Tensor, top_k: int, ids: torch.Tensor, n_valid=None, cand=None):
+    """Row-wise (score desc, doc_id asc) top-k on the device.  With ``cand`` (candidate
+    set indices per row), element i of row r has doc id ids[cand[r, i]]."""
     rows, n = scores.shape
     k = min(top_k, n)
     if k <= engine.topk_max_k():
+        if cand is not None:  # ids gathered inside the kernel
+            return engine.topk(scores, k, ids=ids, n_valid=n_valid, id_index=cand.contiguous())
         return engine.topk(scores, k, ids=ids, n_valid=n_valid)
+    if cand is not None:
+        ids = ids[cand.clamp(min=0)]
     # k beyond the single-CTA selector: stable two-key sort on the device
     ids2 = ids if ids.dim() == 2 else ids.expand(rows, n)
     valid = torch.ones_like(scores, dtype=torch.bool)
@@ -378,8 +383,7 @@ def _rank_records_plan(index: DessertIndex, qrecs, m_q: int, top_k: int, plan: S
     N = index.n_docs
     if cand is not None:
         scores = _score_plan_sets(index, qrecs, m_q, plan, cand=cand, n_cand=n_cand)
-        ids = index.doc_ids_dev[cand.clamp(min=0)]
-        out_s, out_i, _ = _rank(scores, top_k, ids, n_valid=n_cand)
+        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev, n_valid=n_cand, cand=cand)
         return out_s, out_i
     chunk = max(1, min(N, SCORE_BUFFER_BYTES // (8 * n_q)))
     if chunk >= N:
@@ -414,8 +418,7 @@ def rank_records(index: DessertIndex, qrecs: torch.Tensor, m_q: int, top_k: int,
     if cand is not None:
         scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, m_q, L, C,
                                             index.lut_dev, cand=cand, n_cand=n_cand)
-        ids = index.doc_ids_dev[cand.clamp(min=0)]
-        out_s, out_i, _ = _rank(scores, top_k, ids, n_valid=n_cand)
+        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev, n_valid=n_cand, cand=cand)
         return out_s, out_i
     if n_q < 8:
         scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, m_q, L, C,
