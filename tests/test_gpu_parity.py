@@ -242,6 +242,26 @@ def test_topk_n_valid_and_per_row_ids():
         assert np.all(out_s[r, kk:].cpu().numpy() == -1.0)
 
 
+@pytest.mark.parametrize("n", [300, 5000])
+def test_topk_indexed_matches_gathered_ids(n):
+    """dsrt_topk_indexed (doc ids read through a candidate index in the kernel) equals the
+    gathered-ids top-k and the oracle ranking; many score ties so the id tie-break decides."""
+    rng = np.random.default_rng(19)
+    rows, k = 6, 50
+    S = np.round(rng.random((rows, n)), 2)                     # heavy ties
+    doc_ids = rng.permutation(1 << 20)[:7000].astype(np.int64)
+    cand = np.stack([rng.permutation(7000)[:n] for _ in range(rows)]).astype(np.int64)
+    nv = np.array([0, 1, n // 2, n, n - 3, 7], dtype=np.int32)
+    St, Ct = torch.from_numpy(S).to(DEV), torch.from_numpy(cand).to(DEV)
+    Dt, Nt = torch.from_numpy(doc_ids).to(DEV), torch.from_numpy(nv).to(DEV)
+    a_s, a_i, a_p = engine.topk(St, k, ids=Dt, n_valid=Nt, id_index=Ct)
+    b_s, b_i, b_p = engine.topk(St, k, ids=Dt[Ct], n_valid=Nt)
+    assert torch.equal(a_s, b_s) and torch.equal(a_i, b_i) and torch.equal(a_p, b_p)
+    for r in range(rows):
+        want = O.rank_topk(S[r, : nv[r]], doc_ids[cand[r, : nv[r]]], k)
+        assert list(a_i[r, : len(want)].cpu().numpy()) == [w[0] for w in want]
+
+
 # ----------------------------------------------------------------- prefilter
 @pytest.mark.parametrize("gemm2", ["0", "1"])  # chunk-max candidates / second screen GEMM
 def test_prefilter_golden(golden_prefilter, gemm2, monkeypatch):
