@@ -1418,11 +1418,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
             int &nsub = nsubs[r];
             const float th = (PASS != 0 && row_ok) ? theta[row] : INFINITY;
             const uint32_t base = tmem + (acc * RT + r) * kSN + (static_cast<uint32_t>(quarter * 32) << 16);
-#pragma unroll 1
-            for (int c0 = half * (kSN / kSHalves); c0 < (half + 1) * (kSN / kSHalves); c0 += 32) {
-                uint32_t r[32];
-                tmem_ld32(base + c0, r);
-                tmem_wait_ld();
+            // one 32-column chunk of accumulators (values r) starting at column c0
+            auto chunk = [&](uint32_t (&r)[32], const int c0) {
                 if (!full_tile) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
@@ -1488,6 +1485,24 @@ __global__ void __launch_bounds__(kSThreads, 1)
                             }
                         }
                     }
+                }
+                        };
+            if constexpr (PASS == 0) {  // both chunks of this half in flight before one wait
+                uint32_t va[32], vb[32];
+                const int c0a = half * (kSN / kSHalves);
+                static_assert(kSN / kSHalves == 64, "two 32-column chunks per half");
+                tmem_ld32(base + c0a, va);
+                tmem_ld32(base + c0a + 32, vb);
+                tmem_wait_ld();
+                chunk(va, c0a);
+                chunk(vb, c0a + 32);
+            } else {
+#pragma unroll 1
+                for (int c0 = half * (kSN / kSHalves); c0 < (half + 1) * (kSN / kSHalves); c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(base + c0, v);
+                    tmem_wait_ld();
+                    chunk(v, c0);
                 }
             }
             }  // r
