@@ -465,13 +465,20 @@ constexpr int kPieceBytes = DSRT_PIECE_BYTES;  // per-warp staging piece
 constexpr int kBufs = DSRT_CAND_BUFS;          // per-warp ring depth
 constexpr int kCandWarps = 8;
 
-template <int K, int W>
+// Candidate-mode pieces: 4 KB when one query vector per lane (the smallest slot
+// rows) still fits 2 CTAs per SM -- fewer, larger pieces cut the per-piece ring
+// bookkeeping (cfg3 scoring 1.595 -> 1.567 ms); 3 KB otherwise.
+template <int QPL>
+constexpr int cand_piece_bytes() {
+    return QPL == 1 ? (kPieceBytes > 4096 ? kPieceBytes : 4096) : kPieceBytes;
+}
+template <int K, int W, int PB = kPieceBytes>
 constexpr int piece_vec() {
-    return kPieceBytes / ((((K * W) + 3) & ~3) * 4);
+    return PB / ((((K * W) + 3) & ~3) * 4);
 }
 template <int QPL>
 constexpr size_t cand_smem_static() {
-    return kCandWarps * (kBufs * kPieceBytes + kBufs * sizeof(uint64_t) + SlotGeom<QPL>::kBytes);
+    return kCandWarps * (kBufs * cand_piece_bytes<QPL>() + kBufs * sizeof(uint64_t) + SlotGeom<QPL>::kBytes);
 }
 
 // Candidate metadata through a lane window: lane l holds (vbeg, vend) of
@@ -519,11 +526,12 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
                       uint16_t *__restrict__ maxcounts, int mc_stride, int mc_q0, int64_t run_len,
                       int64_t runs_per_q) {
     constexpr int R = ((K * W) + 3) & ~3;
-    constexpr int PV = piece_vec<K, W>();
+    constexpr int PB = cand_piece_bytes<QPL>();
+    constexpr int PV = piece_vec<K, W, PB>();
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *bufs = reinterpret_cast<uint32_t *>(smem) + warp * (kBufs * PV * R);
-    uint8_t *after_bufs = smem + kCandWarps * kBufs * kPieceBytes;
+    uint32_t *bufs = reinterpret_cast<uint32_t *>(smem) + warp * (kBufs * PB / 4);
+    uint8_t *after_bufs = smem + kCandWarps * kBufs * PB;
     uint64_t *bars = reinterpret_cast<uint64_t *>(after_bufs) + warp * kBufs;
     uint8_t *slot_mem = after_bufs + kCandWarps * kBufs * sizeof(uint64_t);
     double *lut_s = reinterpret_cast<double *>(slot_mem + kCandWarps * SlotGeom<QPL>::kBytes);
