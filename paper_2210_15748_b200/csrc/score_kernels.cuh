@@ -515,6 +515,9 @@ struct CandWin {
 #ifndef DSRT_CAND_MINB
 #define DSRT_CAND_MINB 2
 #endif
+#ifndef DSRT_CAND_WAVES
+#define DSRT_CAND_WAVES 4  // candidate-mode grid: waves of warps (sets the run length)
+#endif
 template <int K, int W, int QPL, bool SPLIT = false>
 __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     score_cand_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
@@ -697,7 +700,7 @@ static int launch_cand(const uint32_t *recs, const int64_t *set_off, int64_t n_s
     DSRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCandWarps * 32, smem));
     occ = occ < 1 ? 1 : occ;
     // enough warps for ~4 waves, but runs of >= 4 candidates
-    const int64_t want_warps = 4LL * sm_count() * occ * kCandWarps;
+    const int64_t want_warps = static_cast<int64_t>(DSRT_CAND_WAVES) * sm_count() * occ * kCandWarps;
     int64_t runs = (want_warps + n_qsets - 1) / n_qsets;
     runs = tmax<int64_t>(1, tmin<int64_t>(runs, (cand_ld + 3) / 4));
     const int64_t run_len = (cand_ld + runs - 1) / runs;
