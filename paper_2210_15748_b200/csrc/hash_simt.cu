@@ -178,10 +178,35 @@ __global__ void __launch_bounds__(kHRows)
     }
 }
 
+// Small-batch pack: one thread per (row, output item) -- item i < max(L, R) is
+// code i (if i < L) and record word i (if i < R) -- instead of a thread per row
+// walking all L * C bits through a local-memory record (the batch-1 latency path).
 __global__ void hash_pack_kernel(const uint32_t *__restrict__ bits, int bw, int64_t n, int L, int C,
                                  void *codes_out, uint32_t *recs_out) {
-    const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (row < n) pack_row(bits + row * bw, L, C, row, codes_out, recs_out);
+    const int W = plane_words(L), R = record_words(L, C);
+    const int items = L > R ? L : R;
+    const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t row = g / items;
+    const int i = static_cast<int>(g - row * items);
+    if (row >= n) return;
+    const uint32_t *b = bits + row * bw;
+    auto bit = [&](int p) { return (__ldg(b + (p >> 5)) >> (p & 31)) & 1u; };
+    if (codes_out != nullptr && i < L) {
+        uint32_t code = 0;
+        for (int c = 0; c < C; ++c) code |= bit(i * C + c) << c;
+        const int code_bytes = C <= 8 ? 1 : (C <= 16 ? 2 : 4);
+        if (code_bytes == 1) static_cast<uint8_t *>(codes_out)[row * L + i] = static_cast<uint8_t>(code);
+        else if (code_bytes == 2) static_cast<uint16_t *>(codes_out)[row * L + i] = static_cast<uint16_t>(code);
+        else static_cast<uint32_t *>(codes_out)[row * L + i] = code;
+    }
+    if (recs_out != nullptr && i < R) {  // word i = plane bit (i / W) of tables 32 (i % W) ..
+        uint32_t word = 0;
+        if (i < C * W) {
+            const int pb = i / W, t0 = 32 * (i % W);
+            for (int j = 0; j < 32 && t0 + j < L; ++j) word |= bit((t0 + j) * C + pb) << j;
+        }
+        recs_out[row * R + i] = word;
+    }
 }
 
 template <typename TX, typename A>
@@ -194,8 +219,9 @@ static int launch_hash(const void *X, int64_t n, int d, const void *planes, int 
         DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&bits), static_cast<size_t>(n) * bw * 4, st));
         hash_simt_chunk_kernel<TX, A><<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(bw)), kHRows, 0, st>>>(
             static_cast<const TX *>(X), n, d, static_cast<const A *>(planes), L * C, bits, bw, zero_rows);
-        hash_pack_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(bits, bw, n, L, C, codes,
-                                                                               recs);
+        const int64_t items = n * static_cast<int64_t>(tmax(L, record_words(L, C)));
+        hash_pack_kernel<<<static_cast<unsigned>((items + 127) / 128), 128, 0, st>>>(bits, bw, n, L, C, codes,
+                                                                                   recs);
         cudaFreeAsync(bits, st);
         DSRT_LAUNCH_CHECK();
         return DSRT_OK;
