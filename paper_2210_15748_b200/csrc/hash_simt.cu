@@ -131,20 +131,23 @@ __global__ void __launch_bounds__(kHRows)
 // becomes a grid dimension; each CTA writes one sign word per row (same
 // per-(row, plane) sequential FMA as above, so bits are identical) and a
 // per-row pass packs the words into codes and records.
-template <typename TX, typename A>
+template <typename TX, typename A, int NPL>
 __global__ void __launch_bounds__(kHRows)
     hash_simt_chunk_kernel(const TX *__restrict__ X, int64_t n, int d, const A *__restrict__ planes, int P,
                            uint32_t *__restrict__ bits, int bw, uint32_t *zero_rows) {
+    // NPL planes per CTA: 32 (one sign word per row) or 8 (one sign byte; tiny
+    // batches, where 32-plane CTAs leave most SMs idle)
+    static_assert(NPL == 32 || NPL == 8, "sign word or byte");
     __shared__ A xs[kHDim][kHRows + 1];
-    __shared__ __align__(16) A ps[kHDim][kHPlanes];
+    __shared__ __align__(16) A ps[kHDim][NPL];
     const int tid = threadIdx.x;
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kHRows;
     const int64_t row = row0 + tid;
-    const int p0 = blockIdx.y * kHPlanes;
+    const int p0 = blockIdx.y * NPL;
     bool nonzero = false;
-    A acc[kHPlanes];
+    A acc[NPL];
 #pragma unroll
-    for (int j = 0; j < kHPlanes; ++j) acc[j] = A(0);
+    for (int j = 0; j < NPL; ++j) acc[j] = A(0);
     for (int k0 = 0; k0 < d; k0 += kHDim) {
         __syncthreads();
         for (int i = tid; i < kHRows * kHDim; i += kHRows) {
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kHRows)
             if (gr < n && k0 + kk < d) v = to_acc<TX, A>(X[gr * d + k0 + kk]);
             xs[kk][r] = v;
         }
-        for (int i = tid; i < kHPlanes * kHDim; i += kHRows) {
+        for (int i = tid; i < NPL * kHDim; i += kHRows) {
             const int pp = i / kHDim, kk = i % kHDim;
             A v = A(0);
             if (p0 + pp < P && k0 + kk < d) v = planes[static_cast<int64_t>(p0 + pp) * d + k0 + kk];
@@ -166,14 +169,15 @@ __global__ void __launch_bounds__(kHRows)
             const A xv = xs[kk][tid];
             nonzero |= (xv != A(0));
 #pragma unroll
-            for (int j = 0; j < kHPlanes; ++j) acc[j] = fma(xv, ps[kk][j], acc[j]);
+            for (int j = 0; j < NPL; ++j) acc[j] = fma(xv, ps[kk][j], acc[j]);
         }
     }
     uint32_t word = 0;
 #pragma unroll
-    for (int j = 0; j < kHPlanes; ++j) word |= (acc[j] > A(0) ? 1u : 0u) << j;
+    for (int j = 0; j < NPL; ++j) word |= (acc[j] > A(0) ? 1u : 0u) << j;
     if (row < n) {
-        bits[row * bw + blockIdx.y] = word;
+        if (NPL == 32) bits[row * bw + blockIdx.y] = word;
+        else reinterpret_cast<uint8_t *>(bits + row * bw)[blockIdx.y] = static_cast<uint8_t>(word);
         if (blockIdx.y == 0 && !nonzero && zero_rows) atomicAdd(zero_rows, 1u);
     }
 }
@@ -217,8 +221,16 @@ static int launch_hash(const void *X, int64_t n, int d, const void *planes, int 
         const int bw = (L * C + 31) / 32;
         uint32_t *bits = nullptr;
         DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&bits), static_cast<size_t>(n) * bw * 4, st));
-        hash_simt_chunk_kernel<TX, A><<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(bw)), kHRows, 0, st>>>(
-            static_cast<const TX *>(X), n, d, static_cast<const A *>(planes), L * C, bits, bw, zero_rows);
+        if (blocks * bw * 4 <= sm_count()) {  // tiny batch: 8-plane CTAs (sign bytes)
+            // (bytes past the last plane stay unwritten: the pack reads only plane bits)
+            hash_simt_chunk_kernel<TX, A, 8><<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>((L * C + 7) / 8)),
+                                               kHRows, 0, st>>>(
+                static_cast<const TX *>(X), n, d, static_cast<const A *>(planes), L * C, bits, bw, zero_rows);
+        } else {
+            hash_simt_chunk_kernel<TX, A, 32><<<dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(bw)), kHRows, 0,
+                                                st>>>(
+                static_cast<const TX *>(X), n, d, static_cast<const A *>(planes), L * C, bits, bw, zero_rows);
+        }
         const int64_t items = n * static_cast<int64_t>(tmax(L, record_words(L, C)));
         hash_pack_kernel<<<static_cast<unsigned>((items + 127) / 128), 128, 0, st>>>(bits, bw, n, L, C, codes,
                                                                                    recs);
