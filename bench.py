@@ -1,19 +1,31 @@
-"""Benchmark of the DESSERT scoring hot path on B200 (driver contract: one JSON line).
+"""Benchmark of the DESSERT vector-set search hot path on B200 (driver contract: one JSON line).
 
-Workload (BASELINE.json configs[1], "cfg1"): N = 100,000 sets, m_i =
-clip(round(N(70, 20)), 8, 180) (~7.0 M vectors), d = 128 fp16 unit vectors
-from a 4,096-centroid Gaussian mixture, L = 64 tables x C = 7 bits; 1,000
-query sets of m_q = 32; exhaustive scoring of every set; top-100.
-A step = hash the 32,000 query vectors (K1) + score every (query set, set)
-pair (K3) + top-100 per query set (K4), inputs resident in HBM.
-The index (7.0 M x 64 B plane records = 448 MB) exceeds the 126 MB L2, so no
-L2 flush is needed between steps.
+Default workload (BASELINE.json configs[4], "cfg4" -- the largest single-GPU
+config, on which the north star's 8M-set target is quoted): N = 8,000,000 sets,
+m_i = clip(round(N(70, 25)), 8, 180) (~560 M vectors), codes only in HBM
+(L = 32 tables x C = 8 bits = 32 B per vector, 17.9 GB of plane records),
+generated on the GPU by hashing unit mixture vectors over 262,144 centroids;
+1,024 query sets of m_q = 32 fp16 vectors; exhaustive scoring of every set;
+top-1,000 per query set.
+A step = hash the 32,768 query vectors (K1, tcgen05) + score every (query
+set, set) pair and keep the top-1,000 (dsrt_search_all: K3 with the
+threshold-append epilogue + K4 merges; no score matrix in HBM), inputs
+resident in HBM.  17.9 GB of records >> 126 MB L2: no flush needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 1|3|4]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 1|2|3|4]
 
-Multi-GPU (torchrun): weak scaling -- every rank holds its own 100k-set shard
-(seeded per rank), all ranks score the same query sets, local top-k are
-all-gathered over NCCL and merged with the same (score desc, doc id asc) key.
+--config 1 / 2 / 3 run the other BASELINE configs (cfg1 exhaustive 100k sets,
+cfg2 index build, cfg3 prefilter pipeline); their lines are kept in profiles/.
+
+Multi-GPU (torchrun, --config 4): ONE index sharded by shard_bounds (contiguous
+set ranges, equal vector counts; strong scaling), every rank scores its shard,
+local top-k all-gathered over NCCL and merged on the device with the same
+(score desc, doc id asc) key; rank 0 checks the merged top-k of 8 query sets
+against the unsharded index.
+
+--impl reference: the unmodified reference package (baseline/_ref) through its
+public build_index / query API on the host cores (bench_reference.py), on a
+bounded sample of the same workload; rank 0 only.
 """
 
 from __future__ import annotations
@@ -30,30 +42,48 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-METRIC = "set-pair scores/sec (cfg1: 100k sets x 1000 query sets, L=64 C=7, exhaustive, top-100)"
 UNIT = "set-pairs/s"
+SPECS = {
+    # workload -> (metric, L, C, size_sd, n_centroids, top_k, n_qsets, n_sets)
+    4: ("set-pair scores/sec (cfg4: 8M sets x 1024 query sets, L=32 C=8, exhaustive, top-1000)",
+        32, 8, 25.0, 262_144, 1000, 1024, 8_000_000),
+    1: ("set-pair scores/sec (cfg1: 100k sets x 1000 query sets, L=64 C=7, exhaustive, top-100)",
+        64, 7, 20.0, 4096, 100, 1000, 100_000),
+}
 
-
-
-def _ncu_traffic(config: str, scale: float = 1.0):
-    """Per-launch DRAM bytes (read + write) of the dominant kernel from the committed
-    `ncu --set full` capture (profiles/r01_ncu_traffic.json), scaled to this launch."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_traffic.json")
-    try:
-        with open(path) as f:
-            rec = json.load(f)[config]
-    except (OSError, KeyError, ValueError):
-        return None, None
-    return rec["traffic_bytes"] * scale, {"source": "profiles/r01_ncu_traffic.json (" + rec["source"] + ")",
-                                          "captured_launch": rec["launch"],
-                                          "dram_read_bytes": rec["dram_read_bytes"] * scale,
-                                          "dram_write_bytes": rec["dram_write_bytes"] * scale}
 
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p, "MEASURED_PEAKS.json"
+    except (OSError, ValueError):
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}, "B200_PROFILING.md fallback"
+
+
+def _ncu_traffic(config: str, scale: float = 1.0):
+    """Per-launch DRAM bytes (read + write) of the dominant kernel from the committed
+    `ncu --set full` capture (profiles/r02_ncu_traffic.json, else r01), scaled to a launch."""
+    for name in ("r02_ncu_traffic.json", "r01_ncu_traffic.json"):
+        path = os.path.join(REPO, "profiles", name)
+        try:
+            with open(path) as f:
+                rec = json.load(f)[config]
+        except (OSError, KeyError, ValueError):
+            continue
+        return rec["traffic_bytes"] * scale, {"source": f"profiles/{name} (" + rec["source"] + ")",
+                                              "captured_launch": rec["launch"],
+                                              "dram_read_bytes": rec["dram_read_bytes"] * scale,
+                                              "dram_write_bytes": rec["dram_write_bytes"] * scale}
+    return None, None
 
 
 # ----------------------------------------------------------------- clocks
@@ -172,154 +202,18 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
-# ------------------------------------------------------------ CPU baseline
-def _port_worker(args):
-    codes, off, qcodes, lut, sets = args
-    from oracle import dessert_oracle as O
-
-    r = 1 << 7 if codes.max() < 128 else 1 << 8
-    L = codes.shape[1]
-    tables = [O.build_tiny_table(codes[off[i]:off[i + 1]], L, r) for i in sets]
-    t0 = time.perf_counter()
-    out = []
-    for qc in qcodes:
-        out.append([O.score_port(t, qc, lut) for t in tables])
-    return time.perf_counter() - t0, len(qcodes) * len(sets)
-
-
-def cpu_port_rate(codes, off, qcodes, lut, n_sets_sample, threads):
-    """Reference algorithm (TinyTable collision keys + numpy mean, index.py:183-216)
-    on a fork pool of `threads` processes, each scoring a contiguous shard."""
-    import multiprocessing as mp
-
-    sets = np.arange(n_sets_sample)
-    shards = np.array_split(sets, threads)
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(threads) as pool:
-        res = pool.map(_port_worker, [(codes, off, qcodes, lut, s) for s in shards])
-    wall = time.perf_counter() - t0
-    pairs = sum(r[1] for r in res)
-    slowest = max(r[0] for r in res)
-    return pairs / slowest, pairs, slowest, wall
-
-
-def host_sample_codes(n_sets, L, C, seed, m_q=32, n_q=2):
-    """cfg1-shaped codes for a bounded sample, generated and hashed on the host
-    (numpy + oracle hash) so the reference arm touches no GPU code."""
-    from oracle import dessert_oracle as O
-    from paper_2210_15748_b200 import workloads
-
-    rng = np.random.default_rng(seed)
-    sizes = workloads.set_sizes(n_sets, 70, 20, seed)
-    off = workloads.offsets(sizes)
-    cents = rng.standard_normal((4096, 128))
-    cents /= np.linalg.norm(cents, axis=1, keepdims=True)
-    X = cents[rng.integers(0, 4096, size=int(off[-1]))] + 0.05 * rng.standard_normal((int(off[-1]), 128))
-    X = (X / np.linalg.norm(X, axis=1, keepdims=True)).astype(np.float16)
-    P = O.sample_planes(128, C, L, 0)
-    codes = O.hash_matrix(P, L, C, X.astype(np.float64))
-    qs = []
-    for _ in range(n_q):
-        s = int(rng.integers(0, n_sets))
-        rows = off[s] + rng.integers(0, sizes[s], size=m_q)
-        q = X[rows].astype(np.float64) + 0.1 * rng.standard_normal((m_q, 128))
-        qs.append(O.hash_matrix(P, L, C, q / np.linalg.norm(q, axis=1, keepdims=True)))
-    return codes, off, np.stack(qs), O.sim_lut(C, L)
-
-
-def run_reference(args):
-    world, rank, _ = _dist()
-    if rank != 0:
-        return 0
-    threads = len(os.sched_getaffinity(0))
-    n_sample = min(100_000, 250 * threads)
-    codes, off, qcodes, lut = host_sample_codes(n_sample, 64, 7, seed=1, n_q=8)
-    vals = []
-    for _ in range(args.warmup):
-        cpu_port_rate(codes, off, qcodes[:1], lut, min(200, n_sample), threads)
-    for _ in range(args.steps):
-        rate, pairs, slowest, wall = cpu_port_rate(codes, off, qcodes, lut, n_sample, threads)
-        vals.append(rate)
-    v = float(np.median(vals))
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * 1e8 / v,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic (cfg1-shaped sample, host-generated)",
-        "config": {"workload": "cfg1", "n_sets": 100_000, "n_qsets": 1000, "m_q": 32, "L": 64,
-                   "C": 7, "top_k": 100, "sample": f"{qcodes.shape[0]} query sets x {n_sample} sets"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{qcodes.shape[0]} query sets x {n_sample} sets per step, "
-                                   "fork pool, reference TinyTable algorithm (oracle port)"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
-    return 0
-
-
-# ------------------------------------------------------------------ GPU arm
-def run_gpu(args):
+# ------------------------------------------------------------------ helpers
+def _timed(step_fn, steps, warmup, local, stream, world=1):
+    """W untimed warm-up steps; then K steps bracketed by barrier + synchronize, timed
+    with CUDA events on the launch stream; max over ranks; clocks sampled meanwhile."""
     import torch
     import torch.distributed as dist
 
-    import paper_2210_15748_b200 as d
-    from paper_2210_15748_b200 import engine, workloads
-
-    world, rank, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    n_sets, n_q, m_q, L, C, top_k = 100_000, 1000, 32, 64, 7, 100
-
-    # ---- setup (untimed): synthetic cfg1 shard, index build on the GPU
-    sizes = workloads.set_sizes(n_sets, 70, 20, seed=100 + rank)
-    off = workloads.offsets(sizes)
-    X, _ = workloads.gpu_mixture(int(off[-1]), 4096, 128, 0.05, seed=200 + rank,
-                                 dtype=torch.float16, device=dev)
-    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
-    doc_ids = np.arange(n_sets, dtype=np.int64) + rank * n_sets
-    idx = d.build_from_vectors(X, sizes, doc_ids, cfg, keep_codes=(rank == 0))
-    Qv = workloads.gpu_queries(X, off, n_q, m_q, seed=300)      # same queries on every rank
-    Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
-    del X
+    if os.environ.get("DSRT_PROFILE_STEPS"):  # ncu --profile-from-start off: capture the steps only
+        torch.cuda.cudart().cudaProfilerStart()
+    for _ in range(warmup):
+        step_fn(False)
     torch.cuda.synchronize()
-
-    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0])
-    planes = idx.family.device_planes(mode, dev)
-    stream = torch.cuda.current_stream()
-    ev = []
-
-    def step(timed_kernel=False):
-        _, qrecs, _ = engine.hash_vectors(Q2, planes, mode, L, C, want_codes=False,
-                                          check_zero=False)
-        if timed_kernel:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        scores, _ = engine.score_all(idx.records, idx.set_off, qrecs, m_q, L, C, idx.lut_dev)
-        if timed_kernel:
-            e1.record(stream)
-            ev.append((e0, e1))
-        out_s, out_i, _ = engine.topk(scores, top_k, ids=idx.doc_ids_dev)
-        if world > 1:
-            gs = [torch.empty_like(out_s) for _ in range(world)]
-            gi = [torch.empty_like(out_i) for _ in range(world)]
-            dist.all_gather(gs, out_s)
-            dist.all_gather(gi, out_i)
-            out_s, out_i, _ = engine.topk(torch.cat(gs, 1).contiguous(), top_k,
-                                          ids=torch.cat(gi, 1).contiguous())
-        return out_s, out_i
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
-    # INT-pipe peak (microbenchmark, measured now on this GPU)
-    mb = engine.microbench_int()
-
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -328,98 +222,242 @@ def run_gpu(args):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for _ in range(args.steps):
-        step(timed_kernel=True)
+    for _ in range(steps):
+        step_fn(True)
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1) / args.steps
+    if os.environ.get("DSRT_PROFILE_STEPS"):
+        torch.cuda.cudart().cudaProfilerStop()
+    ms = t0.elapsed_time(t1) / steps
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device=torch.device("cuda", local))
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-    pairs_per_step = n_q * n_sets * world
+    return ms, clk
+
+
+def hash_flip_rate(family, Q2, L, C, mode):
+    """Product-path query hash bits (K1 in `mode`) vs the float64 oracle hash_matrix
+    (lsh.py:90-106): flips inside / outside the |w.x| < 1e-4 |w||x| band."""
+    import torch
+
+    from oracle import dessert_oracle as O
+    from paper_2210_15748_b200 import engine
+
+    planes = family.device_planes(mode, Q2.device)
+    codes, _, _ = engine.hash_vectors(Q2, planes, mode, L, C, want_records=False, check_zero=False)
+    got = codes.cpu().numpy().astype(np.int64)
+    X = Q2.double().cpu().numpy()
+    want = O.hash_matrix(family.planes, L, C, X)
+    proj = O.projections(family.planes, X)
+    band = np.abs(proj) < 1e-4 * np.linalg.norm(family.planes, axis=1)[None, :] * \
+        np.linalg.norm(X, axis=1)[:, None]
+    bg = ((got[:, :, None] >> np.arange(C)) & 1).reshape(len(X), L * C)
+    bw = ((want[:, :, None] >> np.arange(C)) & 1).reshape(len(X), L * C)
+    flips = bg != bw
+    torch.cuda.synchronize()
+    return {"vectors": int(len(X)), "bits": int(flips.size), "flips": int(flips.sum()),
+            "flips_outside_band": int((flips & ~band).sum()), "band_fraction": float(band.mean()),
+            "rate": float(flips.mean()), "mode": int(mode),
+            "reference": "oracle float64 hash_matrix (lsh.py:90-106), same planes"}
+
+
+def _cpu_scoring_baseline(workload, n_sets, n_qsets_step, steps, warmup):
+    import bench_reference as BR
+
+    _, L, C, sd, n_cent, top_k, _, _ = SPECS[workload]
+    r = BR.scoring_baseline(L=L, C=C, size_sd=sd, n_centroids=n_cent, top_k=top_k, n_sets=n_sets,
+                            n_qsets_step=n_qsets_step, steps=steps, warmup=warmup)
+    api = ("reference dessert.build_index + dessert.query (baseline/_ref, unmodified)"
+           if r["kind"] == "reference" else "oracle port of the reference algorithm")
+    r["sample"] = (f"cfg{workload}-shaped host sample: {n_sets} sets x {n_qsets_step} query sets per "
+                   f"step ({r['pairs_per_step']} set-pairs, median step {r['ms_per_step']:.0f} ms), "
+                   f"top-{top_k}; {api}; {r['cores']}-process fork pool, one set shard per process, "
+                   "shard results merged with the reference key")
+    return r
+
+
+# --------------------------------------------------------- scoring (cfg4/cfg1)
+def run_scoring(args, workload):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2210_15748_b200 as d
+    from paper_2210_15748_b200 import engine, workloads
+    from paper_2210_15748_b200.distributed import merge_topk_device, shard_bounds
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    metric, L, C, sd, n_cent, top_k, n_q, n_sets = SPECS[workload]
+    n_sets = args.sets or n_sets
+    m_q = 32
+    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
+
+    # ---- setup (untimed): synthetic codes generated on the GPU, one index, sharded by rank
+    t_gen = time.perf_counter()
+    if workload == 4:
+        sizes = workloads.set_sizes(n_sets, 70, sd, seed=400)
+        recs, Qv = workloads.gpu_codes_only(sizes, cfg, n_centroids=n_cent, n_qsets=n_q, m_q=m_q,
+                                            seed=401, device=dev)
+    else:
+        sizes = workloads.set_sizes(n_sets, 70, sd, seed=100)
+        off0 = workloads.offsets(sizes)
+        X, _ = workloads.gpu_mixture(int(off0[-1]), n_cent, 128, 0.05, seed=200,
+                                     dtype=torch.float16, device=dev)
+        Qv = workloads.gpu_queries(X, off0, n_q, m_q, seed=300)
+        _, recs = d.lsh.hash_device(d.sample_srp_family(128, C, L, 0), X, want_codes=False)
+        del X
+    off = workloads.offsets(sizes)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    full = None
+    if world > 1:
+        s0, s1 = shard_bounds(sizes, world)[rank]
+        mine = recs[int(off[s0]):int(off[s1])].clone()
+        if rank == 0:  # keep the unsharded index for the merged-result check
+            full = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
+        del recs
+        idx = d.build_from_records(mine, sizes[s0:s1], np.arange(s0, s1), cfg)
+    else:
+        s0, s1 = 0, n_sets
+        idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
+        del recs
+    Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
+    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0])
+    planes = idx.family.device_planes(mode, dev)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    state = {"ovf": 0}
+
+    def step(timed):
+        _, qrecs, _ = engine.hash_vectors(Q2, planes, mode, L, C, want_codes=False, check_zero=False)
+        s, i, ovf = engine.search_all(idx.records, idx.set_off, idx.doc_ids_dev, qrecs, m_q, L, C,
+                                      idx.lut_dev, top_k, mode=0)
+        state["last_ovf"] = ovf
+        if world > 1:
+            gs = [torch.empty_like(s) for _ in range(world)]
+            gi = [torch.empty_like(i) for _ in range(world)]
+            dist.all_gather(gs, s)
+            dist.all_gather(gi, i)
+            s, i = merge_topk_device(torch.cat(gs, 1), torch.cat(gi, 1), top_k)
+        return s, i
+
+    engine.search_profile(False)
+    step(False)  # first call: lazy init outside the measured region
+    torch.cuda.synchronize()
+    engine.search_profile(True)
+    engine.search_profile_read()
+
+    ms, clk = _timed(step, args.steps, max(3, args.warmup), local, stream, world)
+    prof = engine.search_profile_read()  # warm-up + timed steps
+    engine.search_profile(False)
+    n_prof_steps = args.steps + max(3, args.warmup)
+    score_ms = prof["score_ms"] / n_prof_steps
+    other_ms = prof["other_ms"] / n_prof_steps
+    overflow = int(state["last_ovf"].item())
+    pairs_per_step = n_q * n_sets
     value = pairs_per_step / (ms * 1e-3)
 
-    # ---- e2e: public API, host (pinned) query vectors in, host results out
+    # ---- e2e: the public API (query_batch), pinned host query vectors in, host results out
     Qh = Qv.cpu().pin_memory()
-    for _ in range(2):
-        d.query_batch(idx, Qh.to(dev, non_blocking=True), top_k, return_tensors=True)
+    d.query_batch(idx, Qh.to(dev, non_blocking=True), top_k, return_tensors=True)
     torch.cuda.synchronize()
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    if world > 1:
+        dist.barrier()
     te = time.perf_counter()
-    h2d = d2h = 0
     for _ in range(e2e_steps):
-        Qd = Qh.to(dev, non_blocking=True)
-        s_, i_ = d.query_batch(idx, Qd, top_k, return_tensors=True)
+        s_, i_ = d.query_batch(idx, Qh.to(dev, non_blocking=True), top_k, return_tensors=True)
         if world > 1:
             gs = [torch.empty_like(s_) for _ in range(world)]
             gi = [torch.empty_like(i_) for _ in range(world)]
             dist.all_gather(gs, s_)
             dist.all_gather(gi, i_)
-            s_, i_, _ = engine.topk(torch.cat(gs, 1).contiguous(), top_k,
-                                    ids=torch.cat(gi, 1).contiguous())
+            s_, i_ = merge_topk_device(torch.cat(gs, 1), torch.cat(gi, 1), top_k)
         hs, hi = s_.cpu(), i_.cpu()
-        h2d = Qh.numel() * Qh.element_size()
-        d2h = hs.numel() * 8 + hi.numel() * 8
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - te) / e2e_steps
     if world > 1:
         tt = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
+    h2d = Qh.numel() * Qh.element_size()
+    d2h = hs.numel() * 8 + hi.numel() * 8
 
-    # ---- roofline of the dominant kernel (K3 scoring)
-    total_vec = int(off[-1])
-    compares = float(n_q) * m_q * L * total_vec                   # per launch
-    achieved = compares / (kern_ms * 1e-3)
-    p_int = mb["lop3_ops_per_s"] * 4.0                            # 4 byte-compares / lane-op
-    rec_bytes = total_vec * engine.record_words(L, C) * 4
-    traffic, traffic_src = _ncu_traffic("cfg1", n_sets / 100_000 * n_q / 1000)
-    alg_bytes = rec_bytes + n_q * n_sets * 8 + n_q * m_q * engine.record_words(L, C) * 4
+    # ---- multi-GPU: merged top-k of 8 query sets == the unsharded index (rank 0)
+    shard_check = None
+    if world > 1:
+        if rank == 0:
+            q8 = Qv[:8].to(dev)
+            ws_, wi_ = d.query_batch(full, q8, top_k, return_tensors=True)
+            shard_check = {"query_sets": 8, "equal": bool(torch.equal(ws_, hs[:8].to(dev))
+                                                          and torch.equal(wi_, hi[:8].to(dev)))}
+        dist.barrier()
+
+    # ---- roofline of the dominant kernel (K3 scoring launches inside dsrt_search_all)
+    local_vec = int(off[s1] - off[s0])
+    compares = float(n_q) * m_q * L * local_vec                    # per step, this rank
+    achieved = compares / (score_ms * 1e-3)
+    mb = engine.microbench_int()
+    p_int = mb["lop3_ops_per_s"] * 4.0                             # 4 byte-compares / lane-op
+    rec_bytes = local_vec * engine.record_words(L, C) * 4
+    peaks, peaks_src = _peaks()
+    # traffic: ncu capture of the last (largest) scoring launch, scaled to the whole step
+    traffic, traffic_src = _ncu_traffic(f"cfg{workload}", 1.0)
+    code_gbs = rec_bytes / (score_ms * 1e-3) / 1e9
     roofline = {
         "bound": "int", "unit": "Gcompare/s", "achieved": achieved / 1e9, "peak": p_int / 1e9,
         "frac": achieved / p_int, "traffic": traffic,
-        "traffic_detail": dict(traffic_src or {}, algorithmic_bytes=alg_bytes,
-                               ratio=None if traffic is None else traffic / alg_bytes),
-        "kernel": "score_all_kernel<7,2,1,8,2>", "kernel_ms": kern_ms,
+        "traffic_detail": dict(traffic_src or {}, algorithmic_bytes=rec_bytes,
+                               ratio=None if traffic is None else traffic / rec_bytes,
+                               per="one bench step (all scoring launches)"),
+        "kernel": f"score_all_kernel<{C},{(L + 31) // 32},1,8,{4 if L <= 32 else 2}> (threshold-append epilogue)",
+        "kernel_ms": score_ms, "other_search_ms": other_ms,
         "per_launch": {"compares": compares, "code_bytes": rec_bytes,
-                       "hbm_floor_ms": rec_bytes / 6456.2e9 * 1e3},
+                       "hbm_floor_ms": rec_bytes / (peaks.get("hbm_gbs", 6650.0) * 1e9) * 1e3,
+                       "note": "per step: the scoring launches of one dsrt_search_all call"},
+        "achieved_hbm_gbs": code_gbs,
+        "hbm_note": "code bytes of one pass over the index / scoring time; every query-set group "
+                    "re-reads the records, mostly from L2 (dram traffic in traffic_detail)",
         "peak_source": "measured on this GPU in-run: LOP3 lane-ops/s x 4 (dsrt_microbench_int)",
         "int_microbench": mb,
     }
-
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (cfg1-shaped, generated on GPU)",
-        "config": {"workload": "cfg1", "n_sets_per_gpu": n_sets, "n_qsets": n_q, "m_q": m_q,
-                   "L": L, "C": C, "top_k": top_k, "vectors_per_gpu": total_vec,
-                   "l2": "inputs larger than L2 (448 MB plane records), no flush",
-                   "parallelism": f"shard{world}" if world > 1 else "single"},
+        "metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u8",
+        "data": f"synthetic (cfg{workload}-shaped, generated on GPU)",
+        "config": {"workload": f"cfg{workload}", "n_sets": n_sets, "n_qsets": n_q, "m_q": m_q, "L": L,
+                   "C": C, "top_k": top_k, "vectors": int(off[-1]), "vectors_this_rank": local_vec,
+                   "l2": f"inputs larger than L2 ({rec_bytes / 1e9:.1f} GB plane records per rank), no flush",
+                   "parallelism": f"shard{world} (one index, shard_bounds)" if world > 1 else "single",
+                   "generation_s": t_gen},
         "query_sets_per_sec": n_q / (ms * 1e-3),
         "e2e": {"value": pairs_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
-        "gpu_launches": 3 * args.steps + (1 if world > 1 else 0) * args.steps,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+                "path": "query_batch (pinned host fp16 query vectors -> hash -> dsrt_search_all -> "
+                        "host top-k)" + (" + NCCL all-gather + merge" if world > 1 else "")},
+        "gpu_launches": int(round((1 + prof["launches"] / n_prof_steps + (1 if world > 1 else 0))
+                                  * args.steps)),
+        "search": {"score_ms": score_ms, "topk_and_list_ms": other_ms,
+                   "launches_per_step": prof["launches"] / n_prof_steps, "overflow": overflow},
         "roofline": roofline,
         "clocks": clk,
     }
+    if shard_check is not None:
+        line["shard_check"] = shard_check
+    if rank == 0:
+        line["hash_bit_flips"] = hash_flip_rate(idx.family, Q2, L, C, mode)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # bounded sample (~1.5 s per core): 8 query sets x 1000 sets per process
-        threads = len(os.sched_getaffinity(0))
-        n_sample = min(n_sets, 1000 * threads)
-        codes = idx.codes[: int(off[n_sample])].cpu().numpy().astype(np.int64)
-        qcd, _ = d.lsh.hash_device(idx.family, Q2[: 8 * m_q], want_records=False)
-        qc = qcd.cpu().numpy().astype(np.int64).reshape(8, m_q, L)
-        rate, pairs, slowest, wall = cpu_port_rate(codes, off[: n_sample + 1], qc,
-                                                   idx.lookup.table, n_sample, threads)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"8 query sets x {n_sample} sets ({pairs} set-pairs, "
-                                          f"{slowest:.1f} s), reference TinyTable algorithm "
-                                          "(oracle port), fork pool"}
+        r = _cpu_scoring_baseline(workload, args.cpu_sets, 8, 2, 1)
+        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                                "kind": r["kind"], "sample": r["sample"]}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -427,8 +465,33 @@ def run_gpu(args):
     return 0
 
 
+# ------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    workload = args.config if args.config in SPECS else 4
+    metric, L, C, _, _, top_k, n_q, n_sets = SPECS[workload]
+    r = _cpu_scoring_baseline(workload, args.cpu_sets, 8, args.steps, args.warmup)
+    v = r["value"]
+    line = {
+        "impl": "reference", "metric": metric, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": f"synthetic (cfg{workload}-shaped host sample)",
+        "config": {"workload": f"cfg{workload}", "n_sets": n_sets, "n_qsets": n_q, "m_q": 32, "L": L,
+                   "C": C, "top_k": top_k, "sample": f"{r['n_qsets_step']} query sets x {r['n_sets']} sets per step"},
+        "step": {"measured_ms_per_step": r["ms_per_step"], "pairs_per_step": r["pairs_per_step"],
+                 "full_workload_ms_extrapolated": n_q * n_sets / v * 1e3, "setup_s": r["setup_s"]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
 
-# ------------------------------------------------------------- cfg4 / cfg3
+
+# ------------------------------------------------------------- cfg3 / cfg2
 def _clocks_and_time(step_fn, steps, warmup, local, stream):
     import torch
 
@@ -449,108 +512,6 @@ def _clocks_and_time(step_fn, steps, warmup, local, stream):
     if os.environ.get("DSRT_PROFILE_STEPS"):
         torch.cuda.cudart().cudaProfilerStop()
     return t0.elapsed_time(t1) / steps, clocks.stop()
-
-
-def run_cfg4(args):
-    """cfg4: 8M sets (m_i ~ N(70,25) clipped), codes only (L=32, C=8), 1,024 query sets,
-    exhaustive scoring, top-1,000 (chunked score buffer + top-k merge)."""
-    import torch
-
-    import paper_2210_15748_b200 as d
-    from paper_2210_15748_b200 import _lib, engine, workloads
-
-    world, rank, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    n_sets, n_q, m_q, L, C, top_k = args.sets or 8_000_000, 1024, 32, 32, 8, 1000
-    sizes = workloads.set_sizes(n_sets, 70, 25, seed=400)
-    cfg = d.IndexConfig(d=128, C=C, L=L, seed=0, filter=d.FilterConfig(enabled=False))
-    t_gen = time.perf_counter()
-    recs, Qv = workloads.gpu_codes_only(sizes, cfg, n_centroids=262_144, n_qsets=n_q, m_q=m_q,
-                                        seed=401, device=dev)
-    torch.cuda.synchronize()
-    t_gen = time.perf_counter() - t_gen
-    idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
-    Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
-    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0])
-    planes = idx.family.device_planes(mode, dev)
-    stream = torch.cuda.current_stream()
-    chunk = max(1, min(n_sets, args.score_buffer // (8 * n_q)))
-    buf = torch.empty((n_q, chunk), dtype=torch.float64, device=dev)
-    kev = []
-
-    def step(timed):
-        _, qrecs, _ = engine.hash_vectors(Q2, planes, mode, L, C, want_codes=False,
-                                          check_zero=False)
-        ps, pi = [], []
-        for s0 in range(0, n_sets, chunk):
-            s1 = min(n_sets, s0 + chunk)
-            if timed:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            engine.score_all(idx.records, idx.set_off, qrecs, m_q, L, C, idx.lut_dev,
-                             set_begin=s0, set_end=s1, scores=buf, ld=chunk)
-            if timed:
-                e1.record(stream)
-                kev.append((e0, e1, s1 - s0))
-            a, b, _ = engine.topk(buf if s1 - s0 == chunk else buf[:, : s1 - s0].contiguous(),
-                                  top_k, ids=idx.doc_ids_dev[s0:s1])
-            ps.append(a)
-            pi.append(b)
-        return engine.topk(torch.cat(ps, 1).contiguous(), top_k, ids=torch.cat(pi, 1).contiguous())
-
-    ms, clk = _clocks_and_time(step, args.steps, max(3, args.warmup), local, stream)
-    off = idx.set_off
-    total_vec = int(off[-1].item())
-    so = idx.set_off.cpu().numpy()
-    kern = []
-    for e0, e1, w in kev:
-        kern.append((e0.elapsed_time(e1), w))
-    k_ms = float(np.sum([k for k, _ in kern])) / args.steps
-    launches_per_step = len(kern) // args.steps
-    compares = float(n_q) * m_q * L * total_vec
-    mb = engine.microbench_int()
-    p_int = mb["lop3_ops_per_s"] * 4.0
-    achieved = compares / (k_ms * 1e-3)
-    value = n_q * n_sets / (ms * 1e-3)
-    rec_bytes = total_vec * engine.record_words(L, C) * 4
-    per_launch_sets = min(n_sets, chunk)
-    traffic4, traffic4_src = _ncu_traffic("cfg4", per_launch_sets / 1_000_000 * n_q / 1024)
-    alg4 = rec_bytes * per_launch_sets / n_sets + n_q * per_launch_sets * 8
-    # e2e: one query_batch call (public API) with pinned host query vectors and host results
-    Qh = Qv.cpu().pin_memory()
-    te = time.perf_counter()
-    s_e, i_e = d.query_batch(idx, Qh.to(dev, non_blocking=True), top_k, return_tensors=True)
-    hs, hi = s_e.cpu(), i_e.cpu()
-    e2e_s = time.perf_counter() - te
-    line = {
-        "metric": "set-pair scores/sec (cfg4: 8M sets x 1024 query sets, L=32 C=8, exhaustive, top-1000)",
-        "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u8", "data": "synthetic (cfg4-shaped codes, generated on GPU)",
-        "config": {"workload": "cfg4", "n_sets": n_sets, "n_qsets": n_q, "m_q": m_q, "L": L, "C": C,
-                   "top_k": top_k, "vectors": total_vec, "score_chunk_sets": chunk,
-                   "l2": "inputs larger than L2 (17.9 GB records)", "generation_s": t_gen},
-        "roofline": {"bound": "int", "unit": "Gcompare/s", "achieved": achieved / 1e9,
-                     "peak": p_int / 1e9, "frac": achieved / p_int, "traffic": traffic4,
-                     "traffic_detail": dict(traffic4_src or {}, per="one 1M-set launch",
-                                            algorithmic_bytes=alg4,
-                                            ratio=None if traffic4 is None else traffic4 / alg4),
-                     "kernel": "score_all_kernel<8,1,1,8,4>", "kernel_ms_per_step": k_ms,
-                     "launches_per_step": launches_per_step,
-                     "per_step": {"compares": compares, "code_bytes_per_pass": rec_bytes},
-                     "achieved_hbm_gbs_code_stream": rec_bytes / (k_ms * 1e-3) / 1e9,
-                     "peak_source": "measured in-run: LOP3 lane-ops/s x 4", "int_microbench": mb},
-        "e2e": {"value": n_q * n_sets / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": Qh.numel() * Qh.element_size(),
-                "d2h_bytes_per_step": hs.numel() * 8 + hi.numel() * 8, "ms_per_step": e2e_s * 1e3,
-                "path": "query_batch (hash -> chunked exhaustive scoring -> top-k merge)"},
-        "clocks": clk, "gpu_launches": (2 + 2 * launches_per_step) * args.steps,
-    }
-    del so
-    print(json.dumps(line))
-    return 0
 
 
 def run_cfg3(args):
@@ -806,6 +767,12 @@ def run_cfg2(args):
                 "path": "build_from_vectors (pinned host bf16 -> device, hash, layout)"},
         "clocks": clk, "gpu_launches": 4 * args.steps,
     }
+    if not args.no_cpu_baseline:
+        import bench_reference as BR
+
+        r = BR.build_baseline(L=L, C=C)
+        line["cpu_baseline"] = {"value": r["value"], "unit": "vectors/s", "cores": r["cores"],
+                                "kind": r["kind"], "sample": r["sample"]}
     print(json.dumps(line))
     return 0
 
@@ -817,21 +784,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
     ap.add_argument("--vectors", type=int, default=0, help="override cfg2 vector count")
-    ap.add_argument("--sets", type=int, default=0, help="override N (cfg3/cfg4)")
+    ap.add_argument("--sets", type=int, default=0, help="override N (cfg1/3/4)")
+    ap.add_argument("--cpu-sets", type=int, default=20_000,
+                    help="sets in the CPU reference sample (per step: 8 query sets x this)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--score-buffer", type=int, default=8 << 30)
     ap.add_argument("--latency-queries", type=int, default=1000)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    if args.config == 4:
-        return run_cfg4(args)
     if args.config == 3:
         return run_cfg3(args)
     if args.config == 2:
         return run_cfg2(args)
-    return run_gpu(args)
+    return run_scoring(args, args.config)
 
 
 if __name__ == "__main__":

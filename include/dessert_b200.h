@@ -175,6 +175,35 @@ int dsrt_topk_indexed(const double *scores, int64_t ld, const uint64_t *ids, con
                       double *out_scores, uint64_t *out_ids, int64_t *out_pos, void *stream);
 
 /*
+ * Exhaustive search = K3 + K4 fused through survivor lists (search.cu):
+ * replaces query()'s exhaustive branch, _score_chunk over every set plus
+ * heapq.nsmallest(top_k, key=(-score, doc_id)) (index.py:250-261, 302-319),
+ * for n_qsets query sets at once, without materialising the score matrix.
+ * sigma = max with optional weights (m_q float64 or NULL).  Outputs
+ * out_scores / out_ids (n_qsets, k) as dsrt_topk (padding -1.0 / UINT64_MAX).
+ * mode 0: threshold rounds when profitable (K3 epilogue appends sets whose
+ * score reaches the running k-th best); mode 1: materialised chunks of at most
+ * score_buffer_bytes, merged by K4.  *overflow (device int32) is set when a
+ * survivor list overflowed in mode 0: results are then invalid and the caller
+ * reruns with mode 1.  No host synchronisation inside (graph-capturable).
+ */
+size_t dsrt_search_all_workspace(int64_t n_sets, int64_t n_qsets, int m_q, int k, int mode,
+                                 size_t score_buffer_bytes);
+int dsrt_search_all(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                    const uint64_t *doc_ids, const uint32_t *qrecords, int64_t n_qsets, int m_q,
+                    int L, int C, const double *lut, const double *weights, int k, int mode,
+                    size_t score_buffer_bytes, double *out_scores, uint64_t *out_ids,
+                    int32_t *overflow, void *workspace, size_t ws_bytes, void *stream);
+/*
+ * Measurement hook: while enabled, every launch of dsrt_search_all is bracketed
+ * by CUDA events on its stream; _read synchronises on them and returns the
+ * summed milliseconds of the scoring launches and of the top-k / list launches
+ * and the number of launch calls timed since the last read (then resets).
+ */
+void dsrt_search_profile(int enable);
+int dsrt_search_profile_read(double *score_ms, double *other_ms, int64_t *launches);
+
+/*
  * K5 -- replaces prefilter.filter_candidates (prefilter.py:111-144).
  * Q: (n_qsets * m_q, d) float64 query vectors; centroids (k_c, d) float64.
  * postings CSR: post_off (k_c + 1), post_docs (ascending doc indices).

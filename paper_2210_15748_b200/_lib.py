@@ -58,6 +58,11 @@ SIGNATURES = {
     "dsrt_collision_counts": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "dsrt_topk": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_topk_max_k": (_i32, []),
+    "dsrt_search_all_workspace": (_sz, [_i64, _i64, _i32, _i32, _i32, _sz]),
+    "dsrt_search_profile": (None, [_i32]),
+    "dsrt_search_profile_read": (_i32, [_vp, _vp, _vp]),
+    "dsrt_search_all": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32,
+                               _i32, _sz, _vp, _vp, _vp, _vp, _sz, _vp]),
     "dsrt_topk_indexed": (_i32, [_vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_prefilter": (_i32, [_vp, _i64, _i32, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _i32, _i32,
                               _vp, _vp, _vp, _sz, _vp]),

@@ -6,45 +6,63 @@
 namespace dsrt {
 
 // ----------------------------------------------- m_q > 128: finalize pass
-__device__ double pw_rec(const double *a, int n) {
+// per-query value w[i] * LUT[c_q] of one (query set, set) row
+struct McRow {
+    const uint16_t *mc;
+    const double *lut, *w;
+    __device__ __forceinline__ double operator()(int i) const {
+        const double v = __ldg(lut + mc[i]);
+        return __dmul_rn(w != nullptr ? __ldg(w + i) : 1.0, v);
+    }
+};
+
+// numpy pairwise_sum_DOUBLE of f(lo .. lo + n - 1): 8 strided accumulators per
+// <= 128 leaf, recursive split n2 = n/2 - (n/2 mod 8) above (no scratch).
+template <class F>
+__device__ double pw_rec(const F &f, int lo, int n) {
     if (n < 8) {
         double r = 0.0;
-        for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+        for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(lo + i));
         return r;
     }
     if (n <= 128) {
         double r[8];
-        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        for (int j = 0; j < 8; ++j) r[j] = f(lo + j);
         int i;
         for (i = 8; i < n - (n % 8); i += 8)
-            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(lo + i + j));
         double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                                __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+        for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
         return res;
     }
     int n2 = n / 2;
     n2 -= n2 % 8;
-    return __dadd_rn(pw_rec(a, n2), pw_rec(a + n2, n - n2));
+    return __dadd_rn(pw_rec(f, lo, n2), pw_rec(f, lo + n2, n - n2));
 }
 
-// One thread per (row): LUT[maxcounts] -> numpy pairwise mean; a = per-thread
-// scratch in global memory (rows * m_q doubles).
-__global__ void finalize_kernel(const uint16_t *__restrict__ mc, int64_t rows, int m_q,
+// One thread per target e < w of one query set: LUT[maxcounts] -> weighted
+// numpy pairwise mean -> out[e].  Candidate lists: entries e >= n_cand stay
+// unwritten and invalid set indices get NaN, as on the m_q <= 128 path (their
+// maxcount rows were never written and are not read).
+__global__ void finalize_kernel(const uint16_t *__restrict__ mc, int64_t w, int m_q,
                                 const double *__restrict__ lut, const double *__restrict__ weights,
-                                double *__restrict__ scratch, double *__restrict__ scores,
-                                int64_t row_len, int64_t ld) {
-    const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (r >= rows) return;
-    double *a = scratch + r * m_q;
-    for (int i = 0; i < m_q; ++i) {
-        const double v = __ldg(lut + mc[r * m_q + i]);
-        a[i] = weights != nullptr ? __dmul_rn(__ldg(weights + i), v) : v;
+                                double *__restrict__ out, const int64_t *__restrict__ cand_row,
+                                const int32_t *__restrict__ n_cand_q, int64_t n_sets) {
+    const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (e >= w) return;
+    if (n_cand_q != nullptr && e >= tmin<int64_t>(w, tmax<int32_t>(0, __ldg(n_cand_q)))) return;
+    if (cand_row != nullptr) {
+        const int64_t s = __ldg(cand_row + e);
+        if (s < 0 || s >= n_sets) {
+            out[e] = __longlong_as_double(0x7ff8000000000000ll);
+            return;
+        }
     }
-    const double sum = __dadd_rn(0.0, pw_rec(a, m_q));
-    scores[(r / row_len) * ld + (r % row_len)] = __ddiv_rn(sum, static_cast<double>(m_q));
+    const McRow f{mc + e * m_q, lut, weights};
+    const double sum = __dadd_rn(0.0, pw_rec(f, 0, m_q));
+    out[e] = __ddiv_rn(sum, static_cast<double>(m_q));
 }
-
 
 extern template int run_w<1>(const ScoreArgs &, int, int, cudaStream_t);
 extern template int run_w<2>(const ScoreArgs &, int, int, cudaStream_t);
@@ -83,8 +101,12 @@ static int run_k(const ScoreArgs &a, int C, int qpl, cudaStream_t st) {
 }
 
 // m_q <= 128 runs in one pass; larger m_q runs 128-query slices writing
-// maxcounts, then finalize_kernel applies numpy's recursive pairwise sum.
-static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
+// uint16 maxcounts, then finalize_kernel applies numpy's recursive pairwise sum.
+// The maxcount scratch is bounded: set ranges are processed in sub-ranges of
+// at most kMcBudget bytes per query set.
+constexpr size_t kMcBudget = size_t(256) << 20;
+
+int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
     if (const char *e = getenv("DSRT_QS")) a.qs_override = atoi(e);
     DSRT_REQUIRE(a.m_q >= 1, DSRT_EINVAL, "empty query: need at least one query vector");
     DSRT_REQUIRE(a.L >= 1 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", a.L, C);
@@ -96,47 +118,65 @@ static int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
         a.mc_q0 = 0;
         return run_k(a, C, qpl == 3 ? 4 : qpl, st);
     }
-    const int64_t row_len = a.cand_mode ? a.cand_ld : (a.se - a.sb);
-    const int64_t rows = a.n_qsets * row_len;
-    if (rows == 0) return DSRT_OK;
-    // Each 128-query slice is a pseudo query set: query slice r of set q has
-    // records at qrecs + (q*m_q + 128*r)*R, which the kernel addresses as
-    // (qset*m_q_slice + qi)*R only when m_q_slice == m_q.  Run slices per query
-    // set with n_qsets = 1 to keep the addressing simple.
-    uint16_t *mc = a.mc;
+    DSRT_REQUIRE(a.app.tau == nullptr, DSRT_EUNSUPPORTED,
+                 "invalid parameter: threshold append needs m_q <= 128");
+    // targets of one query set: [t0, t1) = set range (exhaustive), identity
+    // candidates [0, cand_ld) (cand == nullptr) or one candidate list (unsplit)
+    const bool split = !a.cand_mode || a.cand == nullptr;
+    const int64_t width = a.cand_mode ? a.cand_ld : (a.se - a.sb);
+    if (width == 0) return DSRT_OK;
+    const int64_t sub = split ? tmax<int64_t>(1, static_cast<int64_t>(kMcBudget / (2 * a.m_q))) : width;
     uint16_t *own = nullptr;
-    if (mc == nullptr) {
-        DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&own), rows * a.m_q * sizeof(uint16_t), st));
-        mc = own;
-    }
-    double *scratch = nullptr;
-    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&scratch), rows * a.m_q * sizeof(double), st));
+    if (a.mc == nullptr)
+        DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&own),
+                               static_cast<size_t>(tmin(sub, width)) * a.m_q * sizeof(uint16_t), st));
+    const int64_t ld = a.cand_mode ? a.cand_ld : a.ld;
     int rc = DSRT_OK;
     for (int64_t qs = 0; qs < a.n_qsets && rc == DSRT_OK; ++qs) {
-        for (int q0 = 0; q0 < a.m_q && rc == DSRT_OK; q0 += 128) {
-            ScoreArgs b = a;
-            b.n_qsets = 1;
-            b.m_q = min(128, a.m_q - q0);
-            b.qrecs = a.qrecs + (qs * a.m_q + q0) * static_cast<int64_t>(R);
-            b.scores = nullptr;
-            b.weights = nullptr;
-            b.mc = mc + qs * row_len * a.m_q;
-            b.mc_stride = a.m_q;
-            b.mc_q0 = q0;
-            if (b.cand_mode && b.cand) b.cand = a.cand + qs * a.cand_ld;
-            if (b.cand_mode && b.n_cand) b.n_cand = a.n_cand + qs;
-            const int qpl = (b.m_q + 31) / 32;
-            rc = run_k(b, C, qpl == 3 ? 4 : qpl, st);
+        for (int64_t e0 = 0; e0 < width && rc == DSRT_OK; e0 += sub) {
+            const int64_t e1 = tmin(width, e0 + sub);
+            // maxcounts of (qs, e0 .. e1): the caller's array or the scratch
+            uint16_t *mc = own ? own : a.mc + (qs * ld + e0) * a.m_q;
+            for (int q0 = 0; q0 < a.m_q && rc == DSRT_OK; q0 += 128) {
+                // Each 128-query slice is a pseudo query set (n_qsets = 1) whose
+                // records start at qrecs + (qs*m_q + q0)*R; it writes uint16 counts
+                // at mc[e*m_q + q0 + qi].
+                ScoreArgs b = a;
+                b.n_qsets = 1;
+                b.m_q = min(128, a.m_q - q0);
+                b.qrecs = a.qrecs + (qs * a.m_q + q0) * static_cast<int64_t>(R);
+                b.scores = nullptr;
+                b.weights = nullptr;
+                b.mc = mc;
+                b.mc_stride = a.m_q;
+                b.mc_q0 = q0;
+                b.ld = e1 - e0;
+                if (!b.cand_mode) {
+                    b.sb = a.sb + e0;
+                    b.se = a.sb + e1;
+                } else if (b.cand == nullptr) {  // identity candidates: shift the set window
+                    b.set_off = a.set_off + e0;
+                    b.n_sets = tmin<int64_t>(a.n_sets - e0, e1 - e0);
+                    b.cand_ld = e1 - e0;
+                    b.n_cand = nullptr;  // entries >= n_cand may be written (they are unspecified)
+                } else {
+                    b.cand = a.cand + qs * a.cand_ld;
+                    if (a.n_cand) b.n_cand = a.n_cand + qs;
+                }
+                const int qpl = (b.m_q + 31) / 32;
+                rc = run_k(b, C, qpl == 3 ? 4 : qpl, st);
+            }
+            if (rc == DSRT_OK && a.scores != nullptr) {
+                const int64_t w = e1 - e0;
+                const bool list = a.cand_mode && a.cand != nullptr;
+                const int32_t *nc = list && a.n_cand ? a.n_cand + qs : nullptr;
+                finalize_kernel<<<static_cast<unsigned>((w + 127) / 128), 128, 0, st>>>(
+                    mc, w, a.m_q, a.lut, a.weights, a.scores + qs * ld + e0,
+                    list ? a.cand + qs * a.cand_ld : nullptr, nc, a.n_sets);
+                if (cudaGetLastError() != cudaSuccess) rc = DSRT_ECUDA;
+            }
         }
     }
-    if (rc == DSRT_OK && a.scores != nullptr) {
-        const int64_t blocks = (rows + 127) / 128;
-        finalize_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(
-            mc, rows, a.m_q, a.lut, a.weights, scratch, a.scores, row_len,
-            a.cand_mode ? a.cand_ld : a.ld);
-        if (cudaGetLastError() != cudaSuccess) rc = DSRT_ECUDA;
-    }
-    cudaFreeAsync(scratch, st);
     if (own) cudaFreeAsync(own, st);
     return rc;
 }

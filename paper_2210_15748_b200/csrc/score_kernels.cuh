@@ -62,6 +62,20 @@ __device__ __forceinline__ double lane_score(const uint8_t *__restrict__ row, in
     return __ddiv_rn(__dadd_rn(0.0, res), static_cast<double>(n));
 }
 
+// Threshold-append epilogue (exhaustive search, search.cu): instead of
+// storing every score, a set whose score reaches the query set's current
+// threshold tau[q] (the k-th best score so far) is appended as (score, doc id)
+// to the query set's survivor list at cnt[q]++ (one atomic per warp flush).
+// Appends past `cap` are counted but not stored (overflow -> caller reruns).
+struct AppendOut {
+    const double *tau;        // (n_qsets) thresholds; nullptr = append mode off
+    int32_t *cnt;             // (n_qsets) list fill
+    double *cs;               // (n_qsets, cap) scores
+    uint64_t *cid;            // (n_qsets, cap) doc ids
+    const uint64_t *doc_ids;  // (n_sets) doc id of each set
+    int64_t cap;
+};
+
 // Per-warp deferred epilogue: 32 slot rows of c_q bytes.
 template <int QPL>
 struct Slots {
@@ -112,6 +126,35 @@ struct Slots {
             if (mc != nullptr && ok) {
                 uint16_t *dst = mc + (mc_row0 + col0 + lane) * mc_stride + mc_q0;
                 for (int i = 0; i < m_q; ++i) dst[i] = row[i];
+            }
+        }
+        __syncwarp();
+        n = 0;
+        valid = 0;
+    }
+
+    // append-mode flush: lane i < n scores slot i (set index set0 + i) and
+    // appends it when score >= tau[qs]
+    __device__ __forceinline__ void flush_append(int m_q, const double *__restrict__ lut_s,
+                                                 const double *__restrict__ w_s,
+                                                 const AppendOut &app, int64_t qs, int64_t set0) {
+        const int lane = threadIdx.x & 31;
+        __syncwarp();
+        double sc = 0.0;
+        bool keep = false;
+        if (lane < n && ((valid >> lane) & 1u)) {
+            sc = lane_score(buf + lane * SlotGeom<QPL>::kRow, m_q, lut_s, w_s);
+            keep = sc >= __ldg(app.tau + qs);
+        }
+        const unsigned bal = __ballot_sync(kFull, keep);
+        if (bal != 0u) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(app.cnt + qs, __popc(bal));
+            base = __shfl_sync(kFull, base, 0);
+            const int64_t pos = base + __popc(bal & ((1u << lane) - 1u));
+            if (keep && pos < app.cap) {
+                app.cs[qs * app.cap + pos] = sc;
+                app.cid[qs * app.cap + pos] = __ldg(app.doc_ids + set0 + lane);
             }
         }
         __syncwarp();
@@ -342,7 +385,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
                      int64_t set_begin, int64_t set_end, const uint32_t *__restrict__ qrecs,
                      int64_t n_qsets, int m_q, int L, const double *__restrict__ lut,
                      const double *__restrict__ weights, double *__restrict__ scores, int64_t ld,
-                     uint16_t *__restrict__ maxcounts, int mc_stride, int mc_q0, int n_chunks) {
+                     uint16_t *__restrict__ maxcounts, int mc_stride, int mc_q0, int n_chunks,
+                     AppendOut app) {
     constexpr int R = ((K * W) + 3) & ~3;
     constexpr int S = QS * QPL;  // register slots per lane
     constexpr int kTileVec = tile_vec<K, W>();
@@ -423,9 +467,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
 #pragma unroll
         for (int j = 0; j < QS; ++j) {
             const int64_t qs = qset0 + j;
-            if (qs < n_qsets)
-                slots[j].flush(m_q, lut_s, w_s, scores ? scores + qs * ld : nullptr, slot_col, maxcounts,
-                               qs * ld, mc_stride, mc_q0);
+            if (qs < n_qsets) {
+                if (app.tau != nullptr)
+                    slots[j].flush_append(m_q, lut_s, w_s, app, qs, set_begin + slot_col);
+                else
+                    slots[j].flush(m_q, lut_s, w_s, scores ? scores + qs * ld : nullptr, slot_col,
+                                   maxcounts, qs * ld, mc_stride, mc_q0);
+            }
             slots[j].n = 0;
             slots[j].valid = 0;
         }
@@ -676,7 +724,7 @@ template <int K, int W, int QPL, int QS>
 static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, int64_t se,
                       const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
                       const double *weights, double *scores, int64_t ld, uint16_t *mc,
-                      int mc_stride, int mc_q0, cudaStream_t st) {
+                      int mc_stride, int mc_q0, const AppendOut &app, cudaStream_t st) {
     constexpr int NW = 8;
     const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1 + m_q) * sizeof(double);
     auto kern = score_all_kernel<K, W, QPL, NW, QS>;
@@ -694,7 +742,7 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
     DSRT_REQUIRE(groups < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many query sets");
     kern<<<grid, (NW + 1) * 32, smem, st>>>(recs, set_off, sb, se, qrecs, n_qsets, m_q, L, lut,
                                            weights, scores, ld, mc, mc_stride, mc_q0,
-                                           static_cast<int>(chunks));
+                                           static_cast<int>(chunks), app);
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
@@ -746,7 +794,11 @@ struct ScoreArgs {
     uint16_t *mc;
     int mc_stride, mc_q0;
     int qs_override;  // 0 = heuristic; else query sets per warp (1/2/4)
+    AppendOut app;    // exhaustive threshold-append epilogue (app.tau == nullptr: off)
 };
+
+// K3 entry (score.cu): dispatch on (C, W, QPL, QS); m_q > 128 via slices + finalize.
+int score_dispatch(ScoreArgs a, int C, cudaStream_t st);
 
 template <int K, int W, int QPL>
 static int run_one(const ScoreArgs &a, cudaStream_t st) {
@@ -766,13 +818,15 @@ static int run_one(const ScoreArgs &a, cudaStream_t st) {
         const int qs = a.qs_override > 0 ? a.qs_override : (a.n_qsets >= 256 ? (W == 1 ? 4 : 2) : 1);
         if (qs == 4)
             return launch_all<K, W, QPL, 4>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
-                                            a.L, a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+                                            a.L, a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0,
+                                            a.app, st);
         if (qs == 2)
             return launch_all<K, W, QPL, 2>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q,
-                                            a.L, a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+                                            a.L, a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0,
+                                            a.app, st);
     }
     return launch_all<K, W, QPL, 1>(a.recs, a.set_off, a.sb, a.se, a.qrecs, a.n_qsets, a.m_q, a.L,
-                                    a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, st);
+                                    a.lut, a.weights, a.scores, a.ld, a.mc, a.mc_stride, a.mc_q0, a.app, st);
 }
 
 template <int K, int W>

@@ -44,15 +44,12 @@ def all_gather_topk(scores: torch.Tensor, ids: torch.Tensor, group=None):
 
 
 def merge_topk_device(scores: torch.Tensor, ids: torch.Tensor, k: int):
-    """Device re-rank of gathered candidates with K4 (padding scores < 0 sort last)."""
+    """Device re-rank of gathered candidates with K4 (score desc, doc id asc).  Padding
+    entries (score -1.0, id UINT64_MAX) sort after every real score (K4 orders keys by
+    IEEE value), so they surface only when fewer than k real candidates exist."""
     from . import engine
 
-    valid = (scores >= 0).sum(dim=1).to(torch.int32)
-    # padded entries are -1.0; push them past the valid ones by masking to 0 count via n_valid
-    order = torch.argsort((scores < 0).to(torch.int8), dim=1, stable=True)
-    s = torch.gather(scores, 1, order).contiguous()
-    i = torch.gather(ids, 1, order).contiguous()
-    out_s, out_i, _ = engine.topk(s, min(k, s.shape[1]), ids=i, n_valid=valid)
+    out_s, out_i, _ = engine.topk(scores.contiguous(), min(k, scores.shape[1]), ids=ids.contiguous())
     return out_s, out_i
 
 

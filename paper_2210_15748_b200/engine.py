@@ -260,7 +260,43 @@ def topk(scores: torch.Tensor, k: int, ids: torch.Tensor | None = None, n_valid=
 
 
 def topk_max_k() -> int:
+    """Largest k of the shared-memory selector; larger k runs the global-merge kernel."""
     return _lib.lib().dsrt_topk_max_k()
+
+
+def search_all(records, set_off, doc_ids, qrecords, m_q: int, L: int, C: int, lut, k: int,
+               weights=None, mode: int = 0, score_buffer_bytes: int = 4 << 30):
+    """Exhaustive top-k of every query set over all sets (K3 + K4 fused, dsrt_search_all).
+
+    Returns (scores (n_q, k) f64, doc ids (n_q, k) int64, overflow (1,) int32 device flag).
+    mode 0 may set ``overflow`` (survivor list too small): the caller reruns with mode 1."""
+    _need(set_off, torch.int64, "set_off")
+    _need(doc_ids, torch.int64, "doc_ids")
+    n_sets = set_off.shape[0] - 1
+    n_q = qrecords.shape[0] // m_q
+    if weights is not None:
+        _need(weights, torch.float64, "weights")
+    out_s = torch.empty((n_q, k), dtype=torch.float64, device=records.device)
+    out_i = torch.empty((n_q, k), dtype=torch.int64, device=records.device)
+    ovf = torch.empty(1, dtype=torch.int32, device=records.device)
+    ws_bytes = _lib.lib().dsrt_search_all_workspace(n_sets, n_q, m_q, k, mode, score_buffer_bytes)
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=records.device)
+    _lib.call("dsrt_search_all", _ptr(records), _ptr(set_off), n_sets, _ptr(doc_ids), _ptr(qrecords),
+              n_q, m_q, L, C, _ptr(lut), _ptr(weights), k, mode, score_buffer_bytes, _ptr(out_s),
+              _ptr(out_i), _ptr(ovf), _ptr(ws), ws_bytes, _stream())
+    return out_s, out_i, ovf
+
+
+def search_profile(enable: bool) -> None:
+    """Bracket every dsrt_search_all launch with CUDA events (measurement hook)."""
+    _lib.lib().dsrt_search_profile(1 if enable else 0)
+
+
+def search_profile_read() -> dict:
+    """Summed ms of the scoring and top-k/list launches since the last read (syncs)."""
+    a, b, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    _lib.call("dsrt_search_profile_read", ctypes.byref(a), ctypes.byref(b), ctypes.byref(n))
+    return {"score_ms": a.value, "other_ms": b.value, "launches": n.value}
 
 
 # ------------------------------------------------------------------- K5

@@ -279,48 +279,36 @@ def add_sets(index: DessertIndex, docs) -> DessertIndex:
         if str(e).startswith("zero vector"):
             raise ValueError(f"zero vector in document {_zero_row_doc(items)}") from None
         raise
+    # validate and build every new piece first; the index is updated only when all
+    # of them succeeded (a failed call leaves it unchanged)
     all_sizes = np.concatenate([index.sizes, sizes])
-    index.records = torch.cat([index.records, recs])
-    if index.codes is not None:
-        index.codes = torch.cat([index.codes, codes])
-    index.set_off = _layout(all_sizes, index.device)
-    index.sizes = all_sizes
-    index.doc_ids = np.concatenate([index.doc_ids, np.array([i for i, _ in items], np.uint64)])
-    index.doc_ids_dev = torch.from_numpy(index.doc_ids.view(np.int64)).to(index.device)
+    set_off = _layout(all_sizes, index.device)          # raises "set too large"
+    new_filter = None
     if index.filter is not None:
         from .prefilter import extend_centroid_index
 
         centroids, cindex = index.filter
-        index.filter = (centroids, extend_centroid_index(cindex, X, centroids, sizes))
+        new_filter = (centroids, extend_centroid_index(cindex, X, centroids, sizes))
+    records = torch.cat([index.records, recs])
+    codes_all = torch.cat([index.codes, codes]) if index.codes is not None else None
+    doc_ids = np.concatenate([index.doc_ids, np.array([i for i, _ in items], np.uint64)])
+    doc_ids_dev = torch.from_numpy(doc_ids.view(np.int64)).to(index.device)
+    index.records, index.codes, index.set_off, index.sizes = records, codes_all, set_off, all_sizes
+    index.doc_ids, index.doc_ids_dev = doc_ids, doc_ids_dev
+    if new_filter is not None:
+        index.filter = new_filter
     return index
 
 
 # --------------------------------------------------------------------- query
 def _rank(scores: torch.Tensor, top_k: int, ids: torch.Tensor, n_valid=None, cand=None):
-    """Row-wise (score desc, doc_id asc) top-k on the device.  With ``cand`` (candidate
-    set indices per row), element i of row r has doc id ids[cand[r, i]]."""
+    """Row-wise (score desc, doc_id asc) top-k on the device (K4, any k).  With ``cand``
+    (candidate set indices per row), element i of row r has doc id ids[cand[r, i]]."""
     rows, n = scores.shape
-    k = min(top_k, n)
-    if k <= engine.topk_max_k():
-        if cand is not None:  # ids gathered inside the kernel
-            return engine.topk(scores, k, ids=ids, n_valid=n_valid, id_index=cand.contiguous())
-        return engine.topk(scores, k, ids=ids, n_valid=n_valid)
-    if cand is not None:
-        ids = ids[cand.clamp(min=0)]
-    # k beyond the single-CTA selector: stable two-key sort on the device
-    ids2 = ids if ids.dim() == 2 else ids.expand(rows, n)
-    valid = torch.ones_like(scores, dtype=torch.bool)
-    if n_valid is not None:
-        valid = torch.arange(n, device=scores.device)[None, :] < n_valid[:, None].long()
-    s = torch.where(valid, scores, torch.full_like(scores, -1.0))
-    o1 = torch.argsort(ids2, dim=1, stable=True)
-    s1 = torch.gather(s, 1, o1)
-    o2 = torch.argsort(-s1, dim=1, stable=True)
-    pos = torch.gather(o1, 1, o2)[:, :k]
-    out_s = torch.gather(s, 1, pos)
-    out_i = torch.gather(ids2, 1, pos)
-    bad = out_s < 0
-    return (out_s.masked_fill(bad, -1.0), out_i.masked_fill(bad, -1), pos.masked_fill(bad, -1))
+    k = max(1, min(top_k, n))
+    if cand is not None:  # ids gathered inside the kernel
+        return engine.topk(scores, k, ids=ids, n_valid=n_valid, id_index=cand.contiguous())
+    return engine.topk(scores, k, ids=ids, n_valid=n_valid)
 
 
 def _results(out_s: torch.Tensor, out_i: torch.Tensor) -> list[RankedResults]:
@@ -385,6 +373,9 @@ def _rank_records_plan(index: DessertIndex, qrecs, m_q: int, top_k: int, plan: S
         scores = _score_plan_sets(index, qrecs, m_q, plan, cand=cand, n_cand=n_cand)
         out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev, n_valid=n_cand, cand=cand)
         return out_s, out_i
+    if plan.kind == 0 and _fast_kernels(index.config.L, index.config.C):
+        # weighted sigma = max: the fused exhaustive search (weights in the K3 epilogue)
+        return _search(index, qrecs, m_q, top_k, plan.weights, 0)
     chunk = max(1, min(N, SCORE_BUFFER_BYTES // (8 * n_q)))
     if chunk >= N:
         scores = _score_plan_sets(index, qrecs, m_q, plan, n_q=n_q, cand_ld=N)
@@ -403,8 +394,13 @@ def _rank_records_plan(index: DessertIndex, qrecs, m_q: int, top_k: int, plan: S
     return out_s, out_i
 
 
+def _fast_kernels(L: int, C: int) -> bool:
+    """The K3 kernels' envelope (score_max_fast_supported in score.cu)."""
+    return 1 <= L <= 128 and 1 <= C <= 16 and C * ((L + 31) // 32) <= 32
+
+
 def rank_records(index: DessertIndex, qrecs: torch.Tensor, m_q: int, top_k: int,
-                 cand=None, n_cand=None, plan: ScorePlan | None = None):
+                 cand=None, n_cand=None, plan: ScorePlan | None = None, exhaustive_mode: int = 0):
     """Score query-set records (n_qsets*m_q, R) and rank; returns (scores, ids) (n_qsets, k).
 
     ``plan`` (from ``score_plan``) selects the general aggregation kernel for
@@ -420,34 +416,23 @@ def rank_records(index: DessertIndex, qrecs: torch.Tensor, m_q: int, top_k: int,
                                             index.lut_dev, cand=cand, n_cand=n_cand)
         out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev, n_valid=n_cand, cand=cand)
         return out_s, out_i
-    if n_q < 8:
-        scores, _ = engine.score_candidates(index.records, index.set_off, qrecs, m_q, L, C,
-                                            index.lut_dev, cand_ld=N, n_qsets=n_q)
-        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev)
-        return out_s, out_i
-    # exhaustive batched: chunk the set range so the score buffer stays bounded
-    chunk = max(1, min(N, SCORE_BUFFER_BYTES // (8 * n_q)))
-    if chunk >= N:
-        scores, _ = engine.score_all(index.records, index.set_off, qrecs, m_q, L, C,
-                                     index.lut_dev)
-        out_s, out_i, _ = _rank(scores, top_k, index.doc_ids_dev)
-        return out_s, out_i
-    buf = torch.empty((n_q, chunk), dtype=torch.float64, device=index.device)
-    parts_s, parts_i = [], []
-    for s0 in range(0, N, chunk):
-        s1 = min(N, s0 + chunk)
-        engine.score_all(index.records, index.set_off, qrecs, m_q, L, C, index.lut_dev,
-                         set_begin=s0, set_end=s1, scores=buf, ld=chunk)
-        ps, pi, _ = _rank(buf[:, : s1 - s0] if s1 - s0 < chunk else buf, top_k,
-                          index.doc_ids_dev[s0:s1])
-        parts_s.append(ps)
-        parts_i.append(pi)
-    S = torch.cat(parts_s, dim=1).contiguous()
-    I = torch.cat(parts_i, dim=1).contiguous()
-    valid = (S >= 0).sum(dim=1).to(torch.int32)
-    # padded entries (-1) sort last; n_valid is not needed because -1 < any score
-    out_s, out_i, _ = _rank(S, top_k, I)
-    del valid
+    return _search(index, qrecs, m_q, top_k, None, exhaustive_mode)
+
+
+def _search(index: DessertIndex, qrecs, m_q: int, top_k: int, weights, mode: int):
+    """Exhaustive ranking of every set (dsrt_search_all: K3 + K4 without the score
+    matrix).  Threshold mode (0) reruns materialised (1) when a survivor list
+    overflowed; mode 1 alone inside CUDA-graph capture (no host sync)."""
+    L, C = index.config.L, index.config.C
+    k = max(1, min(top_k, index.n_docs))
+    args = (index.records, index.set_off, index.doc_ids_dev, qrecs, m_q, L, C, index.lut_dev, k)
+    if mode == 0 and torch.cuda.is_current_stream_capturing():
+        mode = 1
+    out_s, out_i, ovf = engine.search_all(*args, weights=weights, mode=mode,
+                                          score_buffer_bytes=SCORE_BUFFER_BYTES)
+    if mode == 0 and int(ovf.item()) != 0:
+        out_s, out_i, _ = engine.search_all(*args, weights=weights, mode=1,
+                                            score_buffer_bytes=SCORE_BUFFER_BYTES)
     return out_s, out_i
 
 
@@ -468,6 +453,7 @@ class _QueryGraph:
         self.top_k, self.probe, self.k_filter = top_k, probe, k_filter
         self.deps = self._deps(index)
         self.lock = threading.Lock()
+        self.done = None  # event: last replay's outputs copied out
         self.q_in = torch.empty(q.shape, dtype=q.dtype, device=index.device)
         self.q_in.copy_(q)
         self._run(index)  # eager warm-up: lazy initialisation outside the capture
@@ -500,15 +486,25 @@ class _QueryGraph:
         cand = n_cand = None
         if ix.filter is not None:
             cand, n_cand = _candidates(ix, Qdev, m_q, self.probe, self.k_filter)
-        out_s, out_i = rank_records(ix, qrecs, m_q, self.top_k, cand, n_cand)
+        out_s, out_i = rank_records(ix, qrecs, m_q, self.top_k, cand, n_cand, exhaustive_mode=1)
         return out_s, out_i, zero, n_cand
 
     def __call__(self, q: torch.Tensor, to_host: bool = True):
+        # The captured buffers (q_in, outputs) are shared by every caller: the next
+        # caller's stream waits until the previous replay and its output copies
+        # finished (they may run on another stream when to_host=False).
+        stream = torch.cuda.current_stream()
+        if self.done is not None:
+            stream.wait_event(self.done)
         self.q_in.copy_(q, non_blocking=True)
         self.graph.replay()
         if to_host:
-            return tuple(None if t is None else t.cpu() for t in self.out)
-        return tuple(None if t is None else t.clone() for t in self.out)
+            out = tuple(None if t is None else t.cpu() for t in self.out)
+        else:
+            out = tuple(None if t is None else t.clone() for t in self.out)
+        self.done = torch.cuda.Event()
+        self.done.record(stream)
+        return out
 
 
 def _graph_ok(index: DessertIndex, n_q: int) -> bool:
