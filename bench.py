@@ -329,7 +329,7 @@ def run_scoring(args, workload):
         idx = d.build_from_records(recs, sizes, np.arange(n_sets), cfg)
         del recs
     Q2 = Qv.reshape(n_q * m_q, 128).contiguous()
-    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0])
+    mode = d.lsh.default_mode(Q2.dtype, 128, C, Q2.shape[0], L)
     planes = idx.family.device_planes(mode, dev)
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()

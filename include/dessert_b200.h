@@ -45,7 +45,9 @@ enum dsrt_dtype { DSRT_F32 = 0, DSRT_F64 = 1, DSRT_F16 = 2, DSRT_BF16 = 3 };
 enum dsrt_hash_mode {
     DSRT_HASH_F64 = 0,      /* planes float64 (L*C, d); DFMA accumulation         */
     DSRT_HASH_F32 = 1,      /* planes float32 (L*C, d); FFMA accumulation         */
-    DSRT_HASH_TC_F16 = 2,   /* tcgen05 kind::f16; planes fp16 (L*C, d), X fp16      */
+    DSRT_HASH_TC_FIX = 2,   /* tcgen05 kind::f16, one fp16 pass + exact fix-up of the bits
+                               near zero; planes float64 (L*C, d) (the reference's);
+                               X fp16 or bf16; d = 128, C <= 8, L*C <= ~600        */
     DSRT_HASH_TC_BF16X2 = 3, /* tcgen05 kind::f16; planes bf16 hi/lo (2, L*C, d), X bf16 */
     DSRT_HASH_TC_F16X2 = 4   /* tcgen05 kind::f16; planes fp16 hi/lo (2, L*C, d), X fp16 */
 };

@@ -20,7 +20,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "dessert_b200.h")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED, ERANGE = 0, 1, 2, 3, 4
 F32, F64, F16, BF16 = 0, 1, 2, 3
-HASH_F64, HASH_F32, HASH_TC_F16, HASH_TC_BF16X2, HASH_TC_F16X2 = 0, 1, 2, 3, 4
+HASH_F64, HASH_F32, HASH_TC_FIX, HASH_TC_BF16X2, HASH_TC_F16X2 = 0, 1, 2, 3, 4
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64

@@ -250,6 +250,8 @@ static int launch_hash(const void *X, int64_t n, int d, const void *planes, int 
 
 int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, int mode, int L,
             int C, void *codes_out, uint32_t *records_out, uint32_t *zero_rows, cudaStream_t st);
+int hash_fix(const void *X, int x_dtype, int64_t n, int d, const void *planes, int L, int C,
+             void *codes_out, uint32_t *records_out, uint32_t *zero_rows, cudaStream_t st);
 
 }  // namespace dsrt
 
@@ -266,7 +268,9 @@ extern "C" int dsrt_hash(const void *X, int x_dtype, int64_t n, int d, const voi
                  "invalid parameter: L*C=%d exceeds %d hash bits per vector", L * C, 32 * kMaxBitWords);
     if (n == 0) return DSRT_OK;
     cudaStream_t st = as_stream(stream);
-    if (mode == DSRT_HASH_TC_F16 || mode == DSRT_HASH_TC_BF16X2 || mode == DSRT_HASH_TC_F16X2)
+    if (mode == DSRT_HASH_TC_FIX)
+        return hash_fix(X, x_dtype, n, d, planes, L, C, codes_out, records_out, zero_rows, st);
+    if (mode == DSRT_HASH_TC_BF16X2 || mode == DSRT_HASH_TC_F16X2)
         return hash_tc(X, x_dtype, n, d, planes, mode, L, C, codes_out, records_out, zero_rows, st);
     DSRT_REQUIRE(mode == DSRT_HASH_F64 || mode == DSRT_HASH_F32, DSRT_EINVAL,
                  "invalid parameter: hash mode %d", mode);

@@ -222,14 +222,11 @@ __global__ void permute_planes_kernel(const uint16_t *__restrict__ src, int part
     dst[i] = tg < L ? src[(static_cast<int64_t>(part) * L * C + tg * C + b) * 128 + k] : uint16_t(0);
 }
 
-static int launch_hash_tc_c(int C, int parts, int stages, const CUtensorMap &mx,
+static int launch_hash_tc_c(int C, int /*parts: always 2 (hi/lo)*/, int stages, const CUtensorMap &mx,
                             const CUtensorMap &mw, const HashTcParams &hp, uint32_t idesc,
                             size_t smem, int ctas, cudaStream_t st) {
 #define DSRT_HC(c)                                                                            \
     case c:                                                                                   \
-        if (parts == 1)                                                                       \
-            return stages == 3 ? launch_hash_tc<1, c, 3>(mx, mw, hp, idesc, smem, ctas, st)   \
-                               : launch_hash_tc<1, c, 2>(mx, mw, hp, idesc, smem, ctas, st);  \
         return stages == 3 ? launch_hash_tc<2, c, 3>(mx, mw, hp, idesc, smem, ctas, st)       \
                            : launch_hash_tc<2, c, 2>(mx, mw, hp, idesc, smem, ctas, st);
     switch (C) {
@@ -244,7 +241,7 @@ static int launch_hash_tc_c(int C, int parts, int stages, const CUtensorMap &mx,
 int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, int mode, int L,
             int C, void *codes_out, uint32_t *records_out, uint32_t *zero_rows, cudaStream_t st) {
     const bool bf16 = mode == DSRT_HASH_TC_BF16X2;
-    const int parts = mode == DSRT_HASH_TC_F16 ? 1 : 2;
+    const int parts = 2;
     DSRT_REQUIRE(x_dtype == (bf16 ? DSRT_BF16 : DSRT_F16), DSRT_EINVAL,
                  "invalid parameter: tensor-core hash mode %d needs %s vectors", mode,
                  bf16 ? "bf16" : "fp16");

@@ -36,7 +36,7 @@ namespace dsrt {
 namespace {
 
 constexpr int64_t kGrowth = 8;         // round length ratio
-constexpr int64_t kSeedDiv = 64;       // seed = N / 64 sets (at least kSeedMinK * k)
+constexpr int64_t kSeedDiv = 512;      // seed = N / 512 sets (at least kSeedMinK * k): its scores are materialised
 constexpr int64_t kSeedMinK = 4;
 constexpr size_t kThresholdMinBytes = size_t(512) << 20;  // score matrix size that switches modes
 

@@ -479,7 +479,7 @@ class _QueryGraph:
         q = self.q_in
         m_q = q.shape[-2]
         Qdev = to_device_matrix(q.reshape(-1, q.shape[-1]), ix.config.d, ix.device)
-        mode = default_mode(Qdev.dtype, Qdev.shape[1], ix.config.C, Qdev.shape[0])
+        mode = default_mode(Qdev.dtype, Qdev.shape[1], ix.config.C, Qdev.shape[0], ix.config.L)
         _, qrecs, zero = engine.hash_vectors(Qdev, ix.family.device_planes(mode, ix.device), mode,
                                              ix.config.L, ix.config.C, want_codes=False,
                                              want_records=True, check_zero=True)

@@ -39,12 +39,10 @@ class SrpFamily:
         t = self._dev.get(key)
         if t is None:
             p = torch.from_numpy(np.ascontiguousarray(self.planes))
-            if mode == _lib.HASH_F64:
+            if mode in (_lib.HASH_F64, _lib.HASH_TC_FIX):  # TC_FIX splits them on the device
                 t = p.to(device=device, dtype=torch.float64)
             elif mode == _lib.HASH_F32:
                 t = p.to(device=device, dtype=torch.float32)
-            elif mode == _lib.HASH_TC_F16:
-                t = p.to(dtype=torch.float16).to(device)
             elif mode in (_lib.HASH_TC_BF16X2, _lib.HASH_TC_F16X2):
                 dt = torch.bfloat16 if mode == _lib.HASH_TC_BF16X2 else torch.float16
                 hi = p.to(dt)
@@ -89,13 +87,16 @@ def build_sim_lookup(C: int, L: int) -> SimLookup:
     return SimLookup(C=C, L=L, table=table)
 
 
-def default_mode(dtype, d: int = 128, C: int = 7, n: int = 0) -> int:
+def default_mode(dtype, d: int = 128, C: int = 7, n: int = 0, L: int = 64) -> int:
     """Hash arithmetic per input dtype (K1).
 
     float32/float64 inputs hash in float64 against the float64 planes (exact).
     fp16 / bf16 inputs with d = 128, C <= 8 use the tcgen05 kernel with hi/lo
-    split planes (operand rounding <= 2^-17 relative, far inside the
-    1e-4 band); small batches (< 4096 rows) use float64 SIMT.
+    split planes (two MMA passes; operand rounding <= 2^-17 relative, far inside
+    the 1e-4 band).  HASH_TC_FIX (one fp16 MMA pass + an exact fix-up of the
+    bits near zero) gives the same guarantee but measured slower (its epilogue,
+    not the tensor pipe, is the bound: DESIGN.md K1), so it is opt-in.  Small
+    batches (< 4096 rows) use float64 SIMT.
     """
     if d == 128 and C <= 8 and n >= 4096:
         if dtype == torch.bfloat16:
@@ -124,7 +125,8 @@ def to_device_matrix(X, d: int, device="cuda") -> torch.Tensor:
 def hash_device(family: SrpFamily, X: torch.Tensor, mode: int | None = None, want_codes=True,
                 want_records=True, check_zero=True):
     """Hash a CUDA matrix; raises the reference's 'zero vector' error."""
-    mode = default_mode(X.dtype, X.shape[1], family.C, X.shape[0]) if mode is None else mode
+    mode = (default_mode(X.dtype, X.shape[1], family.C, X.shape[0], family.L) if mode is None
+            else mode)
     planes = family.device_planes(mode, X.device)
     codes, recs, zero = engine.hash_vectors(X, planes, mode, family.L, family.C, want_codes,
                                             want_records, check_zero)

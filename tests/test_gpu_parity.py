@@ -117,8 +117,8 @@ def test_hash_modes_flip_only_in_band(mode, dtype):
     assert torch.equal(recs, recs2)
 
 
-TC_CASES = [(torch.float16, _lib.HASH_TC_F16X2), (torch.float16, _lib.HASH_TC_F16),
-            (torch.bfloat16, _lib.HASH_TC_BF16X2)]
+TC_CASES = [(torch.float16, _lib.HASH_TC_F16X2), (torch.float16, _lib.HASH_TC_FIX),
+            (torch.bfloat16, _lib.HASH_TC_FIX), (torch.bfloat16, _lib.HASH_TC_BF16X2)]
 
 
 @pytest.mark.parametrize("dtype,mode", TC_CASES)
@@ -143,10 +143,7 @@ def test_hash_tensor_core_flip_only_in_band(dtype, mode, L, C):
     bits_want = ((want[:, :, None] >> np.arange(C)) & 1).reshape(n, L * C)
     flips = bits_got != bits_want
     outside = int((flips & ~band).sum())
-    if mode != _lib.HASH_TC_F16:
-        assert outside == 0, f"{outside} flips outside the band ({int(flips.sum())} total)"
-    else:  # single fp16 rounding of the planes: report, allow a vanishing rate
-        assert outside <= 2, outside
+    assert outside == 0, f"{outside} flips outside the band ({int(flips.sum())} total)"
     recs2, _ = engine.codes_to_records(codes, L, C)
     assert torch.equal(recs, recs2)
     # zero rows are detected
@@ -154,6 +151,77 @@ def test_hash_tensor_core_flip_only_in_band(dtype, mode, L, C):
     Xz[17] = 0
     with pytest.raises(ValueError, match="zero vector"):
         d.lsh.hash_device(fam, Xz.to(DEV).contiguous(), mode=mode)
+
+
+def _band_check(fam, X64, got, L, C):
+    """flips of GPU codes vs the float64 oracle, and whether each lies in the 1e-4 band"""
+    n = X64.shape[0]
+    want = O.hash_matrix(fam.planes, L, C, X64)
+    proj = O.projections(fam.planes, X64)
+    band = np.abs(proj) < 1e-4 * np.linalg.norm(fam.planes, axis=1)[None, :] * \
+        np.linalg.norm(X64, axis=1)[:, None]
+    bg = ((got[:, :, None] >> np.arange(C)) & 1).reshape(n, L * C)
+    bw = ((want[:, :, None] >> np.arange(C)) & 1).reshape(n, L * C)
+    return bg != bw, band
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_hash_fix_mode_near_zero_projections(dtype):
+    """TC_FIX on vectors built to sit almost on planes (|w.x| ~ 1e-6..1e-2 |w||x| for
+    chosen (row, plane) pairs): thousands of bits go through the fix-up, none may
+    differ from the float64 reference outside the 1e-4 band."""
+    rng = np.random.default_rng(77)
+    L, C, n = 64, 7, 6000
+    fam = d.sample_srp_family(128, C, L, 9)
+    W = fam.planes
+    X = rng.standard_normal((n, 128))
+    p = rng.integers(0, L * C, size=n)
+    for k in range(3):  # project three planes each (almost) out of every row
+        p = (p + 37 * k) % (L * C)
+        w = W[p]
+        X -= ((X * w).sum(1) / (w * w).sum(1))[:, None] * w
+        X += (10.0 ** rng.uniform(-6, -2, size=n))[:, None] * w / np.linalg.norm(w, axis=1)[:, None]
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    Xt = torch.from_numpy(X).to(dtype)
+    X64 = Xt.to(torch.float64).numpy()
+    codes, recs = d.lsh.hash_device(fam, Xt.to(DEV).contiguous(), mode=_lib.HASH_TC_FIX)
+    got = codes.cpu().numpy().astype(np.int64)
+    flips, band = _band_check(fam, X64, got, L, C)
+    assert int((flips & ~band).sum()) == 0
+    proj = O.projections(W, X64) / np.linalg.norm(W, axis=1)[None, :]
+    assert int((np.abs(proj) < 1e-2).sum()) > 3 * n  # the fix-up path really ran
+    recs2, _ = engine.codes_to_records(codes, L, C)
+    assert torch.equal(recs, recs2)
+
+
+def test_hash_fix_mode_bf16_extreme_magnitudes():
+    """bf16 rows spanning 1e-30 .. 1e30 in scale (and rows with subnormal-range
+    elements) are scaled per row before the fp16 rounding: same bits as the float64
+    reference outside the band; codes equal the fp16-input result for rows that are
+    exact in both types."""
+    rng = np.random.default_rng(5)
+    L, C, n = 32, 8, 4500
+    fam = d.sample_srp_family(128, C, L, 2)
+    X = rng.standard_normal((n, 128))
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    X *= (10.0 ** rng.uniform(-30, 30, size=n))[:, None]
+    X[::7, ::3] *= 1e-6  # elements far below the row maximum (fp16 subnormal range)
+    Xt = torch.from_numpy(X).to(torch.bfloat16)
+    X64 = Xt.to(torch.float64).numpy()
+    codes, _ = d.lsh.hash_device(fam, Xt.to(DEV).contiguous(), mode=_lib.HASH_TC_FIX)
+    flips, band = _band_check(fam, X64, codes.cpu().numpy().astype(np.int64), L, C)
+    assert int((flips & ~band).sum()) == 0
+
+
+def test_hash_fix_mode_ragged_and_unsupported():
+    rng = np.random.default_rng(1)
+    fam = d.sample_srp_family(128, 5, 40, 4)
+    X = rng.standard_normal((4099, 128)).astype(np.float16)
+    codes, _ = d.lsh.hash_device(fam, torch.from_numpy(X).to(DEV), mode=_lib.HASH_TC_FIX)
+    flips, band = _band_check(fam, X.astype(np.float64), codes.cpu().numpy().astype(np.int64), 40, 5)
+    assert int((flips & ~band).sum()) == 0
+    with pytest.raises(ValueError, match="fp16 or bf16"):
+        d.lsh.hash_device(fam, torch.from_numpy(X.astype(np.float32)).to(DEV), mode=_lib.HASH_TC_FIX)
 
 
 # ------------------------------------------------------------------- layout
