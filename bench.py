@@ -653,6 +653,14 @@ def run_cfg3(args):
         # count, placement plan, place, score, top-k
         "gpu_launches": 13 * args.steps,
     }
+    if not args.no_cpu_baseline:
+        import bench_reference as BR
+
+        r = BR.cfg3_baseline(n_qsets=16)
+        if r is not None:
+            line["cpu_baseline"] = {"value": r["value"], "unit": r["unit"], "cores": r["cores"],
+                                    "kind": r["kind"], "sample": r["sample"],
+                                    "per_query_set_s": r["per_query_set_s"], "setup_s": r["setup_s"]}
     print(json.dumps(line))
     return 0
 

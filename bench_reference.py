@@ -262,3 +262,97 @@ def build_baseline(*, L, C, n_vec_hash=1 << 20, n_sets_tt=20_000, seed=9, procs=
             "sample": f"hash_matrix on {n_vec_hash} vectors ({t_hash:.1f} s, OpenBLAS {procs} threads) "
                       f"+ build_tiny_table on {n_sets_tt} sets / {need} vectors ({t_tt:.1f} s, "
                       f"{procs}-process fork pool); value = 1/(1/hash + 1/tinytable) vectors/s"}
+
+
+# ------------------------------------------------------------ cfg3 (prefilter pipeline)
+class _PoolSketches:
+    """A length-N sequence of reference TinyTables backed by a pool of real ones
+    (set i -> pool[i % len(pool)]): the reference's query() only indexes
+    index.sketches[i] and takes len(), so it runs unmodified over N sets."""
+
+    def __init__(self, pool, n):
+        self.pool, self.n = pool, n
+
+    def __len__(self):
+        return self.n
+
+    def __getitem__(self, i):
+        return self.pool[i % len(self.pool)]
+
+
+def _cfg3_worker(args):
+    _limit_blas()
+    lo, hi, top_k = args
+    ri, _, _ = _import_ref()
+    index, Qs = _STATE["index"], _STATE["Q"]
+    t0 = time.perf_counter()
+    out = [ri.query(index, Qs[i], top_k) for i in range(lo, hi)]
+    return time.perf_counter() - t0, len(out)
+
+
+def cfg3_baseline(*, L=32, C=7, n_sets=1_000_000, n_cent=65536, probe=4, k_filter=4096, top_k=100,
+                  n_qsets=16, pool_sets=2000, seed=11, procs=None):
+    """cfg3 reference: the UNMODIFIED dessert.query with the centroid prefilter on a
+    cfg3-shaped index -- 1M sets whose postings come from ~70M vectors drawn over
+    65,536 centroids (prefilter.py:111-144 on the full-size CentroidIndex), and
+    TinyTables from a pool of 2,000 real sets for the <= 4,096 candidates
+    (_score_chunk, index.py:250-261) -- one query set per host core at a time."""
+    kind = reference_kind()
+    if kind != "reference":
+        return None
+    procs = procs or host_cores()
+    ri, rl, rs = _import_ref()
+    import dessert.prefilter as rp
+
+    t_setup = time.perf_counter()
+    rng = np.random.default_rng(seed)
+    cents = rng.standard_normal((n_cent, 128))
+    cents /= np.linalg.norm(cents, axis=1, keepdims=True)
+    sizes = np.clip(np.rint(rng.normal(70.0, 20.0, size=n_sets)), 8, 180).astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    n_vec = int(off[-1])
+    vcent = rng.integers(0, n_cent, size=n_vec).astype(np.int64)  # each vector's centroid
+    key = np.unique(vcent * n_sets + np.repeat(np.arange(n_sets, dtype=np.int64), sizes))
+    pc, pdoc = np.divmod(key, n_sets)
+    bounds = np.searchsorted(pc, np.arange(n_cent + 1))
+    postings = [pdoc[bounds[c]:bounds[c + 1]] for c in range(n_cent)]
+    del key, pc
+    cfg = ri.IndexConfig(d=128, C=C, L=L, seed=0,
+                         filter=ri.FilterConfig(enabled=True, centroids=n_cent, probe=probe,
+                                                k_filter=k_filter))
+    fam = rl.sample_srp_family(128, C, L, 0)
+    pool = []
+    for s in range(pool_sets):
+        m = int(sizes[s])
+        v = cents[vcent[off[s]:off[s] + m]] + 0.05 * rng.standard_normal((m, 128))
+        v = (v / np.linalg.norm(v, axis=1, keepdims=True)).astype(np.float16).astype(np.float64)
+        pool.append(rs.build_tiny_table(rl.hash_matrix(fam, v), L, 1 << C))
+    index = ri.DessertIndex(config=cfg, family=fam, lookup=rl.build_sim_lookup(C, L),
+                            sketches=_PoolSketches(pool, n_sets),
+                            doc_ids=np.arange(n_sets, dtype=np.uint64),
+                            sizes=sizes[np.arange(n_sets) % pool_sets],
+                            filter=(rp.Centroids(k=n_cent, seed=0, vectors=cents),
+                                    rp.CentroidIndex(n_docs=n_sets, postings=postings)))
+    Q = np.empty((n_qsets, 32, 128))
+    for i in range(n_qsets):  # 32 perturbed vectors of a random set (its vectors' centroids)
+        s = int(rng.integers(0, n_sets))
+        rows = off[s] + rng.integers(0, sizes[s], size=32)
+        q = cents[vcent[rows]] + 0.05 * rng.standard_normal((32, 128)) + 0.1 * rng.standard_normal((32, 128))
+        Q[i] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    t_setup = time.perf_counter() - t_setup
+    _STATE["index"], _STATE["Q"] = index, Q
+    cuts = np.linspace(0, n_qsets, min(procs, n_qsets) + 1).astype(np.int64)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(cuts) - 1) as p:
+        p.map(_cfg3_worker, [(int(cuts[j]), int(cuts[j]) + 1, top_k) for j in range(len(cuts) - 1)])  # warm-up
+        t0 = time.perf_counter()
+        per = p.map(_cfg3_worker, [(int(cuts[j]), int(cuts[j + 1]), top_k) for j in range(len(cuts) - 1)])
+        wall = time.perf_counter() - t0
+    _STATE.clear()
+    return {"value": n_qsets / wall, "unit": "query sets/s", "cores": len(cuts) - 1, "kind": kind,
+            "wall_s": wall, "setup_s": t_setup, "per_query_set_s": float(np.mean([t for t, _ in per])),
+            "sample": f"{n_qsets} query sets through the unmodified dessert.query (prefilter probe "
+                      f"{probe}, k_filter {k_filter}, top-{top_k}) on a cfg3-shaped index: {n_sets} sets, "
+                      f"postings of {n_vec} vectors over {n_cent} centroids (filter_candidates at full "
+                      f"size), candidate TinyTables from a pool of {pool_sets} real L={L} C={C} sets; "
+                      f"{len(cuts) - 1}-process fork pool, one query set per process at a time"}

@@ -106,11 +106,50 @@ static int run_k(const ScoreArgs &a, int C, int qpl, cudaStream_t st) {
 // at most kMcBudget bytes per query set.
 constexpr size_t kMcBudget = size_t(256) << 20;
 
+bool score_max_fast_supported(int L, int C);
+int score_general_max(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                      const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                      const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, int C, const double *lut,
+                      const double *weights, double *scores, cudaStream_t st);
+
+// Shapes outside the register-blocked kernels (C > 16 or C * ceil(L/32) > 32;
+// the reference allows C <= 24 and any L, lsh.py:17, 54-66): scores through the
+// general kernel K3g (score_agg.cu) with sigma = max -- same arithmetic, no
+// register blocking.  Integer max counts and the threshold-append epilogue
+// stay with the fast kernels.
+static int score_general(const ScoreArgs &a, int C, cudaStream_t st) {
+    DSRT_REQUIRE(a.mc == nullptr && a.app.tau == nullptr, DSRT_EUNSUPPORTED,
+                 "invalid parameter: max counts / threshold search need C <= 16 and "
+                 "C*ceil(L/32) <= 32 (L=%d, C=%d)", a.L, C);
+    if (a.scores == nullptr) return DSRT_OK;
+    const int R = record_words(a.L, C);
+    const int64_t width = a.cand_mode ? a.cand_ld : (a.se - a.sb);
+    if (width == 0) return DSRT_OK;
+    // exhaustive ranges: identity candidates over the shifted set window
+    const int64_t *off = a.cand_mode ? a.set_off : a.set_off + a.sb;
+    const int64_t ns = a.cand_mode ? a.n_sets : width;
+    const int64_t ld = a.ld > 0 ? a.ld : width;
+    if (ld == width)
+        return score_general_max(a.recs, off, ns, a.cand_mode ? a.cand : nullptr,
+                                 a.cand_mode ? a.n_cand : nullptr, width, a.qrecs, a.n_qsets, a.m_q,
+                                 a.L, C, a.lut, a.weights, a.scores, st);
+    for (int64_t qs = 0; qs < a.n_qsets; ++qs) {  // strided output rows: one query set per call
+        const int64_t *cq = a.cand_mode && a.cand ? a.cand + qs * a.cand_ld : nullptr;
+        const int32_t *nq = a.cand_mode && a.n_cand ? a.n_cand + qs : nullptr;
+        const int rc = score_general_max(a.recs, off, ns, cq, nq, width,
+                                         a.qrecs + qs * a.m_q * static_cast<int64_t>(R), 1, a.m_q, a.L,
+                                         C, a.lut, a.weights, a.scores + qs * ld, st);
+        if (rc) return rc;
+    }
+    return DSRT_OK;
+}
+
 int score_dispatch(ScoreArgs a, int C, cudaStream_t st) {
     if (const char *e = getenv("DSRT_QS")) a.qs_override = atoi(e);
     DSRT_REQUIRE(a.m_q >= 1, DSRT_EINVAL, "empty query: need at least one query vector");
     DSRT_REQUIRE(a.L >= 1 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", a.L, C);
     if (a.n_qsets == 0) return DSRT_OK;
+    if (!score_max_fast_supported(a.L, C)) return score_general(a, C, st);
     const int R = record_words(a.L, C);
     if (a.m_q <= 128) {
         const int qpl = (a.m_q + 31) / 32;

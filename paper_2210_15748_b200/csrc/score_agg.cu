@@ -14,8 +14,10 @@
 // Work item = (query set, target).  One warp per item, persistent grid; lane
 // = query vector (32-wide slices of m_q).  Target records are warp-uniform
 // (broadcast loads); the avg-phi counts c_qj > 0 are compacted per lane into
-// warp scratch [k][lane] (uint8, c <= L <= 255) and summed in the reference's
-// order afterwards.
+// warp scratch [k][lane] (uint16, c <= L) and summed in the reference's order
+// afterwards.  Any L (runtime plane-word loop above 128 tables) and C <= 24:
+// this kernel is also the sigma = max path for shapes outside the K3 kernels'
+// register envelope (C > 16 or C * ceil(L/32) > 32), see score_general in score.cu.
 #include "common.cuh"
 
 namespace dsrt {
@@ -35,10 +37,10 @@ int score_avg_fast(const uint32_t *records, const int64_t *set_off, int64_t n_se
 constexpr int64_t kOvfCap = 1 << 20;  // overflow items recomputed from a list
 
 constexpr int kAggWarps = 8;
-constexpr int kAggMaxC = 16;
+constexpr int kAggMaxC = 24;
 
 // numpy pairwise_sum_DOUBLE over v(start..start+n) where v(k) = table[s[k * 32]]
-__device__ double pw_counts(const uint8_t *s, int n, const double *__restrict__ table) {
+__device__ double pw_counts(const uint16_t *s, int n, const double *__restrict__ table) {
     if (n < 8) {
         double r = 0.0;
         for (int i = 0; i < n; ++i) r = __dadd_rn(r, __ldg(table + s[i * 32]));
@@ -101,7 +103,7 @@ struct AggArgs {
     const double *table;    // (L+1)
     const double *weights;  // (m_q) or NULL
     double *scores;         // (n_qsets, cand_ld)
-    uint8_t *scratch;       // per warp: 32 * m_cap count bytes, then m_q doubles
+    uint8_t *scratch;       // per warp: 32 * m_cap uint16 counts, then m_q doubles
     int64_t m_cap;
     size_t warp_bytes;
     uint32_t *status;       // bit 0: target set larger than m_cap
@@ -109,14 +111,17 @@ struct AggArgs {
     int64_t n_items;
 };
 
-template <int W>
+// WT = plane words per table bit held in registers (1..4); WT = 0: any W, query
+// words re-read through L1 for every set vector (L > 128, the rare shapes).
+template <int WT>
 __global__ void __launch_bounds__(kAggWarps * 32)
     score_agg_kernel(const AggArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = blockIdx.x * static_cast<int64_t>(kAggWarps) + (threadIdx.x >> 5);
     const int64_t n_warps = static_cast<int64_t>(gridDim.x) * kAggWarps;
-    uint8_t *cnt = a.scratch + gw * a.warp_bytes;
-    double *pq = reinterpret_cast<double *>(cnt + 32 * a.m_cap);
+    uint16_t *cnt = reinterpret_cast<uint16_t *>(a.scratch + gw * a.warp_bytes);
+    double *pq = reinterpret_cast<double *>(a.scratch + gw * a.warp_bytes + 64 * a.m_cap);
+    const int W = WT > 0 ? WT : plane_words(a.L);
     const int64_t items = a.items ? a.n_items : a.n_qsets * a.cand_ld;
     const uint32_t tail = (a.L % 32) ? ((1u << (a.L % 32)) - 1u) : 0xffffffffu;
     for (int64_t ii = gw; ii < items; ii += n_warps) {
@@ -141,29 +146,41 @@ __global__ void __launch_bounds__(kAggWarps * 32)
         for (int q0 = 0; q0 < a.m_q; q0 += 32) {
             const int q = q0 + lane;
             const bool act = q < a.m_q;
-            uint32_t qw[kAggMaxC][W];
+            constexpr int WR = WT > 0 ? WT : 1;
+            uint32_t qw[kAggMaxC][WR];
             const uint32_t *qr = a.qrecs + (qs * a.m_q + (act ? q : 0)) * static_cast<int64_t>(a.R);
+            if constexpr (WT > 0) {
 #pragma unroll
-            for (int b = 0; b < kAggMaxC; ++b)
+                for (int b = 0; b < kAggMaxC; ++b)
 #pragma unroll
-                for (int w = 0; w < W; ++w) qw[b][w] = (b < a.C) ? __ldg(qr + b * W + w) : 0u;
+                    for (int w = 0; w < WT; ++w) qw[b][w] = (b < a.C) ? __ldg(qr + b * WT + w) : 0u;
+            }
             int cmax = 0, nz = 0;
             for (int64_t j = 0; j < m; ++j) {
                 const uint32_t *x = xr + j * a.R;
                 int mm = 0;
+                if constexpr (WT > 0) {
 #pragma unroll
-                for (int w = 0; w < W; ++w) {
-                    uint32_t acc = 0;
+                    for (int w = 0; w < WT; ++w) {
+                        uint32_t acc = 0;
 #pragma unroll
-                    for (int b = 0; b < kAggMaxC; ++b)
-                        if (b < a.C) acc |= qw[b][w] ^ __ldg(x + b * W + w);
-                    if (w == W - 1) acc &= tail;
-                    mm += __popc(acc);
+                        for (int b = 0; b < kAggMaxC; ++b)
+                            if (b < a.C) acc |= qw[b][w] ^ __ldg(x + b * WT + w);
+                        if (w == WT - 1) acc &= tail;
+                        mm += __popc(acc);
+                    }
+                } else {
+                    for (int w = 0; w < W; ++w) {
+                        uint32_t acc = 0;
+                        for (int b = 0; b < a.C; ++b) acc |= __ldg(qr + b * W + w) ^ __ldg(x + b * W + w);
+                        if (w == W - 1) acc &= tail;
+                        mm += __popc(acc);
+                    }
                 }
                 const int c = a.L - mm;
                 cmax = tmax(cmax, c);
                 if (a.kind == 1 && c > 0 && act) {
-                    cnt[nz * 32 + lane] = static_cast<uint8_t>(c);
+                    cnt[nz * 32 + lane] = static_cast<uint16_t>(c);
                     ++nz;
                 }
             }
@@ -194,7 +211,7 @@ static int64_t agg_warps(int64_t items) {
 }
 
 static size_t agg_warp_bytes(int m_q, int64_t m_cap) {
-    return (static_cast<size_t>(32 * m_cap) + 15) / 16 * 16 + static_cast<size_t>(m_q) * 8;
+    return static_cast<size_t>(64 * m_cap) + static_cast<size_t>(m_q) * 8;
 }
 
 }  // namespace dsrt
@@ -218,7 +235,7 @@ extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, i
                               int64_t m_cap, double *scores, void *workspace, size_t ws_bytes,
                               void *stream) {
     DSRT_REQUIRE(m_q >= 1, DSRT_EINVAL, "empty query: need at least one query vector");
-    DSRT_REQUIRE(L >= 1 && L <= 255 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", L, C);
+    DSRT_REQUIRE(L >= 1 && L <= 65535 && C >= 1, DSRT_EINVAL, "invalid parameter: L=%d C=%d", L, C);
     DSRT_REQUIRE(C <= kAggMaxC, DSRT_EUNSUPPORTED, "invalid parameter: C=%d > %d", C, kAggMaxC);
     DSRT_REQUIRE(inner_kind == 0 || inner_kind == 1, DSRT_EINVAL,
                  "invalid parameter: inner_kind=%d (0 max, 1 avg-phi)", inner_kind);
@@ -227,7 +244,6 @@ extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, i
     DSRT_REQUIRE(cand != nullptr || cand_ld <= n_sets, DSRT_EINVAL,
                  "invalid parameter: cand_ld > n_sets without a candidate list");
     const int W = plane_words(L);
-    DSRT_REQUIRE(W <= 4, DSRT_EUNSUPPORTED, "invalid parameter: L=%d > 128 for the aggregation kernel", L);
     const int64_t items = n_qsets * cand_ld;
     if (items == 0) return DSRT_OK;
     if (inner_kind == 0 && score_max_fast_supported(L, C))  // weighted max: the K3 kernels
@@ -283,7 +299,8 @@ extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, i
         case 1: score_agg_kernel<1><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
         case 2: score_agg_kernel<2><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
         case 3: score_agg_kernel<3><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
-        default: score_agg_kernel<4><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
+        case 4: score_agg_kernel<4><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
+        default: score_agg_kernel<0><<<blocks, kAggWarps * 32, 0, st>>>(a); break;
     }
     DSRT_LAUNCH_CHECK();
     uint32_t h = 0;
@@ -293,3 +310,20 @@ extern "C" int dsrt_score_agg(const uint32_t *records, const int64_t *set_off, i
                  static_cast<long long>(m_cap));
     return DSRT_OK;
 }
+
+namespace dsrt {
+// sigma = max (kind 0) on the general kernel with its own stream-ordered workspace:
+// the K3 entry points' path for shapes outside the register-blocked kernels.
+int score_general_max(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
+                      const int64_t *cand, const int32_t *n_cand, int64_t cand_ld,
+                      const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, int C, const double *lut,
+                      const double *weights, double *scores, cudaStream_t st) {
+    const size_t ws = dsrt_score_agg_workspace(n_qsets, cand_ld, m_q, 0);
+    void *w = nullptr;
+    DSRT_CUDA(malloc_async(&w, ws, st));
+    const int rc = dsrt_score_agg(records, set_off, n_sets, cand, n_cand, cand_ld, qrecs, n_qsets, m_q, L, C,
+                                  0, lut, weights, 0, scores, w, ws, st);
+    cudaFreeAsync(w, st);
+    return rc;
+}
+}  // namespace dsrt

@@ -56,12 +56,16 @@ struct Plan {
     size_t off_lists = 0, off_cnt = 0, off_tau = 0, total = 0;
 };
 
-Plan make_plan(int64_t N, int64_t n_q, int m_q, int k, int mode, size_t buf_bytes) {
+}  // namespace
+bool score_max_fast_supported(int L, int C);
+namespace {
+
+Plan make_plan(int64_t N, int64_t n_q, int m_q, int k, int mode, size_t buf_bytes, bool fast = true) {
     Plan p;
     const int64_t per_set = 8 * tmax<int64_t>(1, n_q);
     const int64_t chunk_w = tmax<int64_t>(1, tmin<int64_t>(N, static_cast<int64_t>(buf_bytes) / per_set));
     const int64_t s0 = tmin<int64_t>(chunk_w, tmax<int64_t>(N / kSeedDiv, kSeedMinK * k));
-    p.threshold = mode == 0 && m_q <= 128 && n_q >= 8 && s0 < N && s0 >= 2 * static_cast<int64_t>(k) &&
+    p.threshold = mode == 0 && fast && m_q <= 128 && n_q >= 8 && s0 < N && s0 >= 2 * static_cast<int64_t>(k) &&
                   static_cast<size_t>(n_q) * N * 8 > threshold_min_bytes();
     if (p.threshold) {
         p.chunk = s0;
@@ -243,7 +247,9 @@ using namespace dsrt;
 extern "C" size_t dsrt_search_all_workspace(int64_t n_sets, int64_t n_qsets, int m_q, int k, int mode,
                                             size_t score_buffer_bytes) {
     if (n_sets <= 0 || n_qsets <= 0 || k < 1) return 256;
-    return make_plan(n_sets, n_qsets, m_q, k, mode, score_buffer_bytes).total;
+    // either plan (threshold rounds need fast-kernel shapes; others run materialised)
+    return tmax(make_plan(n_sets, n_qsets, m_q, k, mode, score_buffer_bytes, true).total,
+                make_plan(n_sets, n_qsets, m_q, k, mode, score_buffer_bytes, false).total);
 }
 
 extern "C" int dsrt_search_all(const uint32_t *records, const int64_t *set_off, int64_t n_sets,
@@ -266,7 +272,7 @@ extern "C" int dsrt_search_all(const uint32_t *records, const int64_t *set_off, 
         t.scores = nullptr; t.ld = 0; t.n = 0; t.k = k; t.out_s = out_scores; t.out_id = out_ids;
         return topk_run(t, n_qsets, st);
     }
-    const Plan p = make_plan(n_sets, n_qsets, m_q, k, mode, score_buffer_bytes);
+    const Plan p = make_plan(n_sets, n_qsets, m_q, k, mode, score_buffer_bytes, score_max_fast_supported(L, C));
     DSRT_REQUIRE(workspace != nullptr && ws_bytes >= p.total, DSRT_EINVAL,
                  "invalid parameter: search workspace %zu < %zu bytes", ws_bytes, p.total);
     uint8_t *ws = static_cast<uint8_t *>(workspace);

@@ -346,8 +346,8 @@ def score_plan(index: DessertIndex, scorer: Scorer | None, m_q: int) -> ScorePla
     scorer = scorer or index.config.scorer()
     weights = scoring.resolve_weights(scorer, m_q)
     kind = scoring.inner_kind_code(scorer)
-    if kind == 0 and weights is None:
-        return None
+    if kind == 0 and weights is None and _fast_kernels(index.config.L, index.config.C):
+        return None  # shapes outside the K3 register envelope take the general kernel
     table = scoring.table_for(index.lookup.table, scorer)
     return ScorePlan(
         kind=kind,

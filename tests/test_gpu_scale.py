@@ -183,3 +183,75 @@ def test_cfg4_full_size_one_query_set():
     out_s, out_i = d.query_codes_batch(idx, qcodes, top_k, return_tensors=True)
     np.testing.assert_array_equal(out_i[0].cpu().numpy().astype(np.int64), order)
     np.testing.assert_array_equal(out_s[0].cpu().numpy(), want[order])
+
+
+def _hash_flips_vs_f64(planes: np.ndarray, Xs: torch.Tensor, codes: torch.Tensor, L: int, C: int):
+    """Bit flips of device codes vs the float64 projection X @ planes.T > 0 (lsh.py:103),
+    and how many of them lie outside |w.x| < 1e-4 |w||x|.  float64 GEMM on the device
+    as the checker, 250k rows at a time."""
+    P = torch.from_numpy(planes).to(Xs.device)
+    wn = P.norm(dim=1)
+    flips = outside = 0
+    for lo in range(0, Xs.shape[0], 250_000):
+        x = Xs[lo:lo + 250_000].double()
+        proj = x @ P.T
+        want = (proj > 0).reshape(-1, L, C)
+        c = codes[lo:lo + 250_000].to(torch.int64)
+        got = ((c[:, :, None] >> torch.arange(C, device=c.device)) & 1).bool()
+        f = (got != want).reshape(x.shape[0], L * C)
+        band = proj.abs() < 1e-4 * wn[None, :] * x.norm(dim=1)[:, None]
+        flips += int(f.sum())
+        outside += int((f & ~band).sum())
+    return flips, outside
+
+
+@pytest.mark.parametrize("mode", ["default", "fix"])
+def test_cfg2_full_size_hash_band(mode):
+    """cfg2: 10M bf16 mixture vectors (4,096 centroids, noise 0.05), L=64 C=7: the
+    device codes of 1M sampled rows flip no bit outside the 1e-4 band vs float64
+    (SURVEY 8(c)); the flip rate is printed (the north star asks for it reported)."""
+    from paper_2210_15748_b200 import _lib
+
+    n, L, C = 10_000_000, 64, 7
+    X, _ = workloads.gpu_mixture(n, 4096, 128, 0.05, seed=601, dtype=torch.bfloat16, device=DEV)
+    fam = d.sample_srp_family(128, C, L, 0)
+    m = None if mode == "default" else _lib.HASH_TC_FIX
+    codes, _ = d.lsh.hash_device(fam, X, mode=m, want_records=False)
+    g = torch.Generator(device=DEV)
+    g.manual_seed(7)
+    samp = torch.randperm(n, generator=g, device=DEV)[:1_000_000]
+    flips, outside = _hash_flips_vs_f64(fam.planes, X[samp], codes[samp], L, C)
+    print(f"cfg2 hash ({mode}): {flips} flips in {1_000_000 * L * C} bits, {outside} outside the band")
+    assert outside == 0
+
+
+def test_cfg3_postings_exact_10m():
+    """K6 at cfg3's centroid count: 10M fp16 vectors from the 65,536-centroid mixture in
+    ~143k sets; every (document, centroid) posting pair equals the float64 argmax
+    assignment of all 10M vectors (prefilter.py:85-108), computed by a device float64
+    GEMM as the checker."""
+    n_cent = 65536
+    sizes = workloads.set_sizes(143_000, 70, 20, seed=510)
+    off = workloads.offsets(sizes)
+    n = int(off[-1])
+    X, cents = workloads.gpu_mixture(n, n_cent, 128, 0.05, seed=511, dtype=torch.float16, device=DEV)
+    cvec = cents.double()
+    cvec = cvec / cvec.norm(dim=1, keepdim=True)
+    centroids = prefilter.Centroids(k=n_cent, seed=0, vectors=cvec.cpu().numpy())
+    off_dev = torch.from_numpy(off).to(DEV)
+    cindex = prefilter.build_centroid_index(X, centroids, set_off=off_dev, n_docs=len(sizes))
+    # checker: float64 argmax of every vector (first index on ties, like np.argmax)
+    am = torch.empty(n, dtype=torch.int64, device=DEV)
+    CT = cvec.T.contiguous()
+    for lo in range(0, n, 131072):
+        s = X[lo:lo + 131072].double() @ CT
+        am[lo:lo + 131072] = torch.argmax(s, dim=1)
+    doc = torch.repeat_interleave(torch.arange(len(sizes), device=DEV),
+                                  torch.from_numpy(sizes).to(DEV))
+    want = torch.unique(am * len(sizes) + doc)  # (centroid, doc) pairs, deduplicated, sorted
+    po = cindex.post_off
+    cnt = (po[1:] - po[:-1]).to(torch.int64)
+    cid = torch.repeat_interleave(torch.arange(n_cent, device=DEV), cnt)
+    got = cid * len(sizes) + cindex.post_docs.to(torch.int64)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    assert torch.equal(got, want)  # also checks each posting is ascending and duplicate-free
