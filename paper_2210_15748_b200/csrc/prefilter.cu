@@ -1827,6 +1827,138 @@ extern "C" int dsrt_posting_chunk_bounds(const int64_t *post_off, const int64_t 
     return DSRT_OK;
 }
 
+
+// ====================================================================
+// General path: probe > kMaxProbe, k_filter > kSelMax or m_q*probe > 65535
+// (the reference accepts any values, prefilter.py:111-144).  Same arithmetic as
+// the fast path, with the per-row / per-query-set selections done by K4:
+//   sims    thread per (row, centroid): the sequential-FMA float64 dot of
+//           probe_kernel (bit-identical sims) -> rows x k_c
+//   probe   K4 top-P per row by (sim desc, id asc) = argsort(-sims, stable)[:P]
+//   count   warp per (query row, probed centroid) posting: u32 atomics per doc
+//   select  K4 top-k_filter per query set over keys (count, or -1 untouched)
+//           by (count desc, index asc); untouched docs never enter the list.
+// Temporaries are stream-ordered allocations, processed in bounded batches.
+namespace dsrt {
+int topk_run_ext(const double *scores, int64_t ld, int64_t n, int k, double *out_s, uint64_t *out_id,
+                 int64_t n_rows, cudaStream_t st);
+
+__global__ void pfg_sims_kernel(const double *__restrict__ Q, int64_t rows, int d,
+                                const double *__restrict__ cents, int64_t k_c, double *__restrict__ sims) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= rows * k_c) return;
+    const int64_t r = i / k_c, c = i - r * k_c;
+    const double *q = Q + r * d, *x = cents + c * d;
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc = fma(__ldg(q + k), __ldg(x + k), acc);
+    sims[i] = acc;
+}
+
+__global__ void pfg_probed_kernel(const uint64_t *__restrict__ ids, int64_t n, int32_t *__restrict__ probed) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) probed[i] = static_cast<int32_t>(ids[i]);
+}
+
+// grid.x: (query row, probe rank) pairs of one query set batch, grid.y: query set
+__global__ void pfg_count_kernel(const int32_t *__restrict__ probed, int mp, const int64_t *__restrict__ post_off,
+                                 const int64_t *__restrict__ post_docs, int64_t n_docs,
+                                 uint32_t *__restrict__ counts) {
+    const int64_t qs = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t pr = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
+    if (pr >= mp) return;
+    const int64_t c = probed[qs * mp + pr];
+    uint32_t *row = counts + qs * n_docs;
+    for (int64_t e = post_off[c] + lane; e < post_off[c + 1]; e += 32) atomicAdd(row + post_docs[e], 1u);
+}
+
+__global__ void pfg_keys_kernel(const uint32_t *__restrict__ counts, int64_t n, double *__restrict__ keys) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) keys[i] = counts[i] > 0u ? static_cast<double>(counts[i]) : -1.0;
+}
+
+// row per query set: cand = selected doc indices (count >= 1), -1 after n_cand
+__global__ void pfg_cand_kernel(const double *__restrict__ s, const uint64_t *__restrict__ ids, int k,
+                                int64_t *__restrict__ cand, int32_t *__restrict__ n_cand) {
+    const int64_t qs = blockIdx.x;
+    __shared__ int n;
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const bool ok = s[qs * k + i] >= 1.0;
+        cand[qs * k + i] = ok ? static_cast<int64_t>(ids[qs * k + i]) : -1;
+        mine += ok;
+    }
+    atomicAdd(&n, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) n_cand[qs] = n;
+}
+
+static int prefilter_general(const double *Q, int64_t n_q, int m_q, int d, const double *cents, int64_t k_c,
+                             const int64_t *post_off, const int64_t *post_docs, int64_t n_docs, int P,
+                             int k_filter, int64_t *cand, int32_t *n_cand, cudaStream_t st) {
+    const int64_t rows = n_q * m_q;
+    int32_t *probed = nullptr;
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&probed), static_cast<size_t>(rows) * P * 4, st));
+    // ---- probe: sims in row batches of <= 256 MB, top-P per row
+    const int64_t rb = tmax<int64_t>(1, tmin<int64_t>(rows, (int64_t(256) << 20) / (8 * k_c)));
+    double *sims = nullptr, *ts = nullptr;
+    uint64_t *ti = nullptr;
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&sims), static_cast<size_t>(rb) * k_c * 8, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&ts), static_cast<size_t>(rb) * P * 8, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&ti), static_cast<size_t>(rb) * P * 8, st));
+    int rc = DSRT_OK;
+    for (int64_t r0 = 0; r0 < rows && rc == DSRT_OK; r0 += rb) {
+        const int64_t nr = tmin(rb, rows - r0);
+        pfg_sims_kernel<<<static_cast<unsigned>((nr * k_c + 255) / 256), 256, 0, st>>>(Q + r0 * d, nr, d, cents,
+                                                                                      k_c, sims);
+        rc = topk_run_ext(sims, k_c, k_c, P, ts, ti, nr, st);
+        if (rc == DSRT_OK)
+            pfg_probed_kernel<<<static_cast<unsigned>((nr * P + 255) / 256), 256, 0, st>>>(ti, nr * P, probed + r0 * P);
+    }
+    cudaFreeAsync(sims, st);
+    cudaFreeAsync(ts, st);
+    cudaFreeAsync(ti, st);
+    if (rc) {
+        cudaFreeAsync(probed, st);
+        return rc;
+    }
+    // ---- count + select in query-set batches of <= 512 MB of counters and keys
+    const int64_t qb = tmax<int64_t>(1, tmin<int64_t>(n_q, (int64_t(512) << 20) / (12 * tmax<int64_t>(1, n_docs))));
+    uint32_t *counts = nullptr;
+    double *keys = nullptr, *os = nullptr;
+    uint64_t *oi = nullptr;
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&counts), static_cast<size_t>(qb) * n_docs * 4, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&keys), static_cast<size_t>(qb) * n_docs * 8, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&os), static_cast<size_t>(qb) * k_filter * 8, st));
+    DSRT_CUDA(malloc_async(reinterpret_cast<void **>(&oi), static_cast<size_t>(qb) * k_filter * 8, st));
+    const int mp = m_q * P;
+    for (int64_t q0 = 0; q0 < n_q && rc == DSRT_OK; q0 += qb) {
+        const int64_t nq = tmin(qb, n_q - q0);
+        if (cudaMemsetAsync(counts, 0, static_cast<size_t>(nq) * n_docs * 4, st) != cudaSuccess) {
+            rc = DSRT_ECUDA;
+            break;
+        }
+        pfg_count_kernel<<<dim3(static_cast<unsigned>((mp + 7) / 8), static_cast<unsigned>(nq)), 256, 0, st>>>(
+            probed + q0 * mp, mp, post_off, post_docs, n_docs, counts);
+        pfg_keys_kernel<<<static_cast<unsigned>((nq * n_docs + 255) / 256), 256, 0, st>>>(counts, nq * n_docs, keys);
+        rc = topk_run_ext(keys, n_docs, n_docs, k_filter, os, oi, nq, st);
+        if (rc == DSRT_OK)
+            pfg_cand_kernel<<<static_cast<unsigned>(nq), 256, 0, st>>>(os, oi, k_filter, cand + q0 * k_filter,
+                                                                      n_cand + q0);
+    }
+    cudaFreeAsync(counts, st);
+    cudaFreeAsync(keys, st);
+    cudaFreeAsync(os, st);
+    cudaFreeAsync(oi, st);
+    cudaFreeAsync(probed, st);
+    if (rc) return rc;
+    DSRT_LAUNCH_CHECK();
+    return DSRT_OK;
+}
+}  // namespace dsrt
+
 extern "C" size_t dsrt_prefilter_workspace(int64_t n_q, int m_q, int64_t k_c, int64_t n_docs,
                                            int probe) {
     const int P = static_cast<int>(tmin<int64_t>(tmax(probe, 1), k_c));
@@ -1843,13 +1975,12 @@ extern "C" int dsrt_prefilter(const double *Q, int64_t n_q, int m_q, int d, cons
     DSRT_REQUIRE(m_q >= 1 && n_q >= 0, DSRT_EINVAL, "Q must be a non-empty (m_q, d) matrix");
     DSRT_REQUIRE(k_c >= 1 && d >= 1, DSRT_EINVAL, "invalid parameter: k=%lld d=%d", (long long)k_c, d);
     const int P = static_cast<int>(tmin<int64_t>(probe, k_c));
-    DSRT_REQUIRE(P <= kMaxProbe, DSRT_EUNSUPPORTED, "invalid parameter: probe=%d exceeds %d", P, kMaxProbe);
-    DSRT_REQUIRE(k_filter <= kSelMax, DSRT_EUNSUPPORTED, "invalid parameter: k_filter=%d exceeds %d",
-                 k_filter, kSelMax);
     const int max_count = m_q * P;
-    DSRT_REQUIRE(max_count <= 65535, DSRT_EUNSUPPORTED, "invalid parameter: m_q*probe too large");
     DSRT_REQUIRE(k_c < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many centroids");
     if (n_q == 0) return DSRT_OK;
+    if (P > kMaxProbe || k_filter > kSelMax || max_count > 65535)
+        return prefilter_general(Q, n_q, m_q, d, cents, k_c, post_off, post_docs, n_docs, P, k_filter, cand,
+                                 n_cand, as_stream(stream));
     const PrefilterWs w = ws_layout(n_q, m_q, k_c, n_docs, P);
     DSRT_REQUIRE(workspace != nullptr && ws_bytes >= w.total, DSRT_EINVAL,
                  "invalid parameter: prefilter workspace too small");
@@ -1961,13 +2092,12 @@ extern "C" int dsrt_prefilter_tc(const double *Q, int64_t n_q, int m_q, int d, c
     DSRT_REQUIRE(m_q >= 1 && n_q >= 0, DSRT_EINVAL, "Q must be a non-empty (m_q, d) matrix");
     DSRT_REQUIRE(d == 128, DSRT_EUNSUPPORTED, "invalid parameter: tensor-core prefilter needs d=128");
     const int P = static_cast<int>(tmin<int64_t>(probe, k_c));
-    DSRT_REQUIRE(P <= kMaxPtc, DSRT_EUNSUPPORTED, "invalid parameter: probe=%d too large for the screen", P);
-    DSRT_REQUIRE(k_filter <= kSelMax, DSRT_EUNSUPPORTED, "invalid parameter: k_filter=%d exceeds %d",
-                 k_filter, kSelMax);
     const int max_count = m_q * P;
-    DSRT_REQUIRE(max_count <= 65535, DSRT_EUNSUPPORTED, "invalid parameter: m_q*probe too large");
     DSRT_REQUIRE(k_c < (1LL << 31) && cent_max_norm > 0, DSRT_EINVAL, "invalid parameter: centroids");
     if (n_q == 0) return DSRT_OK;
+    if (P > kMaxPtc || k_filter > kSelMax || max_count > 65535)  // outside the screen's envelope
+        return prefilter_general(Q, n_q, m_q, d, cents, k_c, post_off, post_docs, n_docs, P, k_filter, cand,
+                                 n_cand, as_stream(stream));
     const TcWs w = tc_ws_layout(n_q, m_q, k_c, n_docs, P);
     DSRT_REQUIRE(workspace != nullptr && ws_bytes >= w.total, DSRT_EINVAL,
                  "invalid parameter: prefilter workspace too small");

@@ -459,6 +459,19 @@ int topk_run(const TopkArgs &in, int64_t n_rows, cudaStream_t st) {
     return DSRT_OK;
 }
 
+// plain rows (id = element index) for internal callers without the header struct
+int topk_run_ext(const double *scores, int64_t ld, int64_t n, int k, double *out_s, uint64_t *out_id,
+                 int64_t n_rows, cudaStream_t st) {
+    TopkArgs a{};
+    a.scores = scores;
+    a.ld = ld;
+    a.n = n;
+    a.k = k;
+    a.out_s = out_s;
+    a.out_id = out_id;
+    return topk_run(a, n_rows, st);
+}
+
 }  // namespace dsrt
 
 using namespace dsrt;

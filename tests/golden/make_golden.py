@@ -327,11 +327,84 @@ def make_storage():
     np.savez_compressed(os.path.join(HERE, "storage.npz"), **out)
 
 
+ENVELOPE_SHAPES = [  # (L, C, m_q, n_sets, m_max): outside the register-blocked kernels
+    (32, 20, 32, 12, 40), (160, 5, 16, 10, 30), (40, 24, 8, 10, 25), (256, 3, 33, 8, 20),
+    (129, 17, 5, 9, 12)]
+
+
+def make_envelope():
+    """Shapes the reference accepts beyond the fast kernels' register envelope
+    (C up to 24, L > 128; lsh.py:17, 54-66), and the prefilter with probe > 32 and
+    k_filter > 16384 (prefilter.py:111-144)."""
+    rng = np.random.default_rng(4321)
+    out = {}
+    for n, (L, C, m_q, n_sets, m_max) in enumerate(ENVELOPE_SHAPES):
+        r = 1 << C
+        sizes = rng.integers(1, m_max + 1, size=n_sets)
+        hot = rng.integers(0, r, size=(L,))
+        codes = rng.integers(0, r, size=(int(sizes.sum()), L))
+        mask = rng.random(codes.shape) < 0.6
+        codes[mask] = np.broadcast_to(hot, codes.shape)[mask]
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        tables = [dessert.build_tiny_table(codes[off[i]:off[i + 1]], L, r) for i in range(n_sets)]
+        index = ref_index.DessertIndex(config=no_filter(d=4, C=C, L=L),
+                                       family=dessert.sample_srp_family(4, C, L, 0),
+                                       lookup=dessert.build_sim_lookup(C, L), sketches=tables,
+                                       doc_ids=rng.permutation(10 * n_sets)[:n_sets].astype(np.uint64),
+                                       sizes=sizes.astype(np.int64), filter=None)
+        qcodes = rng.integers(0, r, size=(3, m_q, L))
+        qm = rng.random(qcodes.shape) < 0.6
+        qcodes[qm] = np.broadcast_to(hot, qcodes.shape)[qm]
+        out[f"s{n}_shape"] = np.array([L, C, m_q])
+        out[f"s{n}_sizes"] = sizes
+        out[f"s{n}_codes"] = codes.astype(np.int32)
+        out[f"s{n}_qcodes"] = qcodes.astype(np.int32)
+        out[f"s{n}_doc_ids"] = index.doc_ids
+        out[f"s{n}_scores"] = np.stack([ref_scores(index, qc) for qc in qcodes])
+    out["n_shapes"] = np.array(len(ENVELOPE_SHAPES))
+    # vectors -> build_index -> query at such shapes
+    for n, (d, C, L, seed, n_sets, m_q, top_k) in enumerate([(16, 18, 20, 3, 25, 12, 6),
+                                                             (24, 4, 200, 5, 20, 20, 8)]):
+        sizes = rng.integers(1, 16, size=n_sets)
+        X = rng.standard_normal((int(sizes.sum()), d))
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        ids = rng.permutation(500)[:n_sets]
+        index = dessert.build_index([(int(ids[i]), X[off[i]:off[i + 1]]) for i in range(n_sets)],
+                                    no_filter(d=d, C=C, L=L, seed=seed))
+        Q = rng.standard_normal((2, m_q, d))
+        res = [dessert.query(index, q, top_k=top_k) for q in Q]
+        out[f"e{n}_shape"] = np.array([d, C, L, seed, top_k])
+        out[f"e{n}_sizes"] = sizes
+        out[f"e{n}_X"] = X
+        out[f"e{n}_ids"] = ids
+        out[f"e{n}_Q"] = Q
+        out[f"e{n}_top_ids"] = np.array([[d_ for d_, _ in r] for r in res])
+        out[f"e{n}_top_scores"] = np.array([[s for _, s in r] for r in res])
+    # prefilter: probe > 32 and k_filter > 16384 over 20,000 documents
+    d, k = 16, 96
+    docs = [rng.standard_normal((int(rng.integers(1, 6)), d)) for _ in range(20000)]
+    cents = ref_prefilter.train_centroids(np.concatenate(docs), k=k, iters=3, seed=5)
+    cindex = ref_prefilter.build_centroid_index(docs, cents)
+    out["pf_centroids"] = cents.vectors
+    out["pf_n_docs"] = np.array(len(docs))
+    out["pf_post_off"] = np.concatenate([[0], np.cumsum([len(p) for p in cindex.postings])])
+    out["pf_post_docs"] = np.concatenate(cindex.postings).astype(np.int64)
+    cases = []
+    for t, (m_q, probe, k_filter) in enumerate([(32, 40, 20000), (8, 96, 17000), (40, 33, 300),
+                                                (32, 4, 18000), (3, 200, 16385)]):
+        Q = rng.standard_normal((m_q, d))
+        out[f"pf_q{t}"] = Q
+        out[f"pf_r{t}"] = ref_prefilter.filter_candidates(cindex, cents, Q, probe, k_filter)
+        cases.append((probe, k_filter))
+    out["pf_cases"] = np.array(cases)
+    np.savez_compressed(os.path.join(HERE, "envelope.npz"), **out)
+
+
 if __name__ == "__main__":
     assert "reference" in dessert.__file__, dessert.__file__
     makers = {"lsh": make_lsh, "agg": make_agg, "small": make_small, "end_to_end": make_end_to_end,
               "prefilter": make_prefilter, "cfg0": make_cfg0, "kmeans": make_kmeans,
-              "storage": make_storage}
+              "storage": make_storage, "envelope": make_envelope}
     for name in (sys.argv[1:] or list(makers)):  # e.g. `make_golden.py agg` for one fixture
         makers[name]()
     print("golden vectors written to", HERE)
