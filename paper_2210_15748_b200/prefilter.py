@@ -1,12 +1,11 @@
 """Centroid prefilter -- drop-in for dessert.prefilter (reference: pkg/src/dessert/prefilter.py).
 
 ``filter_candidates`` (prefilter.py:111-144) runs on the GPU (K5,
-csrc/prefilter.cu).  Centroid training (prefilter.py:47-82) and the
-centroid->document postings (prefilter.py:85-108) are index-build setup:
-SURVEY.md marks train_centroids out of scope and the postings build as 8(f)
-row f1.  Both are done on the device here with float64 torch tensor ops
-(argmax/unique/sort plumbing, no CPU work), following the reference's
-algorithm and tie rules step by step.
+csrc/prefilter.cu).  Centroid training (prefilter.py:47-82, row f4) is K7
+(csrc/kmeans.cu) and the centroid->document postings (prefilter.py:85-108,
+row f1) are K6 (csrc/prefilter.cu assignment + csrc/postings.cu radix
+postings): native kernels following the reference's algorithm and tie rules
+step by step; torch tensors are only the buffers.
 """
 
 from __future__ import annotations
