@@ -219,6 +219,11 @@ __device__ __forceinline__ int min3(int a, int b, int c) {
     else return min(a, min(b, c));
 }
 
+#ifndef DSRT_SPLIT_UNROLL
+#define DSRT_SPLIT_UNROLL 4  // 4: cfg3 candidate scoring 1.377 -> 1.336 ms (2: less loop overhead per pair)
+#endif
+constexpr int kSplitUnroll = DSRT_SPLIT_UNROLL;  // split-lane pair loop unroll
+
 template <int K, int W>
 __device__ __forceinline__ void scan_split(const uint32_t (&q)[2][K * W], int (&rmin)[2],
                                            const uint32_t *xs, int nv) {
@@ -227,7 +232,7 @@ __device__ __forceinline__ void scan_split(const uint32_t (&q)[2][K * W], int (&
     const uint4 *x4 = reinterpret_cast<const uint4 *>(xs) + h * (R / 4);
     const int np = nv >> 1;  // full vector pairs; half h takes vector 2p + h
     int p = 0;
-#pragma unroll 2
+#pragma unroll kSplitUnroll
     for (; p + 2 <= np; p += 2) {
         uint4 xa[R / 4], xb[R / 4];
 #pragma unroll
@@ -632,21 +637,32 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     // one batch per 32 candidates instead of a dependent load chain per set.
     const int64_t *cand_row = cand ? cand + qset * cand_ld : nullptr;
     CandWin pwin;
-    // producer iterator (lane-uniform state; lane 0 issues the copies)
-    int64_t pe = e_lo, pv, pvend;
-    pwin.get(pe, e_hi, cand_row, set_off, n_sets, pv, pvend);
-    const bool pvalid0 = pvend >= 0;
-    if (!pvalid0) { pv = 0; pvend = 0; }
+    // producer iterator (lane-uniform state; lane 0 issues the copies).  The
+    // per-piece arithmetic is 32-bit -- candidate offset pk within the run and
+    // the vectors prem left in the current candidate; only the record address
+    // pv is 64-bit.
+    const int nrun = static_cast<int>(e_hi - e_lo);
+    int pk = 0, prem;
+    int64_t pv;
+    bool pvalid;
+    {
+        int64_t vb, ve;
+        pwin.get(e_lo, e_hi, cand_row, set_off, n_sets, vb, ve);
+        pvalid = ve >= 0;
+        pv = pvalid ? vb : 0;
+        prem = pvalid ? static_cast<int>(ve - vb) : 0;
+    }
     int issued = 0, consumed = 0, pb = 0;  // pb = issued % kBufs
-    bool pvalid = pvalid0;
     constexpr uint32_t kDone = 1u << 16, kValid = 1u << 17;
-    auto issue = [&]() -> uint32_t {  // next piece (pe, [pv, ..)) into buffer pb; returns its metadata
+    // The buffer being refilled was last read by this warp's LDS, complete before
+    // the __syncwarp that precedes every refill, so no proxy fence is needed for
+    // the bulk copy's write-after-read.
+    auto issue = [&]() -> uint32_t {  // next piece (pk, [pv, ..)) into buffer pb; returns its metadata
         const int b = pb;
         pb = pb + 1 == kBufs ? 0 : pb + 1;
-        const int64_t nvec = pe < e_hi ? tmin<int64_t>(PV, pvend - pv) : 0;
+        const int nvec = pk < nrun ? min(PV, prem) : 0;
         if (lane == 0) {
             const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);
-            fence_proxy_async_smem();
             if (bytes > 0) {
                 mbar_arrive_expect_tx(&bars[b], bytes);
                 bulk_g2s(bufs + b * (PV * R), recs + pv * R, bytes, &bars[b]);
@@ -656,14 +672,17 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         }
         ++issued;
         pv += nvec;
+        prem -= nvec;
         uint32_t meta = static_cast<uint32_t>(nvec);
-        if (pe < e_hi && pv >= pvend) {  // advance to the next candidate
+        if (pk < nrun && prem <= 0) {  // advance to the next candidate
             meta |= kDone | (pvalid ? kValid : 0u);
-            ++pe;
-            if (pe < e_hi) {
-                pwin.get(pe, e_hi, cand_row, set_off, n_sets, pv, pvend);
-                pvalid = pvend >= 0;
-                if (!pvalid) { pv = 0; pvend = 0; }
+            ++pk;
+            if (pk < nrun) {
+                int64_t vb, ve;
+                pwin.get(e_lo + pk, e_hi, cand_row, set_off, n_sets, vb, ve);
+                pvalid = ve >= 0;
+                pv = pvalid ? vb : 0;
+                prem = pvalid ? static_cast<int>(ve - vb) : 0;
             }
         }
         return meta;
@@ -672,13 +691,14 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     // producer recorded at issue time (meta[0] = the oldest outstanding
     // piece: nvec | kDone | kValid), so the per-piece bookkeeping is a
     // register rotation instead of a second walk over the candidate list.
-    int64_t ce = e_lo, slot_col = e_lo;
+    int ck = 0;  // consumed candidates of the run
+    int64_t slot_col = e_lo;
     uint32_t meta[kBufs];
 #pragma unroll
     for (int i = 0; i < kBufs; ++i) meta[i] = issue();
     int b = 0;
     uint32_t phase = 0;
-    while (ce < e_hi) {
+    while (ck < nrun) {
         mbar_wait(&bars[b], phase);
         const uint32_t m0 = meta[0];
         const int nvec = static_cast<int>(m0 & 0xffffu);
@@ -700,7 +720,7 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
                 slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
                 slot_col += 32;
             }
-            ++ce;
+            ++ck;
         }
         __syncwarp();
 #pragma unroll
