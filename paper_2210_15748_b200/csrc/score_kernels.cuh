@@ -96,6 +96,18 @@ struct Slots {
         ++n;
     }
 
+    // write slot row idx without touching the counters (exhaustive kernel: the
+    // QS query sets of a warp share one slot counter; every pushed set is valid)
+    __device__ __forceinline__ void put(const int (&rmin)[QPL], int L, int m_q, int idx) const {
+        const int lane = threadIdx.x & 31;
+        uint8_t *row = buf + idx * SlotGeom<QPL>::kRow;
+#pragma unroll
+        for (int s = 0; s < QPL; ++s) {
+            const int qi = lane + 32 * s;
+            if (qi < m_q) row[qi] = static_cast<uint8_t>(L - rmin[s]);
+        }
+    }
+
     // split-lane layout (QPL == 1): lanes l and l + 16 hold queries l and
     // l + 16 after the half-warp combine; lanes < 16 write both
     __device__ __forceinline__ void push_split(const int (&rmin)[2], int L, int m_q, bool ok) {
@@ -468,10 +480,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     int64_t s = s_lo, slot_col = s_lo - set_begin;
     int64_t s_end_v = win.get(s + 1);
     int64_t v = vbeg;
+    int nslot = 0;  // filled slot rows, shared by the QS query sets (all valid)
     auto flush_all = [&]() {
 #pragma unroll
         for (int j = 0; j < QS; ++j) {
             const int64_t qs = qset0 + j;
+            slots[j].n = nslot;
+            slots[j].valid = nslot == 32 ? 0xffffffffu : ((1u << nslot) - 1u);
             if (qs < n_qsets) {
                 if (app.tau != nullptr)
                     slots[j].flush_append(m_q, lut_s, w_s, app, qs, set_begin + slot_col);
@@ -486,14 +501,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     auto finish_set = [&]() {
 #pragma unroll
         for (int j = 0; j < QS; ++j)
-            slots[j].push(*reinterpret_cast<const int(*)[QPL]>(&rmin[j * QPL]), L, m_q, true);
+            slots[j].put(*reinterpret_cast<const int(*)[QPL]>(&rmin[j * QPL]), L, m_q, nslot);
 #pragma unroll
         for (int i = 0; i < S; ++i) rmin[i] = L;
         ++s;
-        if (slots[0].n == 32) {
+        if (++nslot == 32) {
             if (any_active) flush_all();
-#pragma unroll
-            for (int j = 0; j < QS; ++j) slots[j].n = 0;
+            nslot = 0;
             slot_col += 32;
         }
         if (s < s_hi) s_end_v = win.get(s + 1);
@@ -516,7 +530,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
         if (lane == 0) mbar_arrive(&empty[st]);
     }
     while (s < s_hi) finish_set();  // trailing empty sets (validated away upstream)
-    if (any_active && slots[0].n > 0) flush_all();
+    if (any_active && nslot > 0) flush_all();
 }
 
 // --------------------------------------------------------- candidate lists
@@ -745,7 +759,10 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
                       const uint32_t *qrecs, int64_t n_qsets, int m_q, int L, const double *lut,
                       const double *weights, double *scores, int64_t ld, uint16_t *mc,
                       int mc_stride, int mc_q0, const AppendOut &app, cudaStream_t st) {
-    constexpr int NW = 8;
+#ifndef DSRT_ALL_NW
+#define DSRT_ALL_NW 8
+#endif
+    constexpr int NW = DSRT_ALL_NW;  // consumer warps per CTA (+1 producer warp)
     const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1 + m_q) * sizeof(double);
     auto kern = score_all_kernel<K, W, QPL, NW, QS>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
