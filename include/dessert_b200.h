@@ -124,6 +124,9 @@ int dsrt_collision_counts(const int32_t *offsets, const int32_t *ids, int L, int
  *   scores[q * cand_ld + e].
  * maxcounts (may be NULL): uint16 c_q at [(q * ld_or_cand_ld + e) * m_q + qi].
  * qrecords: (n_qsets, m_q, R) plane records of the query codes.
+ * Any C <= 24 and L: shapes outside the register-blocked kernels (C > 16 or
+ * C * ceil(L/32) > 32) are scored by the general kernel (same bytes); maxcounts
+ * must be NULL for them (DSRT_EUNSUPPORTED otherwise).
  */
 int dsrt_score_all(const uint32_t *records, const int64_t *set_off, int64_t set_begin,
                    int64_t set_end, const uint32_t *qrecords, int64_t n_qsets, int m_q, int L,
@@ -210,7 +213,9 @@ int dsrt_search_profile_read(double *score_ms, double *other_ms, int64_t *launch
  * Q: (n_qsets * m_q, d) float64 query vectors; centroids (k_c, d) float64.
  * postings CSR: post_off (k_c + 1), post_docs (ascending doc indices).
  * Output per query set: cand[q * k_filter + e] (count desc, index asc) and
- * n_cand[q].  workspace from dsrt_prefilter_workspace.
+ * n_cand[q].  workspace from dsrt_prefilter_workspace.  Any probe and k_filter:
+ * probe > 32, k_filter > 16384 or m_q * probe > 65535 run a general path
+ * (float64 sims + K4 selections, temporaries allocated stream-ordered).
  */
 int dsrt_prefilter(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
                    int64_t k_c, const int64_t *post_off, const int64_t *post_docs, int64_t n_docs,
@@ -227,7 +232,7 @@ size_t dsrt_prefilter_workspace(int64_t n_qsets, int m_q, int64_t k_c, int64_t n
  * collects them instead when the chunk-maximum buffer would exceed 1 GB).  The
  * kept centroids are re-ranked in float64 (ties -> lower centroid id); rows with
  * more than 32 fall back to the exact float64 scan.  Selection as
- * dsrt_prefilter.  d = 128, probe <= 12.
+ * dsrt_prefilter.  d = 128; probe > 12 or k_filter > 16384 take the general path.
  */
 int dsrt_prefilter_tc(const double *Q, int64_t n_qsets, int m_q, int d, const double *centroids,
                       const void *centroids_f16, double cent_max_norm, int64_t k_c,

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2; do
-python tools/prof_score.py --sets 1000000 --qsets 256 --L 32 --C 7 --mode cand --cand 4096 --reps 5 >> gpurun_out/pc2.log 2>&1
-DSRT_LIB=paper_2210_15748_b200/csrc/libdessert_U4.so python tools/prof_score.py --sets 1000000 --qsets 256 --L 32 --C 7 --mode cand --cand 4096 --reps 5 >> gpurun_out/pc2.log 2>&1
-done
+export PYTORCH_NO_CUDA_MEMORY_CACHING=1
+timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "small or golden or agg or prefilter or tinytable or layout or hash_golden or cfg0" > gpurun_out/san1.log 2>&1; echo EXIT=$? >> gpurun_out/san1.log
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_envelope.py tests/test_gpu_search.py -m gpu -x -q -k "not concurrent" > gpurun_out/san2.log 2>&1; echo EXIT=$? >> gpurun_out/san2.log
