@@ -198,6 +198,37 @@ def test_two_shards_merge_equals_single_index():
     assert _rows(ms, mi) == want_o
 
 
+def test_sharded_query_batch_nccl_one_rank():
+    """The product multi-GPU function end to end on the GPU: a 1-rank NCCL process
+    group (the only one a single GPU allows), sharded_query_batch = local query_batch
+    + NCCL all-gather + K4 merge, equals query_batch on the same index."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2210_15748_b200.distributed import sharded_query_batch
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    rng = np.random.default_rng(3)
+    sizes = rng.integers(4, 60, size=3000)
+    X = rng.standard_normal((int(sizes.sum()), 32)).astype(np.float32)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    docs = [(int(i) * 7, X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+    idx = d.build_index(docs, d.IndexConfig(d=32, C=6, L=32, seed=1, filter=d.FilterConfig(enabled=False)))
+    Q = torch.from_numpy(rng.standard_normal((9, 16, 32)).astype(np.float32)).cuda()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        ms, mi = sharded_query_batch(idx, Q, 25)
+        ws, wi = d.query_batch(idx, Q, 25, return_tensors=True)
+        assert torch.equal(ms, ws) and torch.equal(mi, wi)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_add_sets_failure_leaves_index_unchanged():
     rng = np.random.default_rng(4)
     docs = [(i, rng.standard_normal((int(rng.integers(1, 20)), 8))) for i in range(40)]
