@@ -458,6 +458,17 @@ def run_scoring(args, workload):
         r = _cpu_scoring_baseline(workload, args.cpu_sets, 8, 2, 1)
         line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"],
                                 "kind": r["kind"], "sample": r["sample"]}
+    if rank == 0 and world == 1 and workload == 4 and not args.no_extra:
+        # the prefilter pipeline (cfg3) measured in the same run: batch-256 query sets/s,
+        # batch-1 p50/p99 through query(), e2e through query_batch (its own line, with the
+        # CPU reference, comes from --config 3)
+        del idx
+        torch.cuda.empty_cache()
+        c3 = cfg3_line(argparse.Namespace(**dict(vars(args), sets=0, steps=20, warmup=5,
+                                                 no_cpu_baseline=True)))
+        line["cfg3"] = {k: c3[k] for k in ("metric", "value", "unit", "ms_per_step", "batch1_latency_ms",
+                                          "e2e", "kernel_ms", "clocks")}
+        line["cfg3"]["roofline"] = {k: c3["roofline"][k] for k in ("bound", "kernel", "frac", "achieved", "peak", "unit")}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -515,6 +526,11 @@ def _clocks_and_time(step_fn, steps, warmup, local, stream):
 
 
 def run_cfg3(args):
+    print(json.dumps(cfg3_line(args)))
+    return 0
+
+
+def cfg3_line(args):
     """cfg3: 1M sets (~70M fp16 vectors) from 65,536 centroids; prefilter probe 4,
     k_filter 4,096; L=32, C=7; top-100.  Batch 256 throughput + batch-1 p50/p99."""
     import torch
@@ -690,8 +706,7 @@ def run_cfg3(args):
             line["cpu_baseline"] = {"value": r["value"], "unit": r["unit"], "cores": r["cores"],
                                     "kind": r["kind"], "sample": r["sample"],
                                     "per_query_set_s": r["per_query_set_s"], "setup_s": r["setup_s"]}
-    print(json.dumps(line))
-    return 0
+    return line
 
 
 def run_cfg2(args):
@@ -821,6 +836,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="cfg4: skip the cfg3 measurements in the line")
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
     ap.add_argument("--vectors", type=int, default=0, help="override cfg2 vector count")
     ap.add_argument("--sets", type=int, default=0, help="override N (cfg1/3/4)")
