@@ -469,6 +469,15 @@ def run_scoring(args, workload):
         line["cfg3"] = {k: c3[k] for k in ("metric", "value", "unit", "ms_per_step", "batch1_latency_ms",
                                           "e2e", "kernel_ms", "clocks")}
         line["cfg3"]["roofline"] = {k: c3["roofline"][k] for k in ("bound", "kernel", "frac", "achieved", "peak", "unit")}
+        del c3
+        torch.cuda.empty_cache()
+        # index build (cfg2): hash + layout of 10M bf16 vectors, with its sampled hash flip rate
+        c2 = cfg2_line(argparse.Namespace(**dict(vars(args), vectors=0, steps=20, warmup=5,
+                                                 no_cpu_baseline=True)))
+        line["cfg2"] = {k: c2[k] for k in ("metric", "value", "unit", "ms_per_step", "e2e", "hash_bit_flips",
+                                          "clocks")}
+        line["cfg2"]["roofline"] = {k: c2["roofline"][k] for k in ("bound", "kernel", "frac", "achieved", "peak",
+                                                                   "unit", "mma_frac")}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -710,6 +719,11 @@ def cfg3_line(args):
 
 
 def run_cfg2(args):
+    print(json.dumps(cfg2_line(args)))
+    return 0
+
+
+def cfg2_line(args):
     """cfg2: index build of 10M bf16 unit vectors (cfg1 mixture, cfg1 set sizes): hash
     (tcgen05, bf16 hi/lo planes, fused sign/pack -> codes + plane records) + CSR layout."""
     import torch
@@ -825,8 +839,7 @@ def run_cfg2(args):
         r = BR.build_baseline(L=L, C=C)
         line["cpu_baseline"] = {"value": r["value"], "unit": "vectors/s", "cores": r["cores"],
                                 "kind": r["kind"], "sample": r["sample"]}
-    print(json.dumps(line))
-    return 0
+    return line
 
 
 def main():
