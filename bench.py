@@ -464,7 +464,7 @@ def run_scoring(args, workload):
         # CPU reference, comes from --config 3)
         del idx
         torch.cuda.empty_cache()
-        c3 = cfg3_line(argparse.Namespace(**dict(vars(args), sets=0, steps=20, warmup=5,
+        c3 = cfg3_line(argparse.Namespace(**dict(vars(args), sets=0, steps=200, warmup=5,
                                                  no_cpu_baseline=True)))
         line["cfg3"] = {k: c3[k] for k in ("metric", "value", "unit", "ms_per_step", "batch1_latency_ms",
                                           "e2e", "kernel_ms", "clocks")}
@@ -472,7 +472,7 @@ def run_scoring(args, workload):
         del c3
         torch.cuda.empty_cache()
         # index build (cfg2): hash + layout of 10M bf16 vectors, with its sampled hash flip rate
-        c2 = cfg2_line(argparse.Namespace(**dict(vars(args), vectors=0, steps=20, warmup=5,
+        c2 = cfg2_line(argparse.Namespace(**dict(vars(args), vectors=0, steps=100, warmup=5,
                                                  no_cpu_baseline=True)))
         line["cfg2"] = {k: c2[k] for k in ("metric", "value", "unit", "ms_per_step", "e2e", "hash_bit_flips",
                                           "clocks")}
