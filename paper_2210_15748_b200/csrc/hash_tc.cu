@@ -21,6 +21,8 @@
 //   warp 1: MMA issuer (one thread, 8 K-steps x parts per tile),
 //   warps 2-5: epilogue (TMEM -> registers -> sign bits -> codes + plane
 //              records), TMEM double-buffered so it overlaps the next MMAs.
+#include <cstdlib>
+
 #include "tc_common.cuh"
 
 namespace dsrt {
@@ -34,6 +36,7 @@ struct HashTcParams {
     void *codes_out;          // uint8 (n, L)   (C <= 8)
     uint32_t *recs_out;       // (n, R)
     uint32_t *zero_rows;
+    int mc;  // > 1: the `groups` CTAs of a cluster share every X tile by TMA multicast
 };
 
 template <int PARTS, int C, int kHStages>
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         tma_prefetch(&map_w);
         for (int s = 0; s < kHStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], p.mc > 1 ? p.mc : 1);  // multicast: every CTA's MMA frees the stage
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -73,8 +76,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
     if (warp == 1) tmem_alloc(&tmem_base, 512);
     tc_fence_before();
     __syncthreads();
+    if (p.mc > 1) cluster_sync_all();  // peers' barriers are initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = tmem_base;
+    const uint16_t cmask = static_cast<uint16_t>((1u << p.mc) - 1u);
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -90,9 +95,15 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 const int st = it % kHStages;
                 if (it >= kHStages) mbar_wait(&empty[st], ((it / kHStages) - 1) & 1);
                 mbar_arrive_expect_tx(&full[st], kTileA);
-                tma_load_2d(sa + st * kTileA, &map_x, 0, static_cast<int>(tile * 128), &full[st]);
-                tma_load_2d(sa + st * kTileA + 128 * 128, &map_x, 64, static_cast<int>(tile * 128),
-                            &full[st]);
+                if (p.mc > 1) {  // X read once: CTA (group) g multicasts the 64-column boxes kb = g mod G
+                    for (int kb = group; kb < 2; kb += p.mc)
+                        tma_load_2d_mc(sa + st * kTileA + kb * 128 * 128, &map_x, kb * 64,
+                                       static_cast<int>(tile * 128), &full[st], cmask);
+                } else {
+                    tma_load_2d(sa + st * kTileA, &map_x, 0, static_cast<int>(tile * 128), &full[st]);
+                    tma_load_2d(sa + st * kTileA + 128 * 128, &map_x, 64, static_cast<int>(tile * 128),
+                                &full[st]);
+                }
             }
         }
     } else if (warp == 1) {
@@ -114,7 +125,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         for (int k = 0; k < 4; ++k)
                             umma_f16(d, ad + 2 * k, bd + 2 * k, idesc, (part | kb | k) != 0);
                     }
-                umma_commit(&empty[st]);
+                if (p.mc > 1)
+                    umma_commit_mc(&empty[st], cmask);
+                else
+                    umma_commit(&empty[st]);
                 umma_commit(&tfull[acc]);
             }
         }
@@ -198,6 +212,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (p.mc > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -267,7 +282,11 @@ int hash_tc(const void *X, int x_dtype, int64_t n, int d, const void *planes, in
         cudaFreeAsync(pp, st);
         return rc;
     }
-    HashTcParams hp{n, L, C, groups, n_pad, parts, codes_out, records_out, zero_rows};
+    // X tiles are shared by the groups' CTAs through a cluster + TMA multicast (each X
+    // byte read from HBM once); DSRT_HASH_MC=0 restores independent loads (A/B timing)
+    const char *mce = getenv("DSRT_HASH_MC");
+    const int mc = (groups >= 2 && groups <= 8 && !(mce && mce[0] == '0')) ? groups : 1;
+    HashTcParams hp{n, L, C, groups, n_pad, parts, codes_out, records_out, zero_rows, mc};
     const size_t b_bytes = static_cast<size_t>(parts) * 2 * n_pad * 128;
     const int stages = (1024 + 3 * 2 * 128 * 128 + b_bytes <= 227 * 1024) ? 3 : 2;
     const size_t smem = 1024 + stages * 2 * 128 * 128 + b_bytes;
@@ -287,7 +306,23 @@ static int launch_hash_tc(const CUtensorMap &mx, const CUtensorMap &mw, const Ha
                           uint32_t idesc, size_t smem, int ctas, cudaStream_t st) {
     auto kern = hash_tc_kernel<PARTS, C, STAGES>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<ctas, kHThreads, smem, st>>>(mx, mw, hp, idesc);
+    if (hp.mc > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+        cfg.blockDim = dim3(kHThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = static_cast<unsigned>(hp.mc);
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DSRT_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mw, hp, idesc));
+    } else {
+        kern<<<ctas, kHThreads, smem, st>>>(mx, mw, hp, idesc);
+    }
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
