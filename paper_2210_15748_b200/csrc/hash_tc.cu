@@ -171,18 +171,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 }
             }
             any_nonzero &= 0x7fffffffu;
-            if (p.codes_out) {  // u8 codes: spread 4 plane bits into 4 bytes per step
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    uint32_t w = 0;
-#pragma unroll
-                    for (int b = 0; b < C; ++b) {
-                        const uint32_t y = (plane[b] >> (4 * k)) & 0xfu;
-                        w |= ((y * 0x00204081u) & 0x01010101u) << b;
-                    }
-                    codes_w[k] = w;
-                }
-            }
+            if (p.codes_out) codes_from_planes<C>(plane, codes_w);  // 8x8 bit transposes
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);

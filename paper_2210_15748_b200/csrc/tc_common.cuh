@@ -131,4 +131,35 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// u8 codes of the 32 tables of a group from its C plane words (bit t of word b =
+// bit b of table t's code): per 8 tables, bytes of the planes gathered by byte
+// permutes into an 8x8 bit matrix, transposed in registers (Hacker's Delight
+// transpose8) -> out[2m] = codes of tables 8m..8m+3, out[2m+1] = 8m+4..8m+7.
+template <int C>
+__device__ __forceinline__ void codes_from_planes(const uint32_t (&P)[C], uint32_t (&out)[8]) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t sel = m | ((4 + m) << 4);
+        uint32_t b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) b[i] = i < C ? P[i < C ? i : 0] : 0u;
+        uint32_t x = __byte_perm(__byte_perm(b[0], b[1], sel), __byte_perm(b[2], b[3], sel), 0x5410);
+        uint32_t y = C > 4 ? __byte_perm(__byte_perm(b[4], b[5], sel), __byte_perm(b[6], b[7], sel), 0x5410)
+                           : 0u;
+        uint32_t t;
+        t = (x ^ (x >> 7)) & 0x00AA00AAu;
+        x = x ^ t ^ (t << 7);
+        t = (x ^ (x >> 14)) & 0x0000CCCCu;
+        x = x ^ t ^ (t << 14);
+        if (C > 4) {
+            t = (y ^ (y >> 7)) & 0x00AA00AAu;
+            y = y ^ t ^ (t << 7);
+            t = (y ^ (y >> 14)) & 0x0000CCCCu;
+            y = y ^ t ^ (t << 14);
+        }
+        out[2 * m] = ((y & 0x0F0F0F0Fu) << 4) | (x & 0x0F0F0F0Fu);
+        out[2 * m + 1] = ((x >> 4) & 0x0F0F0F0Fu) | (y & 0xF0F0F0F0u);
+    }
+}
+
 }  // namespace dsrt

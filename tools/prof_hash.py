@@ -19,6 +19,7 @@ ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--L", type=int, default=64)
 ap.add_argument("--C", type=int, default=7)
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--no-codes", action="store_true", help="records only (no u8 codes output)")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 dt = torch.bfloat16 if a.dtype == "bf16" else torch.float16
@@ -26,15 +27,15 @@ X, _ = workloads.gpu_mixture(a.n, 4096, 128, 0.05, seed=601, dtype=dt, device=de
 fam = d.sample_srp_family(128, a.C, a.L, 0)
 planes = fam.device_planes(a.mode, dev)
 for _ in range(3):
-    engine.hash_vectors(X, planes, a.mode, a.L, a.C, check_zero=False)
+    engine.hash_vectors(X, planes, a.mode, a.L, a.C, want_codes=not a.no_codes, check_zero=False)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(a.reps):
-    engine.hash_vectors(X, planes, a.mode, a.L, a.C, check_zero=False)
+    engine.hash_vectors(X, planes, a.mode, a.L, a.C, want_codes=not a.no_codes, check_zero=False)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.reps
 fl = 2.0 * 128 * a.L * a.C * a.n
-print(f"lib={os.environ.get('DSRT_LIB', 'default')} mode={a.mode} dtype={a.dtype} n={a.n} "
+print(f"lib={os.environ.get('DSRT_LIB', 'default')} mode={a.mode} dtype={a.dtype} n={a.n} codes={not a.no_codes} "
       f"ms={ms:.3f} alg_TFLOPs={fl / ms / 1e9:.1f}")
