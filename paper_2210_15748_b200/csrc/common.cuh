@@ -106,6 +106,27 @@ __device__ __forceinline__ void bulk_g2s_keep(void *smem_dst, const void *gmem_s
         "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// Multicast variant: the bytes land at dst's offset in every CTA of `mask` (this
+// cluster) and complete_tx on each one's barrier at bar's offset.
+__device__ __forceinline__ void bulk_g2s_keep_mc(void *smem_dst, const void *gmem_src, uint32_t bytes,
+                                                 uint64_t *bar, uint64_t policy, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+        : "memory");
+}
+// arrive on the barrier at bar's offset in cluster CTA `rank` (release, cluster scope)
+__device__ __forceinline__ void mbar_arrive_rank(uint64_t *bar, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_threads() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));

@@ -21,6 +21,8 @@
 // into one set score (LUT + numpy pairwise order) -- the float64 epilogue is
 // thus spread over lanes instead of being a warp-wide reduction per set.
 #pragma once
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dsrt {
@@ -396,7 +398,13 @@ constexpr size_t all_smem_static() {
 // chunk's plane records through a kStages ring with cp.async.bulk (TMA);
 // NW consumer warps share every tile, each register-blocking QS query sets
 // (lane l holds query l of each), so one broadcast LDS feeds QS pairs.
-template <int K, int W, int QPL, int NW, int QS>
+//
+// CL = 2: the grid's x (query-set groups) is clustered in pairs that score the same
+// chunk; every record tile is fetched once per pair -- tile t by CTA t % 2 with a
+// multicast bulk copy into both CTAs' ring -- and each consumer warp releases the
+// stage on both CTAs' barriers (count NW * CL), so each record byte crosses the L2
+// -> SM path once per pair instead of twice.
+template <int K, int W, int QPL, int NW, int QS, int CL = 1>
 __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     score_all_kernel(const uint32_t *__restrict__ recs, const int64_t *__restrict__ set_off,
                      int64_t set_begin, int64_t set_end, const uint32_t *__restrict__ qrecs,
@@ -429,17 +437,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
                                           : set_begin + lower_bound_i64(set_off + set_begin, nset, t_hi);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NW);
+            mbar_init(&empty[s], NW * CL);
         }
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i <= L; i += blockDim.x) lut_s[i] = __ldg(lut + i);
     for (int i = threadIdx.x; i < m_q; i += blockDim.x) w_s[i] = weights ? __ldg(weights + i) : 1.0;
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync_threads();  // peers' barriers exist before any multicast
     const int64_t s_lo = bounds[0], s_hi = bounds[1];
-    if (s_lo >= s_hi) return;
+    if (s_lo >= s_hi) return;  // the whole cluster (same chunk) leaves together
     const int64_t vbeg = __ldg(set_off + s_lo), vend = __ldg(set_off + s_hi);
     const int64_t n_tiles = (vend - vbeg + kTileVec - 1) / kTileVec;
+    [[maybe_unused]] const uint32_t crank = CL > 1 ? static_cast<uint32_t>(blockIdx.x % CL) : 0u;
 
     if (warp == NW) {  // ---------------- producer
         if (lane == 0) {
@@ -452,8 +462,18 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
                 const int64_t nvec = tmin<int64_t>(kTileVec, vend - tv0);
                 const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);
                 mbar_arrive_expect_tx(&full[st], bytes);
-                bulk_g2s_keep(tiles + st * (kTileVec * R), recs + tv0 * R, bytes, &full[st], pol);
+                if constexpr (CL > 1) {
+                    if (static_cast<uint32_t>(t % CL) == crank)
+                        bulk_g2s_keep_mc(tiles + st * (kTileVec * R), recs + tv0 * R, bytes, &full[st], pol,
+                                         static_cast<uint16_t>((1u << CL) - 1u));
+                } else {
+                    bulk_g2s_keep(tiles + st * (kTileVec * R), recs + tv0 * R, bytes, &full[st], pol);
+                }
             }
+        }
+        if constexpr (CL > 1) {
+            __syncwarp();  // the .aligned cluster barrier needs the whole warp converged
+            cluster_sync_threads();  // stay until the peers are done with our ring
         }
         return;
     }
@@ -527,10 +547,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
             while (s < s_hi && v == s_end_v) finish_set();
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        if (lane == 0) {
+            if constexpr (CL > 1) {
+#pragma unroll
+                for (int r = 0; r < CL; ++r) mbar_arrive_rank(&empty[st], static_cast<uint32_t>(r));
+            } else {
+                mbar_arrive(&empty[st]);
+            }
+        }
     }
     while (s < s_hi) finish_set();  // trailing empty sets (validated away upstream)
     if (any_active && nslot > 0) flush_all();
+    if constexpr (CL > 1) {
+        __syncwarp();
+        cluster_sync_threads();
+    }
 }
 
 // --------------------------------------------------------- candidate lists
@@ -764,9 +795,16 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
 #endif
     constexpr int NW = DSRT_ALL_NW;  // consumer warps per CTA (+1 producer warp)
     const size_t smem = all_smem_static<K, W, QPL, NW, QS>() + (L + 1 + m_q) * sizeof(double);
-    auto kern = score_all_kernel<K, W, QPL, NW, QS>;
+    // query-set groups in cluster pairs sharing each record tile: opt-in (DSRT_ALL_CLUSTER=1).
+    // Measured at cfg4 shape (1M sets x 1024 query sets): L2 -> SM bytes 88 -> 59 GB, DRAM
+    // reads unchanged (2.88 -> 2.84 GB), kernel 1.176 -> 1.193 s -- the pairing costs more
+    // than it saves in this INT-bound kernel, so it is off by default.
+    const char *ce = getenv("DSRT_ALL_CLUSTER");
+    const bool pair = (ce && ce[0] == '1') && n_qsets > NW * QS;
+    auto kern = pair ? score_all_kernel<K, W, QPL, NW, QS, 2> : score_all_kernel<K, W, QPL, NW, QS, 1>;
     DSRT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t groups = (n_qsets + NW * QS - 1) / (NW * QS);
+    int64_t groups = (n_qsets + NW * QS - 1) / (NW * QS);
+    if (pair) groups += groups & 1;  // whole pairs (an extra CTA with no query sets still streams)
     int occ = 0;
     DSRT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (NW + 1) * 32, smem));
     occ = occ < 1 ? 1 : occ;
@@ -777,9 +815,26 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
     chunks = tmin<int64_t>(chunks, 65535);
     dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(chunks));
     DSRT_REQUIRE(groups < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many query sets");
-    kern<<<grid, (NW + 1) * 32, smem, st>>>(recs, set_off, sb, se, qrecs, n_qsets, m_q, L, lut,
-                                           weights, scores, ld, mc, mc_stride, mc_q0,
-                                           static_cast<int>(chunks), app);
+    if (pair) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3((NW + 1) * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DSRT_CUDA(cudaLaunchKernelEx(&cfg, kern, recs, set_off, sb, se, qrecs, n_qsets, m_q, L, lut, weights,
+                                     scores, ld, mc, mc_stride, mc_q0, static_cast<int>(chunks), app));
+    } else {
+        kern<<<grid, (NW + 1) * 32, smem, st>>>(recs, set_off, sb, se, qrecs, n_qsets, m_q, L, lut,
+                                               weights, scores, ld, mc, mc_stride, mc_q0,
+                                               static_cast<int>(chunks), app);
+    }
     DSRT_LAUNCH_CHECK();
     return DSRT_OK;
 }
