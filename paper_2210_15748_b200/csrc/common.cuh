@@ -88,6 +88,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+// Wait with a suspend-time hint: the warp is descheduled until the phase completes
+// (or the hint expires) instead of re-issuing try_wait -- for producer warps that
+// run ahead of ALU-bound consumers and would otherwise spin on a free-slot barrier.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+    } while (!ok);
+}
 // 1-D bulk async copy global -> shared (TMA engine), completes on `bar`.
 __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes,
                                          uint64_t *bar) {

@@ -457,7 +457,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
             for (int64_t t = 0; t < n_tiles; ++t) {
                 const int st = static_cast<int>(t % kStages);
                 const uint32_t n = static_cast<uint32_t>(t / kStages);
-                if (t >= kStages) mbar_wait(&empty[st], (n - 1) & 1);
+                if (t >= kStages) mbar_wait_suspend(&empty[st], (n - 1) & 1);
                 const int64_t tv0 = vbeg + t * kTileVec;
                 const int64_t nvec = tmin<int64_t>(kTileVec, vend - tv0);
                 const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);

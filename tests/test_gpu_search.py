@@ -73,6 +73,25 @@ def test_search_threshold_equals_materialised_and_oracle(L, C, m_q, k, monkeypat
     assert d.query_codes_batch(idx, q, k) == want
 
 
+@pytest.mark.parametrize("n_q", [70, 128])
+def test_search_cluster_pairs_opt_in(n_q, monkeypatch):
+    """The opt-in cluster-pair mode of the exhaustive kernel (record tiles multicast to
+    both CTAs of a pair; 70 query sets = 3 groups padded to 4, one CTA without query
+    sets) returns the same ranking as the oracle, threshold and materialised."""
+    monkeypatch.setenv("DSRT_SEARCH_MIN_BYTES", "0")
+    monkeypatch.setenv("DSRT_ALL_CLUSTER", "1")
+    L, C, m_q, k = 32, 8, 32, 20
+    sizes, off, codes, q, ids = _case(n_q, 9000, L, C, n_q, m_q)
+    idx = _index(codes, sizes, L, C, ids)
+    want, _ = _want(codes, off, q, idx.lookup.table, ids, k)
+    qrecs, _ = engine.codes_to_records(torch.from_numpy(q.reshape(-1, L)).to(DEV), L, C)
+    args = (idx.records, idx.set_off, idx.doc_ids_dev, qrecs, m_q, L, C, idx.lut_dev, k)
+    for mode in (0, 1):
+        s, i, ovf = engine.search_all(*args, mode=mode, score_buffer_bytes=4 << 30)
+        assert int(ovf.item()) == 0
+        assert _rows(s, i) == want, mode
+
+
 def test_search_overflow_falls_back_exactly(monkeypatch):
     """Sets ordered by ascending score: the seed threshold admits nearly every later
     set, the survivor lists overflow, the flag is raised and rank_records reruns
