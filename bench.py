@@ -472,7 +472,9 @@ def run_scoring(args, workload):
         del c3
         torch.cuda.empty_cache()
         # index build (cfg2): hash + layout of 10M bf16 vectors, with its sampled hash flip rate
-        c2 = cfg2_line(argparse.Namespace(**dict(vars(args), vectors=0, steps=100, warmup=5,
+        # 20 steps as in the driver's runs: 100 back-to-back steps of this tensor-heavy kernel
+        # reach the power cap (sw_power_cap; 1.86 vs 1.62 ms per step measured)
+        c2 = cfg2_line(argparse.Namespace(**dict(vars(args), vectors=0, steps=20, warmup=5,
                                                  no_cpu_baseline=True)))
         line["cfg2"] = {k: c2[k] for k in ("metric", "value", "unit", "ms_per_step", "e2e", "hash_bit_flips",
                                           "clocks")}

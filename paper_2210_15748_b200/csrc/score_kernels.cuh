@@ -810,7 +810,12 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
     occ = occ < 1 ? 1 : occ;
     const int64_t nset = se - sb;
     // ~8 waves of CTAs; each chunk keeps >= 64 sets so tile pipelines stay full
-    int64_t chunks = (8LL * sm_count() * occ + groups - 1) / groups;
+#ifndef DSRT_ALL_WAVES
+#define DSRT_ALL_WAVES 8
+#endif
+    int64_t waves = DSRT_ALL_WAVES;
+    if (const char *e = getenv("DSRT_ALL_WAVES")) waves = tmax(1, atoi(e));  // tuning knob
+    int64_t chunks = (waves * sm_count() * occ + groups - 1) / groups;
     chunks = tmax<int64_t>(1, tmin<int64_t>(chunks, (nset + 63) / 64));
     chunks = tmin<int64_t>(chunks, 65535);
     dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(chunks));
