@@ -129,7 +129,7 @@ constexpr size_t avg_smem_static() {
 }
 
 template <int K, int W>
-__global__ void __launch_bounds__(kCandWarps * 32, 2)
+__global__ void __launch_bounds__(kCandWarps * 32, 16 / kCandWarps)
     score_avg_kernel(const AvgArgs a, int64_t run_len, int64_t runs_per_q) {
     constexpr int R = ((K * W) + 3) & ~3;
     constexpr int PV = piece_vec<K, W>();

@@ -573,7 +573,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
 #endif
 constexpr int kPieceBytes = DSRT_PIECE_BYTES;  // per-warp staging piece
 constexpr int kBufs = DSRT_CAND_BUFS;          // per-warp ring depth
-constexpr int kCandWarps = 8;
+#ifndef DSRT_CAND_WARPS
+#define DSRT_CAND_WARPS 8
+#endif
+constexpr int kCandWarps = DSRT_CAND_WARPS;       // warps per candidate-mode CTA (16 warps per SM)
 
 // Candidate-mode pieces: 4 KB when one query vector per lane (the smallest slot
 // rows) still fits 2 CTAs per SM -- fewer, larger pieces cut the per-piece ring
@@ -623,7 +626,7 @@ struct CandWin {
 // candidates' records through a private kBufs-deep ring filled by
 // cp.async.bulk issued from lane 0.
 #ifndef DSRT_CAND_MINB
-#define DSRT_CAND_MINB 2
+#define DSRT_CAND_MINB (16 / DSRT_CAND_WARPS)
 #endif
 #ifndef DSRT_CAND_WAVES
 #define DSRT_CAND_WAVES 4  // candidate-mode grid: waves of warps (sets the run length)
