@@ -16,18 +16,33 @@
 // b*32 + t = bit b of table t, so one 32-column TMEM load is one plane word;
 // the planes are permuted into that order per call).  CTA c handles
 // group c % G for the 128-row tiles c/G, c/G + n_cta/G, ...  -- consecutive
-// CTAs share each X tile through L2.  Warp roles (192 threads):
+// CTAs share each X tile through L2.  Warp roles (320 threads):
 //   warp 0: TMA producer (3-stage ring of X tiles, planes loaded once),
 //   warp 1: MMA issuer (one thread, 8 K-steps x parts per tile),
 //   warps 2-5: epilogue (TMEM -> registers -> sign bits -> codes + plane
-//              records), TMEM double-buffered so it overlaps the next MMAs.
+//              records), TMEM double-buffered so it overlaps the next MMAs; the
+//              load of plane word b + 1 is in flight while word b is packed.
+//              The planes are stored negated, so the accumulator's sign bit is
+//              the hash bit (one funnel shift per value).
+// Measured bounds at cfg2 (10M bf16 rows, codes + records): 1.60 ms; the MMA/TMA
+// pipeline alone (no accumulator read-out) 1.42-1.49 ms at the ~1.4 GHz the SMs
+// hold under this tensor load, so the kernel is tensor-bound on its two chains.
+// One chain with the same epilogue (timing build DSRT_HASH_EXP_PARTS1, wrong
+// bits) takes 1.37 ms: reading 128 x 32C fp32 accumulators out of TMEM and the
+// bit transposes then pace it, so halving the MMA work cannot halve the time.
+// A second epilogue warp set on alternate tiles (DSRT_HASH_ESETS=2) is slower
+// (1.84 ms: 10 warps cap the kernel at 168 registers and it spills).
 #include <cstdlib>
 
 #include "tc_common.cuh"
 
 namespace dsrt {
 
-constexpr int kHThreads = 192;
+#ifndef DSRT_HASH_ESETS
+#define DSRT_HASH_ESETS 1  // 2 (measured): 10 warps cap the kernel at 168 registers, it spills, 1.60 -> 2.20 ms
+#endif
+constexpr int kHESets = DSRT_HASH_ESETS;         // epilogue warp sets (4 warps each)
+constexpr int kHThreads = 64 + 128 * kHESets;
 
 struct HashTcParams {
     int64_t n_rows;
@@ -117,7 +132,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc * 256;
-                for (int part = 0; part < PARTS; ++part)
+#ifdef DSRT_HASH_EXP_PARTS1  // timing experiment only (wrong bits): one MMA chain instead of hi + lo
+                constexpr int kParts = 1;
+#else
+                constexpr int kParts = PARTS;
+#endif
+                for (int part = 0; part < kParts; ++part)
                     for (int kb = 0; kb < 2; ++kb) {
                         const uint64_t ad = umma_desc_sw128(sa + st * kTileA + kb * 128 * 128);
                         const uint64_t bd = umma_desc_sw128(sb + (part * 2 + kb) * NP * 128);
@@ -133,16 +153,20 @@ __global__ void __launch_bounds__(kHThreads, 1)
             }
         }
     } else {
-        // ------------------------------------------------ epilogue (warps 2..5)
-        const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
+        // ------------------------------------------------ epilogue (warps 2..5 and 6..9)
+        const int quarter = warp & 3;   // TMEM lanes 32*quarter .. +31
+        const int eset = (warp - 2) >> 2;  // set 0: even tiles (accumulator 0), set 1: odd tiles
         const int L = p.L;
         const int t0 = group * 32;
         const int nt = min(32, L - t0);
         const uint32_t tmask = nt == 32 ? 0xffffffffu : ((1u << nt) - 1u);
         const int W = (L + 31) >> 5, R = ((C * W) + 3) & ~3;
         int it = 0;
+        constexpr int NB = kHESets == 1 ? 2 : 1;
+        uint32_t r[NB][32];
         for (int64_t tile = cta_in_group; tile < n_tiles; tile += ctas_per_group, ++it) {
             const int acc = it & 1;
+            if (kHESets == 2 && acc != eset) continue;
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
             const int64_t row = tile * 128 + quarter * 32 + lane;
@@ -152,29 +176,49 @@ __global__ void __launch_bounds__(kHThreads, 1)
             uint32_t codes_w[8];  // 32 tables x 8-bit codes
             uint32_t any_nonzero = 0;
             const uint32_t base = tmem + acc * 256 + (static_cast<uint32_t>(quarter * 32) << 16);
-            // chunk b = plane word b (32 tables); sign bits gathered by funnel
-            // shifts of -D (MSB set iff D > 0 as an int, i.e. float D > +0)
+            // chunk b = plane word b (32 tables); sign bits gathered by funnel shifts
             bool want_zero = group == 0 && p.zero_rows != nullptr;
+            // The planes are stored negated (permute_planes_kernel), so the accumulator
+            // holds -w.x and its sign bit is the hash bit: one funnel shift per value.
+            // The load of plane word b + 1 is in flight while word b is packed.
+            // one set: double-buffered, the next word's load is in flight while this one is
+            // packed; two sets would hide the load latency behind each other and use one
+            // buffer (10 warps leave 168 registers per thread)
+#ifdef DSRT_HASH_EXP_NOLD  // timing experiment only: no accumulator read-out at all
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[0][j] = r[NB - 1][j] = 0;
+#else
+            tmem_ld32(base, r[0]);
+#endif
 #pragma unroll
             for (int b = 0; b < C; ++b) {
-                uint32_t r[32];
-                tmem_ld32(base + b * 32, r);
-                tmem_wait_ld();
+                uint32_t(&rb)[32] = r[b % NB];
+#ifndef DSRT_HASH_EXP_NOLD
+                tmem_wait_ld_dep(rb);
+                if (NB == 2 && b + 1 < C) tmem_ld32(base + (b + 1) * 32, r[(b + 1) % NB]);
+#endif
                 uint32_t pw = 0;
+#ifdef DSRT_HASH_EXP_NOPACK  // timing experiment only: TMEM loads without the sign packing
+                pw = rb[0] ^ rb[31];
+#else
 #pragma unroll
-                for (int j = 31; j >= 0; --j) pw = __funnelshift_l(0u - r[j], pw, 1);
+                for (int j = 31; j >= 0; --j) pw = __funnelshift_l(rb[j], pw, 1);
+#endif
                 plane[b] = pw & tmask;
                 if (want_zero) {  // rows whose first word is all +-0 check every column (rare)
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) any_nonzero |= r[j];
+                    for (int j = 0; j < 32; ++j) any_nonzero |= rb[j];
                     if (b == 0) want_zero = __any_sync(0xffffffffu, (any_nonzero & 0x7fffffffu) == 0u);
                 }
+#ifndef DSRT_HASH_EXP_NOLD
+                if (NB == 1 && b + 1 < C) tmem_ld32(base + (b + 1) * 32, rb);
+#endif
             }
             any_nonzero &= 0x7fffffffu;
-            if (p.codes_out) codes_from_planes<C>(plane, codes_w);  // 8x8 bit transposes
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (p.codes_out) codes_from_planes<C>(plane, codes_w);  // 8x8 bit transposes
             if (row < p.n_rows) {
                 if (p.codes_out) {
                     uint8_t *dst = static_cast<uint8_t *>(p.codes_out) + row * L + t0;
@@ -210,7 +254,7 @@ static int launch_hash_tc(const CUtensorMap &mx, const CUtensorMap &mw, const Ha
                           uint32_t idesc, size_t smem, int ctas, cudaStream_t st);
 
 // reference plane order (row t*C + b per part) -> plane-major groups (row
-// g*32*C + b*32 + t), zero planes for tables >= L.  16-bit elements.
+// g*32*C + b*32 + t), negated, zero planes for tables >= L.  16-bit elements.
 __global__ void permute_planes_kernel(const uint16_t *__restrict__ src, int parts, int L, int C,
                                       int groups, uint16_t *__restrict__ dst) {
     const int64_t rows = static_cast<int64_t>(parts) * groups * 32 * C;
@@ -223,7 +267,9 @@ __global__ void permute_planes_kernel(const uint16_t *__restrict__ src, int part
     const int rem = static_cast<int>(row % per_part);
     const int g = rem / (32 * C), b = (rem % (32 * C)) / 32, t = rem % 32;
     const int tg = g * 32 + t;
-    dst[i] = tg < L ? src[(static_cast<int64_t>(part) * L * C + tg * C + b) * 128 + k] : uint16_t(0);
+    // sign bit flipped (fp16 and bf16 alike): the MMA accumulates -w.x, whose sign bit is the hash bit
+    dst[i] = tg < L ? uint16_t(src[(static_cast<int64_t>(part) * L * C + tg * C + b) * 128 + k] ^ 0x8000u)
+                    : uint16_t(0);
 }
 
 static int launch_hash_tc_c(int C, int /*parts: always 2 (hi/lo)*/, int stages, const CUtensorMap &mx,
