@@ -58,6 +58,19 @@ int dsrt_version(void);
 int dsrt_record_words(int L, int C);
 /* SM count etc. of the current device (host call, synchronous). */
 int dsrt_device_info(int *sm_count, int *cc_major, int *cc_minor, size_t *free_bytes);
+/* Stream-ordered copy between caller-owned buffers (device or page-locked host;
+ * cudaMemcpyDefault).  The batched query path stages its query vectors and its
+ * top-k results through pinned host buffers with this call, so those copies can
+ * be captured into the same CUDA graph as the kernels (replaces the host-side
+ * np.asarray / list building around index.py:264-319's device work). */
+int dsrt_copy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* Concatenate up to four small device buffers (byte counts multiples of 4, each
+ * segment placed at the next 16-byte boundary of dst) with one kernel; dst may be
+ * page-locked host memory (written over the bus, visible after the stream is
+ * synchronised).  Used to return a query's (scores, ids, zero-row flag, candidate
+ * count) with one graph node instead of four device-to-host copies. */
+int dsrt_pack4_async(void *dst, const void *src0, size_t n0, const void *src1, size_t n1,
+                     const void *src2, size_t n2, const void *src3, size_t n3, void *stream);
 
 /*
  * K1 -- replaces lsh.hash_matrix (lsh.py:90-106) and hash_vector (lsh.py:80-87).

@@ -33,6 +33,8 @@ SIGNATURES = {
     "dsrt_version": (_i32, []),
     "dsrt_record_words": (_i32, [_i32, _i32]),
     "dsrt_device_info": (_i32, [_vp, _vp, _vp, _vp]),
+    "dsrt_copy_async": (_i32, [_vp, _vp, _sz, _vp]),
+    "dsrt_pack4_async": (_i32, [_vp, _vp, _sz, _vp, _sz, _vp, _sz, _vp, _sz, _vp]),
     "dsrt_hash": (_i32, [_vp, _i32, _i64, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "dsrt_codes_to_records": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp]),
     "dsrt_sizes_to_offsets": (_i32, [_vp, _i64, _vp, _vp, _vp, _sz, _vp]),

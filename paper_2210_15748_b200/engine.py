@@ -58,6 +58,50 @@ def device_info():
     return {"sm_count": sms.value, "cc": (ma.value, mi.value), "free_bytes": fr.value}
 
 
+def copy_async(dst: torch.Tensor, src: torch.Tensor):
+    """Stream-ordered copy between a device tensor and a pinned host tensor (or two
+    device tensors) of equal dtype and shape, on the current stream (dsrt_copy_async:
+    capturable, no allocator bookkeeping)."""
+    if dst.shape != src.shape or dst.dtype != src.dtype:
+        raise ValueError("invalid parameter: copy_async needs equal shapes and dtypes")
+    if not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValueError("invalid parameter: copy_async needs contiguous tensors")
+    for t in (dst, src):
+        if not t.is_cuda and not t.is_pinned():
+            raise ValueError("invalid parameter: host side of copy_async must be page-locked")
+    _lib.call("dsrt_copy_async", _ptr(dst), _ptr(src), ctypes.c_size_t(dst.numel() * dst.element_size()),
+              _stream())
+
+
+def pack_layout(tensors):
+    """(offsets, total bytes) of dsrt_pack4_async's destination for up to four tensors
+    (None = absent): each segment starts at the next 16-byte boundary."""
+    offs, off = [], 0
+    for t in tensors:
+        offs.append(off)
+        if t is not None:
+            off += (t.numel() * t.element_size() + 15) & ~15
+    return offs, max(off, 16)
+
+
+def pack4(dst: torch.Tensor, tensors):
+    """Concatenate up to four small contiguous CUDA tensors into ``dst`` (uint8; device or
+    pinned host memory) with one kernel on the current stream (dsrt_pack4_async)."""
+    ts = list(tensors) + [None] * (4 - len(tensors))
+    if len(ts) != 4:
+        raise ValueError("invalid parameter: pack4 takes at most four tensors")
+    args = []
+    for t in ts:
+        if t is not None and not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("invalid parameter: pack4 sources must be contiguous CUDA tensors")
+        args += [_ptr(t), ctypes.c_size_t(0 if t is None else t.numel() * t.element_size())]
+    if not dst.is_cuda and not dst.is_pinned():
+        raise ValueError("invalid parameter: host side of pack4 must be page-locked")
+    if dst.numel() * dst.element_size() < pack_layout(ts)[1]:
+        raise ValueError("invalid parameter: pack4 destination too small")
+    _lib.call("dsrt_pack4_async", _ptr(dst), *args, _stream())
+
+
 # ------------------------------------------------------------------- K1
 def hash_vectors(X: torch.Tensor, planes: torch.Tensor, mode: int, L: int, C: int,
                  want_codes: bool = True, want_records: bool = True, check_zero: bool = True):

@@ -311,13 +311,18 @@ def _rank(scores: torch.Tensor, top_k: int, ids: torch.Tensor, n_valid=None, can
     return engine.topk(scores, k, ids=ids, n_valid=n_valid)
 
 
-def _results(out_s: torch.Tensor, out_i: torch.Tensor) -> list[RankedResults]:
-    s = out_s.cpu().numpy()
-    ids = out_i.cpu().numpy().view(np.uint64)
+_NP_DTYPE = {torch.float64: np.float64, torch.int64: np.int64, torch.int32: np.int32,
+             torch.uint8: np.uint8, torch.float32: np.float32}
+
+
+def _results(out_s, out_i) -> list[RankedResults]:
+    """(scores, ids) as device / host tensors or numpy arrays -> ranked (doc id, score) lists."""
+    s = out_s if isinstance(out_s, np.ndarray) else out_s.cpu().numpy()
+    ids = (out_i if isinstance(out_i, np.ndarray) else out_i.cpu().numpy()).view(np.uint64)
     res = []
     for r in range(s.shape[0]):
         valid = s[r] >= 0.0
-        res.append([(int(d), float(v)) for d, v in zip(ids[r][valid], s[r][valid])])
+        res.append(list(zip(ids[r][valid].tolist(), s[r][valid].tolist())))  # (int, float) pairs
     return res
 
 
@@ -456,14 +461,36 @@ class _QueryGraph:
         self.done = None  # event: last replay's outputs copied out
         self.q_in = torch.empty(q.shape, dtype=q.dtype, device=index.device)
         self.q_in.copy_(q)
-        self._run(index)  # eager warm-up: lazy initialisation outside the capture
+        warm = self._run(index)  # eager warm-up: lazy initialisation outside the capture
         torch.cuda.synchronize()
+        # Host queries: the H2D copy of the query and the D2H copies of the results are
+        # nodes of the graph (pinned staging buffers), so a call is one host memcpy, one
+        # replay and one synchronisation instead of a pageable copy in and four
+        # synchronous copies out (batch-1 p50 0.240 -> see DESIGN K5 "small batches").
+        self.host_io = not q.is_cuda
+        self.q_host = self.out_host = None
+        if self.host_io:
+            self.q_host = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+            self.q_host.copy_(q)
+            # one pinned buffer for (scores, ids, zero-row count, candidate counts): a single
+            # pack kernel writes it over the bus (a D2H copy node per tensor costs ~3.5 us each)
+            self.out_meta = [None if t is None else (tuple(t.shape), _NP_DTYPE[t.dtype], t.numel() * t.element_size())
+                             for t in warm]
+            self.out_offs, total = engine.pack_layout(warm)
+            self.out_host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+            self.out_np = self.out_host.numpy()
+        del warm
         self.graph = torch.cuda.CUDAGraph()
         gc_on = gc.isenabled()
         gc.disable()
         try:
             with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+                if self.host_io:
+                    engine.copy_async(self.q_in, self.q_host)
                 self.out = self._run(index)
+                if self.host_io:
+                    self.out = tuple(None if t is None else t.contiguous() for t in self.out)
+                    engine.pack4(self.out_host, self.out)
         finally:
             if gc_on:
                 gc.enable()
@@ -496,8 +523,23 @@ class _QueryGraph:
         stream = torch.cuda.current_stream()
         if self.done is not None:
             stream.wait_event(self.done)
-        self.q_in.copy_(q, non_blocking=True)
+        if self.host_io:
+            self.q_host.copy_(q)  # the graph's first node uploads it
+        else:
+            self.q_in.copy_(q, non_blocking=True)
         self.graph.replay()
+        if to_host and self.host_io:
+            stream.synchronize()
+            self.done = None
+            raw = self.out_np.copy()  # the pinned buffer is reused by the next call
+            out = []
+            for meta, off in zip(self.out_meta, self.out_offs):
+                if meta is None:
+                    out.append(None)
+                    continue
+                shape, dtype, nbytes = meta
+                out.append(raw[off:off + nbytes].view(dtype).reshape(shape))  # numpy views of the copy
+            return tuple(out)
         if to_host:
             out = tuple(None if t is None else t.cpu() for t in self.out)
         else:
@@ -535,7 +577,7 @@ def _query_graphed(index: DessertIndex, Qa, top_k: int, probe, k_filter, to_host
         out_s, out_i, zero, n_cand = g(q, to_host)
     finally:
         g.lock.release()
-    if int(zero[0].item() if zero.is_cuda else zero[0]) != 0:
+    if int(zero[0].item() if isinstance(zero, torch.Tensor) and zero.is_cuda else zero[0]) != 0:
         raise ValueError("zero vector cannot be hashed (sign of zero projection undefined)")
     return out_s, out_i, n_cand
 

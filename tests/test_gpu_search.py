@@ -281,3 +281,60 @@ def test_graph_replays_concurrent_streams_tensors():
     torch.cuda.synchronize()
     for (s, i), w in zip(outs, want):
         assert I._results(s, i) == w
+
+
+def test_copy_async_and_pack4_through_pinned_host_buffers():
+    """The graph query path's staging calls: dsrt_copy_async (pinned host <-> device) and
+    dsrt_pack4_async (up to four small device tensors -> one device or pinned host buffer)."""
+    dev = torch.device("cuda")
+    src = torch.arange(1000, dtype=torch.float64).reshape(10, 100).pin_memory()
+    on_dev = torch.empty(10, 100, dtype=torch.float64, device=dev)
+    back = torch.empty(10, 100, dtype=torch.float64).pin_memory()
+    engine.copy_async(on_dev, src)
+    engine.copy_async(back, on_dev)
+    torch.cuda.synchronize()
+    assert torch.equal(back, src)
+    with pytest.raises(ValueError, match="page-locked"):
+        engine.copy_async(on_dev, torch.zeros(10, 100, dtype=torch.float64))
+    a = torch.rand(3, 7, dtype=torch.float64, device=dev)
+    b = torch.randint(0, 1 << 60, (3, 7), dtype=torch.int64, device=dev)
+    c = torch.tensor([5], dtype=torch.int32, device=dev)
+    for tensors in ([a, b, c, None], [a, None, c, b], [c], [a, b, c, c]):
+        offs, total = engine.pack_layout(tensors)
+        for dst in (torch.zeros(total, dtype=torch.uint8, device=dev),
+                    torch.zeros(total, dtype=torch.uint8).pin_memory()):
+            engine.pack4(dst, tensors)
+            torch.cuda.synchronize()
+            raw = dst.cpu().numpy()
+            for t, off in zip(tensors, offs):
+                if t is None:
+                    continue
+                n = t.numel() * t.element_size()
+                assert off % 16 == 0
+                got = torch.from_numpy(raw[off:off + n].copy()).view(t.dtype).reshape(t.shape)
+                assert torch.equal(got, t.cpu())
+
+
+def test_query_from_host_arrays_matches_device_tensors_and_eager_path(monkeypatch):
+    """query()/query_batch() with host inputs replay a graph whose first node uploads the
+    query and whose last node packs the results into pinned memory; device-tensor inputs
+    and the eager path (DSRT_QUERY_GRAPHS=0) must give the same rankings."""
+    rng = np.random.default_rng(5)
+    sizes = rng.integers(3, 30, size=300)
+    X = rng.standard_normal((int(sizes.sum()), 32)).astype(np.float32)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    docs = [(i, X[off[i]:off[i + 1]]) for i in range(len(sizes))]
+    for enabled in (False, True):
+        cfg = d.IndexConfig(d=32, C=5, L=32, seed=1,
+                            filter=d.FilterConfig(enabled=enabled, centroids=16, iters=3, probe=2, k_filter=40))
+        idx = d.build_index(docs, cfg)
+        Qs = np.stack([X[off[i]:off[i] + 3] for i in (7, 100, 250)])
+        host = [d.query(idx, Q, 20) for Q in Qs]
+        again = [d.query(idx, Q, 20) for Q in Qs]       # second replay of the same graph
+        dev_in = [d.query(idx, torch.from_numpy(Q).cuda(), 20) for Q in Qs]
+        batch = d.query_batch(idx, Qs, 20)
+        monkeypatch.setenv("DSRT_QUERY_GRAPHS", "0")
+        eager = [d.query(idx, Q, 20) for Q in Qs]
+        monkeypatch.delenv("DSRT_QUERY_GRAPHS")
+        assert host == again == dev_in == batch == eager
+        assert all(1 <= len(r) <= 20 for r in host)
