@@ -622,6 +622,33 @@ struct CandWin {
     }
 };
 
+// Piece window of the candidate kernel: lane l holds, for candidate base + l of the
+// run, the byte address of its records and the metadata word of its (single) piece --
+// nvec | kPieceDone | kPieceValid -- or kPieceMulti when the set is longer than one piece
+// (then len is used).  One batch of loads per 32 candidates; issuing a piece is three
+// shuffles and the bulk copy.
+constexpr uint32_t kPieceDone = 1u << 16, kPieceValid = 1u << 17, kPieceMulti = 0xffffffffu;
+struct PieceWin {
+    int32_t base = -(1 << 30), len = 0;  // base: run-relative candidate index of lane 0
+    uint32_t meta = 0;
+    const uint32_t *src = nullptr;
+    template <int PV, int R>
+    __device__ __forceinline__ void load(int32_t k, int64_t e_lo, int64_t e_hi, const int64_t *cand_row,
+                                         const int64_t *set_off, int64_t n_sets,
+                                         const uint32_t *recs) {
+        base = k;
+        const int64_t e = e_lo + k + (threadIdx.x & 31);
+        int64_t sidx = -1;
+        if (e < e_hi) sidx = cand_row ? __ldg(cand_row + e) : e;
+        const bool ok = sidx >= 0 && sidx < n_sets;
+        const int64_t vb = ok ? __ldg(set_off + sidx) : 0;
+        len = ok ? static_cast<int32_t>(__ldg(set_off + sidx + 1) - vb) : 0;
+        src = recs + vb * R;
+        meta = len > PV ? kPieceMulti
+                        : (static_cast<uint32_t>(len) | kPieceDone | (ok ? kPieceValid : 0u));
+    }
+};
+
 // One warp = (query set, run of candidate slots).  Each warp streams its
 // candidates' records through a private kBufs-deep ring filled by
 // cp.async.bulk issued from lane 0.
@@ -680,59 +707,62 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     Slots<QPL> slots{slot_mem + warp * SlotGeom<QPL>::kBytes};
     double *out_row = scores != nullptr ? scores + qset * cand_ld : nullptr;
 
-    // candidate metadata through lane windows: lane l holds (vbeg, vend) of
-    // candidate base + l (vbeg = vend = 0 for an invalid set index), loaded in
-    // one batch per 32 candidates instead of a dependent load chain per set.
+    // candidate metadata through a lane window (PieceWin): one batch of loads per 32
+    // candidates instead of a dependent load chain per set.
     const int64_t *cand_row = cand ? cand + qset * cand_ld : nullptr;
-    CandWin pwin;
-    // producer iterator (lane-uniform state; lane 0 issues the copies).  The
-    // per-piece arithmetic is 32-bit -- candidate offset pk within the run and
-    // the vectors prem left in the current candidate; only the record address
-    // pv is 64-bit.
+    PieceWin pwin;
+    // producer iterator (lane-uniform state; lane 0 issues the copies): pk = candidates of
+    // the run already issued; a set longer than one piece is continued from (mp_src, mp_rem)
     const int nrun = static_cast<int>(e_hi - e_lo);
-    int pk = 0, prem;
-    int64_t pv;
-    bool pvalid;
-    {
-        int64_t vb, ve;
-        pwin.get(e_lo, e_hi, cand_row, set_off, n_sets, vb, ve);
-        pvalid = ve >= 0;
-        pv = pvalid ? vb : 0;
-        prem = pvalid ? static_cast<int>(ve - vb) : 0;
-    }
+    int pk = 0, mp_rem = 0;
+    const uint32_t *mp_src = nullptr;
     int issued = 0, consumed = 0, pb = 0;  // pb = issued % kBufs
-    constexpr uint32_t kDone = 1u << 16, kValid = 1u << 17;
+    constexpr uint32_t kDone = kPieceDone, kValid = kPieceValid;
     // The buffer being refilled was last read by this warp's LDS, complete before
     // the __syncwarp that precedes every refill, so no proxy fence is needed for
     // the bulk copy's write-after-read.
-    auto issue = [&]() -> uint32_t {  // next piece (pk, [pv, ..)) into buffer pb; returns its metadata
+    auto issue = [&]() -> uint32_t {  // next piece into buffer pb; returns its metadata
         const int b = pb;
         pb = pb + 1 == kBufs ? 0 : pb + 1;
-        const int nvec = pk < nrun ? min(PV, prem) : 0;
+        uint32_t meta = 0;
+        const uint32_t *src = nullptr;
+        if (mp_rem > 0) {  // continue a multi-piece set (rare: longer than PV vectors)
+            const int nvec = min(PV, mp_rem);
+            src = mp_src;
+            mp_src += static_cast<int64_t>(nvec) * R;
+            mp_rem -= nvec;
+            meta = static_cast<uint32_t>(nvec);
+            if (mp_rem == 0) {
+                meta |= kDone | kValid;
+                ++pk;
+            }
+        } else if (pk < nrun) {
+            int l = pk - pwin.base;
+            if (l >= 32) {
+                pwin.load<PV, R>(pk, e_lo, e_hi, cand_row, set_off, n_sets, recs);
+                l = 0;
+            }
+            meta = __shfl_sync(kFull, pwin.meta, l);
+            src = reinterpret_cast<const uint32_t *>(
+                __shfl_sync(kFull, reinterpret_cast<unsigned long long>(pwin.src), l));
+            if (meta == kPieceMulti) {
+                mp_rem = __shfl_sync(kFull, pwin.len, l) - PV;
+                mp_src = src + static_cast<int64_t>(PV) * R;
+                meta = static_cast<uint32_t>(PV);
+            } else {
+                ++pk;
+            }
+        }
         if (lane == 0) {
-            const uint32_t bytes = static_cast<uint32_t>(nvec * R * 4);
+            const uint32_t bytes = (meta & 0xffffu) * static_cast<uint32_t>(R * 4);
             if (bytes > 0) {
                 mbar_arrive_expect_tx(&bars[b], bytes);
-                bulk_g2s(bufs + b * (PV * R), recs + pv * R, bytes, &bars[b]);
+                bulk_g2s(bufs + b * (PV * R), src, bytes, &bars[b]);
             } else {
                 mbar_arrive(&bars[b]);
             }
         }
         ++issued;
-        pv += nvec;
-        prem -= nvec;
-        uint32_t meta = static_cast<uint32_t>(nvec);
-        if (pk < nrun && prem <= 0) {  // advance to the next candidate
-            meta |= kDone | (pvalid ? kValid : 0u);
-            ++pk;
-            if (pk < nrun) {
-                int64_t vb, ve;
-                pwin.get(e_lo + pk, e_hi, cand_row, set_off, n_sets, vb, ve);
-                pvalid = ve >= 0;
-                pv = pvalid ? vb : 0;
-                prem = pvalid ? static_cast<int>(ve - vb) : 0;
-            }
-        }
         return meta;
     };
     // Consumer: replays the producer's piece sequence from metadata the
