@@ -716,14 +716,13 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     const int nrun = static_cast<int>(e_hi - e_lo);
     int pk = 0, mp_rem = 0;
     const uint32_t *mp_src = nullptr;
-    int issued = 0, consumed = 0, pb = 0;  // pb = issued % kBufs
     constexpr uint32_t kDone = kPieceDone, kValid = kPieceValid;
     // The buffer being refilled was last read by this warp's LDS, complete before
     // the __syncwarp that precedes every refill, so no proxy fence is needed for
     // the bulk copy's write-after-read.
-    auto issue = [&]() -> uint32_t {  // next piece into buffer pb; returns its metadata
-        const int b = pb;
-        pb = pb + 1 == kBufs ? 0 : pb + 1;
+    // The ring is refilled in consumption order, so the buffer to fill is always the one
+    // just consumed (b), and kBufs pieces are outstanding whenever the loop is left.
+    auto issue = [&](int b) -> uint32_t {  // next piece into buffer b; returns its metadata
         uint32_t meta = 0;
         const uint32_t *src = nullptr;
         if (mp_rem > 0) {  // continue a multi-piece set (rare: longer than PV vectors)
@@ -762,7 +761,6 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
                 mbar_arrive(&bars[b]);
             }
         }
-        ++issued;
         return meta;
     };
     // Consumer: replays the producer's piece sequence from metadata the
@@ -773,7 +771,7 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     int64_t slot_col = e_lo;
     uint32_t meta[kBufs];
 #pragma unroll
-    for (int i = 0; i < kBufs; ++i) meta[i] = issue();
+    for (int i = 0; i < kBufs; ++i) meta[i] = issue(i);
     int b = 0;
     uint32_t phase = 0;
     while (ck < nrun) {
@@ -803,16 +801,14 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
         __syncwarp();
 #pragma unroll
         for (int i = 0; i + 1 < kBufs; ++i) meta[i] = meta[i + 1];
-        meta[kBufs - 1] = issue();  // refill the buffer just consumed
-        ++consumed;
+        meta[kBufs - 1] = issue(b);  // refill the buffer just consumed
         if (++b == kBufs) { b = 0; phase ^= 1u; }
     }
     if (slots.n > 0)
         slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
     // drain: wait for outstanding pieces so no bulk copy outlives the CTA
-    while (consumed < issued) {
+    for (int i = 0; i < kBufs; ++i) {
         mbar_wait(&bars[b], phase);
-        ++consumed;
         if (++b == kBufs) { b = 0; phase ^= 1u; }
     }
 }
