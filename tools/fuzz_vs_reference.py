@@ -151,12 +151,80 @@ def compare(case, a, b):
     return errs
 
 
+def make_case_fp16(seed):
+    """d = 128, C <= 8, >= 4096 fp16 vectors: build_index hashes them on the tcgen05 hi/lo
+    path, whose bits may differ from float64 inside the 1e-4 band only."""
+    rng = np.random.default_rng([seed, 0xF16])
+    if True:
+        case = make_case(int(rng.integers(0, 1 << 30)))
+        rs = np.random.default_rng([seed, 1])
+        n_sets = int(rs.integers(210, 400))  # x >= 20 vectors: at least 4096 rows -> tcgen05 hash
+        sizes = rs.integers(20, 60, size=n_sets)
+        cents = unit(rs.standard_normal((int(rs.integers(2, 30)), 128)))
+        ids = rs.choice(np.arange(1, 10 * n_sets), size=n_sets, replace=False)
+        docs = []
+        for i in range(n_sets):
+            c = cents[rs.integers(0, cents.shape[0], size=sizes[i])]
+            docs.append((int(ids[i]), unit(c + 0.3 * rs.standard_normal((sizes[i], 128))).astype(np.float16)))
+        m_q = int(rs.integers(1, 41))
+        Qs = []
+        for _ in range(int(rs.integers(1, 4))):
+            src = docs[rs.integers(0, n_sets)][1].astype(np.float64)
+            q = src[rs.integers(0, src.shape[0], size=m_q)] + 0.1 * rs.standard_normal((m_q, 128))
+            Qs.append(unit(q).astype(np.float16))
+        case.update(d=128, C=int(rs.integers(1, 9)), L=int(rs.integers(1, 129)), docs=docs, Qs=Qs, m_q=m_q,
+                    top_k=int(rs.integers(1, n_sets + 5)), cand_ix=rs.integers(0, n_sets, size=3),
+                    add_split=0)
+        if case["weights"] is not None:
+            case["weights"] = rs.random(m_q)
+        case["filter"]["k_filter"] = int(rs.integers(1, n_sets + 10))
+        case["filter"]["centroids"] = 0 if rs.random() < 0.4 else int(rs.integers(1, 65))
+    return case
+
+
+def run_fp16_case(case):
+    """Ours first (tensor-core hash of the fp16 documents); then the reference built on OUR
+    codes (its hash_matrix patched for the build only) -- identical codes in, identical
+    scores, rankings, file bytes and prefilter out.  Also counts the bits that differ from
+    the reference's own float64 hash (they must sit inside the band; tests assert that)."""
+    import dessert.index as ref_index
+
+    rb = run_side(d, case, True)
+    cfg = d.IndexConfig(d=128, C=case["C"], L=case["L"], seed=case["cfg_seed"], inner_kind=case["inner"],
+                        phi=case["phi"], filter=d.FilterConfig(**case["filter"]))
+    idx = d.build_index(case["docs"], cfg)
+    codes = idx.codes.cpu().numpy().astype(np.int64)
+    off = np.concatenate([[0], np.cumsum([X.shape[0] for _, X in case["docs"]])])
+    queue = [codes[off[i]:off[i + 1]] for i in range(len(case["docs"]))]
+    orig = ref_index.hash_matrix
+    flips = 0
+
+    def patched(fam, X):
+        nonlocal flips
+        if queue:
+            mine = queue.pop(0)
+            flips += int(np.count_nonzero(np.asarray(orig(fam, X)) != mine))
+            return mine
+        return orig(fam, X)
+
+    ref_index.hash_matrix = patched
+    try:
+        ra = run_side(ref, case, False)
+    finally:
+        ref_index.hash_matrix = orig
+    return ra, rb, flips
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=300)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--fp16", action="store_true",
+                    help="fp16 collections hashed on the tensor-core path; the reference is built on our codes")
     a = ap.parse_args()
+    if a.fp16:
+        return main_fp16(a)
     bad = 0
     t0 = time.time()
     for s in range(a.seed, a.seed + a.cases):
@@ -190,6 +258,32 @@ def main():
         elif a.verbose:
             print("ok:", desc)
     print(f"fuzz: {a.cases} cases, {bad} mismatches, {time.time() - t0:.0f} s")
+    return 1 if bad else 0
+
+
+def main_fp16(a):
+    bad = flips = 0
+    t0 = time.time()
+    for s in range(a.seed, a.seed + a.cases):
+        case = make_case_fp16(s)
+        desc = (f"seed={s} C={case['C']} L={case['L']} sets={len(case['docs'])} m_q={case['m_q']} "
+                f"inner={case['inner']}/{case['phi']} filter={case['filter']} top_k={case['top_k']}")
+        try:
+            ra, rb, f = run_fp16_case(case)
+        except Exception:  # noqa: BLE001
+            bad += 1
+            print("MISMATCH (exception):", desc)
+            print(traceback.format_exc())
+            continue
+        flips += f
+        errs = compare(case, ra, rb)
+        if errs:
+            bad += 1
+            print("MISMATCH:", desc, "|", "; ".join(errs))
+        elif a.verbose:
+            print("ok:", desc, "flipped code entries:", f)
+    print(f"fuzz fp16: {a.cases} cases, {bad} mismatches, {flips} code entries differ from the float64 hash, "
+          f"{time.time() - t0:.0f} s")
     return 1 if bad else 0
 
 
