@@ -638,6 +638,7 @@ struct CandWin {
 // (then len is used).  One batch of loads per 32 candidates; issuing a piece is three
 // shuffles and the bulk copy.
 constexpr uint32_t kPieceDone = 1u << 16, kPieceValid = 1u << 17, kPieceMulti = 0xffffffffu;
+static_assert(kPieceValid == 1u << 17, "the slot valid bit is taken from bit 17 of the piece word");
 struct PieceWin {
     int32_t base = -(1 << 30), len = 0;  // base: run-relative candidate index of lane 0
     uint32_t meta = 0;
@@ -784,6 +785,9 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
     for (int i = 0; i < kBufs; ++i) meta[i] = issue(i);
     int b = 0;
     uint32_t phase = 0;
+    // split-lane slot stores: per-lane predicates and a running row pointer, set up once
+    const bool st0 = SPLIT && lane < 16 && lane < m_q, st1 = SPLIT && lane < 16 && lane + 16 < m_q;
+    uint8_t *wr = slots.buf + lane;
     while (ck < nrun) {
         mbar_wait(&bars[b], phase);
         const uint32_t m0 = meta[0];
@@ -796,7 +800,12 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
             if constexpr (SPLIT) {
 #pragma unroll
                 for (int i = 0; i < 2; ++i) rmin[i] = min(rmin[i], __shfl_xor_sync(kFull, rmin[i], 16));
-                slots.push_split(rmin, L, m_q, (m0 & kValid) != 0);
+                // Slots::push_split with the address and predicate arithmetic hoisted
+                if (st0) wr[0] = static_cast<uint8_t>(L - rmin[0]);
+                if (st1) wr[16] = static_cast<uint8_t>(L - rmin[1]);
+                wr += SlotGeom<QPL>::kRow;
+                slots.valid |= ((m0 >> 17) & 1u) << slots.n;  // kValid
+                ++slots.n;
             } else {
                 slots.push(rmin, L, m_q, (m0 & kValid) != 0);
             }
@@ -805,6 +814,7 @@ __global__ void __launch_bounds__(kCandWarps * 32, DSRT_CAND_MINB)
             if (slots.n == 32) {
                 slots.flush(m_q, lut_s, w_s, out_row, slot_col, maxcounts, qset * cand_ld, mc_stride, mc_q0);
                 slot_col += 32;
+                wr = slots.buf + lane;
             }
             ++ck;
         }
