@@ -334,29 +334,69 @@ __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], in
             i += 2;
         }
     } else if constexpr (W == 1) {
-#pragma unroll PU
-        for (; i + 2 <= nv; i += 2) {
-            uint4 xa[R / 4], xb[R / 4];
+        // explicit trip counts (shifts of nv) and a walking pointer: the compiler's own
+        // unroll prologue cost ~20 instructions per call, i.e. per set
+        constexpr int V = R / 4;
+        auto pair = [&](const uint4 *px) {
+            uint4 xa[V], xb[V];
 #pragma unroll
-            for (int u = 0; u < R / 4; ++u) {
-                xa[u] = x4[i * (R / 4) + u];
-                xb[u] = x4[(i + 1) * (R / 4) + u];
+            for (int u = 0; u < V; ++u) {
+                xa[u] = px[u];
+                xb[u] = px[V + u];
             }
             const uint32_t *a = reinterpret_cast<const uint32_t *>(xa);
             const uint32_t *b = reinterpret_cast<const uint32_t *>(xb);
 #pragma unroll
             for (int s = 0; s < QPL; ++s)
                 rmin[s] = __vimin3_s32(rmin[s], mismatches<K, W>(q[s], a), mismatches<K, W>(q[s], b));
+        };
+        const uint4 *px = x4;
+        if constexpr (PU >= 2) {
+            for (int t = nv >> 2; t > 0; --t) {
+                pair(px);
+                pair(px + 2 * V);
+                px += 4 * V;
+            }
+            if (nv & 2) pair(px);
+        } else {
+            for (int t = nv >> 1; t > 0; --t) {
+                pair(px);
+                px += 2 * V;
+            }
         }
-    }
-#pragma unroll 4
-    for (; i < nv; ++i) {
-        uint4 xv[R / 4];
+        if (nv & 1) {  // odd last vector
+            uint4 xv[V];
 #pragma unroll
-        for (int u = 0; u < R / 4; ++u) xv[u] = x4[i * (R / 4) + u];
+            for (int u = 0; u < V; ++u) xv[u] = x4[(nv - 1) * V + u];
+            const uint32_t *x = reinterpret_cast<const uint32_t *>(xv);
+#pragma unroll
+            for (int s = 0; s < QPL; ++s) rmin[s] = min(rmin[s], mismatches<K, W>(q[s], x));
+        }
+        i = nv;
+    }
+    // one vector at a time: the W >= 2 path (4 per trip, explicit counts as above) and the
+    // odd last vector of the 4-vector W = 1 groups
+    constexpr int V1 = R / 4;
+    auto single = [&](const uint4 *px) {
+        uint4 xv[V1];
+#pragma unroll
+        for (int u = 0; u < V1; ++u) xv[u] = px[u];
         const uint32_t *x = reinterpret_cast<const uint32_t *>(xv);
 #pragma unroll
         for (int s = 0; s < QPL; ++s) rmin[s] = min(rmin[s], mismatches<K, W>(q[s], x));
+    };
+    const uint4 *p1 = x4 + i * V1;
+    const int left = nv - i;
+    for (int t = left >> 2; t > 0; --t) {
+        single(p1);
+        single(p1 + V1);
+        single(p1 + 2 * V1);
+        single(p1 + 3 * V1);
+        p1 += 4 * V1;
+    }
+    for (int r = left & 3; r > 0; --r) {
+        single(p1);
+        p1 += V1;
     }
 }
 
@@ -528,16 +568,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
             slots[j].valid = 0;
         }
     };
+    // slot-row stores (Slots::put for the QS query sets): per-lane predicates and one
+    // running offset, the row of query set j at a compile-time distance
+    bool st_ok[QPL];
+#pragma unroll
+    for (int i = 0; i < QPL; ++i) st_ok[i] = lane + 32 * i < m_q;
+    uint8_t *const wbase = slot_mem + warp * QS * SlotGeom<QPL>::kBytes + lane;
+    int wro = 0;  // nslot * kRow
     auto finish_set = [&]() {
 #pragma unroll
         for (int j = 0; j < QS; ++j)
-            slots[j].put(*reinterpret_cast<const int(*)[QPL]>(&rmin[j * QPL]), L, m_q, nslot);
+#pragma unroll
+            for (int i = 0; i < QPL; ++i)
+                if (st_ok[i])
+                    wbase[wro + j * SlotGeom<QPL>::kBytes + 32 * i] = static_cast<uint8_t>(L - rmin[j * QPL + i]);
+        wro += SlotGeom<QPL>::kRow;
 #pragma unroll
         for (int i = 0; i < S; ++i) rmin[i] = L;
         ++s;
         if (++nslot == 32) {
             if (any_active) flush_all();
             nslot = 0;
+            wro = 0;
             slot_col += 32;
         }
         if (s < s_hi) s_end_v = win.get(s + 1);
