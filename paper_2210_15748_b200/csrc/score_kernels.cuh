@@ -22,6 +22,7 @@
 // thus spread over lanes instead of being a warp-wide reduction per set.
 #pragma once
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -400,7 +401,10 @@ __device__ __forceinline__ void scan_vectors(const uint32_t (&q)[QPL][K * W], in
     }
 }
 
-// Lane-distributed window of set_off: lane l holds set_off[base + l].
+// Lane-distributed window of set_off: lane l holds set_off[base + l] (absolute 64-bit
+// indices), or -- OffWindowRel -- set_off[s_lo + base + l] - vbeg as an int: the window is
+// then built on set_off + s_lo with vbase = the chunk's first vector, so the consumer loop
+// runs on chunk-relative 32-bit indices (launch_all keeps a chunk below 2^31 vectors and sets).
 struct OffWindow {
     const int64_t *off;
     int64_t base, limit;  // valid indices <= limit
@@ -413,6 +417,21 @@ struct OffWindow {
     __device__ __forceinline__ int64_t get(int64_t i) {  // warp-uniform i
         if (i - base >= 32) load(i);
         return __shfl_sync(kFull, v, static_cast<int>(i - base));
+    }
+};
+struct OffWindowRel {
+    const int64_t *off;  // set_off + s_lo
+    int base, limit;
+    int v;
+    int64_t vbase;
+    __device__ __forceinline__ void load(int b) {
+        base = b;
+        const int i = b + (threadIdx.x & 31);
+        v = i <= limit ? static_cast<int>(__ldg(off + i) - vbase) : INT32_MAX;
+    }
+    __device__ __forceinline__ int get(int i) {  // warp-uniform i
+        if (i - base >= 32) load(i);
+        return __shfl_sync(kFull, v, i - base);
     }
 };
 
@@ -544,12 +563,24 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
     Slots<QPL> slots[QS];
 #pragma unroll
     for (int j = 0; j < QS; ++j) slots[j].buf = slot_mem + (warp * QS + j) * SlotGeom<QPL>::kBytes;
-    OffWindow win{set_off, 0, s_hi, 0};
-    win.load(s_lo + 1);
+    // Set and vector indices of the consumer loop.  Two-word records (L = 64, cfg1) run on
+    // chunk-relative 32-bit indices (fewer instructions per set: 205.2 -> 201.2 ms at cfg1
+    // shape); for one-word records the same change re-scheduled the hot loop for the worse
+    // (226.8 -> 230.4 ms at cfg4 shape), so they keep absolute 64-bit indices.
+    using I = std::conditional_t<(W >= 2), int, int64_t>;
+    constexpr bool REL = sizeof(I) == 4;
+    const I s1 = static_cast<I>(REL ? s_hi - s_lo : s_hi);
+    const I v0 = static_cast<I>(REL ? 0 : vbeg), v1 = static_cast<I>(REL ? vend - vbeg : vend);
+    using Win = std::conditional_t<REL, OffWindowRel, OffWindow>;
+    Win win;
+    if constexpr (REL) win = Win{set_off + s_lo, 0, static_cast<int>(s1), 0, vbeg};
+    else win = Win{set_off, 0, s_hi, 0};
+    I s = static_cast<I>(REL ? 0 : s_lo);
+    win.load(s + 1);
 
-    int64_t s = s_lo, slot_col = s_lo - set_begin;
-    int64_t s_end_v = win.get(s + 1);
-    int64_t v = vbeg;
+    int64_t slot_col = s_lo - set_begin;
+    I s_end_v = win.get(s + 1);
+    I v = v0;
     int nslot = 0;  // filled slot rows, shared by the QS query sets (all valid)
     auto flush_all = [&]() {
 #pragma unroll
@@ -592,21 +623,21 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
             wro = 0;
             slot_col += 32;
         }
-        if (s < s_hi) s_end_v = win.get(s + 1);
+        if (s < s1) s_end_v = win.get(s + 1);
     };
 
     for (int64_t t = 0; t < n_tiles; ++t) {
         const int st = static_cast<int>(t % kStages);
         mbar_wait(&full[st], static_cast<uint32_t>(t / kStages) & 1);
         const uint32_t *tile = tiles + st * (kTileVec * R);
-        const int64_t tv0 = vbeg + t * kTileVec;
-        const int64_t tv1 = tmin<int64_t>(tv0 + kTileVec, vend);
+        const I tv0 = v0 + static_cast<I>(t) * kTileVec;
+        const I tv1 = tmin<I>(tv0 + kTileVec, v1);
         while (v < tv1) {
-            const int64_t stop = tmin(s_end_v, tv1);
+            const I stop = tmin<I>(s_end_v, tv1);
             if (any_active && stop > v)
                 scan_vectors<K, W, S>(q, rmin, tile + (v - tv0) * R, static_cast<int>(stop - v));
             v = stop;
-            while (s < s_hi && v == s_end_v) finish_set();
+            while (s < s1 && v == s_end_v) finish_set();
         }
         __syncwarp();
         if (lane == 0) {
@@ -618,7 +649,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, DSRT_ALL_MINB)
             }
         }
     }
-    while (s < s_hi) finish_set();  // trailing empty sets (validated away upstream)
+    while (s < s1) finish_set();  // trailing empty sets (validated away upstream)
     if (any_active && nslot > 0) flush_all();
     if constexpr (CL > 1) {
         __syncwarp();
@@ -919,6 +950,11 @@ static int launch_all(const uint32_t *recs, const int64_t *set_off, int64_t sb, 
     int64_t chunks = (waves * sm_count() * occ + groups - 1) / groups;
     chunks = tmax<int64_t>(1, tmin<int64_t>(chunks, (nset + 63) / 64));
     chunks = tmin<int64_t>(chunks, 65535);
+    // the consumers index a chunk's sets and vectors with 32-bit relative offsets: chunks are cut
+    // by equal vector counts and a set has <= 65535 vectors, so <= 32767 sets per chunk on
+    // average keeps every chunk below 2^31 vectors (and sets)
+    chunks = tmax<int64_t>(chunks, (nset + 32766) / 32767);
+    DSRT_REQUIRE(chunks <= 65535, DSRT_EUNSUPPORTED, "invalid parameter: too many sets for one scoring launch");
     dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(chunks));
     DSRT_REQUIRE(groups < (1LL << 31), DSRT_EUNSUPPORTED, "invalid parameter: too many query sets");
     if (pair) {
